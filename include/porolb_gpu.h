@@ -1,0 +1,279 @@
+/*
+ * porolb_gpu.h -- C ABI of libporolb_cuda.so, the B200 (sm_100a) drop-in for
+ * the reference solver's time-step path (porolb::Simulation and its setup).
+ *
+ * Reference interfaces replaced (paths relative to the reference's proj/):
+ *   pgpu_relaxation_from_magic   lattice.hpp:42-44,   lattice.cpp:58-75
+ *   pgpu_voxelize / _slab        geometry.hpp:76-81,  geometry.cpp:491-632
+ *   pgpu_make_box_geometry       geometry.hpp:83-84,  geometry.cpp:634-640
+ *   pgpu_create                  simulation.hpp:55,   simulation.cpp:80-102
+ *   pgpu_set_body_force          simulation.hpp:57
+ *   pgpu_set_lid_velocity        simulation.hpp:60-61, simulation.cpp:104-112
+ *   pgpu_set_porous              simulation.hpp:63-64, simulation.cpp:114-119
+ *   pgpu_initialize_equilibrium  simulation.hpp:88-89, simulation.cpp:121-128
+ *   pgpu_step                    simulation.hpp:67,   simulation.cpp:344-352
+ *   pgpu_steps_done              simulation.hpp:68
+ *   pgpu_get_pdfs / set_pdfs     simulation.hpp:71-72 (field().cur(k)), field.hpp:48-51
+ *   pgpu_get/set_cell_populations field.hpp:53-60
+ *   pgpu_macroscopic             simulation.hpp:76-78, simulation.cpp:354-369
+ *   pgpu_macroscopic_fields      (bulk form of the above)
+ *   pgpu_planar_profile          simulation.hpp:80-83, simulation.cpp:371-417, profile.cpp:10-19
+ *   pgpu_max_speed               simulation.hpp:85-86, simulation.cpp:419-434
+ *   pgpu_cli_fallback_count      simulation.hpp:73
+ *   pgpu_fluid_cells             simulation.hpp:74
+ *   pgpu_run_to_steady_state     simulation.hpp:134-138, simulation.cpp:441-480
+ *   pgpu_kozeny_carman           glbm.hpp:40-46,      glbm.cpp:90-111
+ *   pgpu_make_glbm_params        simulation.hpp:31-36, simulation.cpp:23-50
+ *   pgpu_glbm_force_and_velocity simulation.hpp:38-43, simulation.cpp:52-66
+ *   pgpu_equilibrium / trt_collide lattice.hpp:46-61, lattice.cpp:77-128
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; every input array is COPIED by the callee,
+ *    the caller keeps ownership (reference ctor deep-copies, simulation.cpp:80-91).
+ *  - Layouts are the reference's: cell c = (z*ny + y)*nx + x (field.hpp:19-21),
+ *    PDF slot f[k*cells + c] (field.hpp:36-37,48-51), fluctuation form.
+ *  - Every call returns a status: PGPU_OK, or the code of the reference
+ *    exception it replaces (errors.hpp:9-21); pgpu_last_error() holds the
+ *    message (thread-local).  The C++ wrapper include/porolb_gpu/porolb_gpu.hpp
+ *    rethrows the reference exception types.
+ *  - A simulation handle is not thread-safe (same as the reference object).
+ *  - There is no CPU fallback: without a usable sm_100 device pgpu_create
+ *    fails with PGPU_ERR_CUDA.
+ */
+#ifndef POROLB_GPU_H
+#define POROLB_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGPU_ABI_VERSION 1
+
+enum pgpu_status {
+  PGPU_OK = 0,
+  PGPU_ERR_CONFIG = 1,      /* porolb::ConfigError */
+  PGPU_ERR_INSTABILITY = 2, /* porolb::NumericalInstability */
+  PGPU_ERR_GEOMETRY = 3,    /* porolb::GeometryError */
+  PGPU_ERR_CUDA = 4,        /* device / driver failure (no reference analogue) */
+  PGPU_ERR_INTERNAL = 5     /* invalid argument or other std::exception */
+};
+
+enum pgpu_wall_scheme { PGPU_SBB = 0, PGPU_CLI = 1 }; /* boundary.hpp:12 */
+enum pgpu_glbm_viscosity { PGPU_VISC_PLAIN = 0, PGPU_VISC_RESCALED = 1, PGPU_VISC_CONSTANT_RATIO = 2 };
+
+typedef struct pgpu_sim pgpu_sim;
+typedef struct pgpu_voxel_geometry pgpu_voxel_geometry;
+
+/* FluidParams, lattice.hpp:32-39 */
+typedef struct {
+  double nu;
+  double omega_plus;
+  double omega_minus;
+  double lambda_magic;
+  double rho0;
+  double body_force[3];
+} pgpu_fluid_params;
+
+/* VoxelGeometry (geometry.hpp:62-73) as plain arrays; BoundaryLink
+ * (boundary.hpp:16-22) as structure-of-arrays.  n_links may be 0. */
+typedef struct {
+  int32_t dims[3];
+  uint8_t periodic[3];
+  const uint8_t* flags;          /* cells; 0 fluid, 1 solid, 2 wall */
+  int64_t n_links;
+  const int64_t* link_fluid_cell;
+  const int64_t* link_second_fluid; /* -1 when none */
+  const int32_t* link_direction;
+  const float* link_q;
+  const uint8_t* link_moving;    /* may be NULL: all false */
+  const double* porosity;        /* nz entries */
+  int64_t fluid_cells;
+  int32_t has_wall_plane_lo, has_wall_plane_hi;
+  double wall_plane_lo, wall_plane_hi;
+  /* x-slab decomposition (multi-GPU).  When slab != 0 the
+   * arrays above describe the local slab [x_offset, x_offset+dims[0]) of a
+   * global domain of global_nx cells along x, and ghost_flags_lo/hi hold the
+   * flags of the neighbouring columns x_offset-1 and x_offset+dims[0]
+   * (ny*nz each, index z*ny+y).  link_second_fluid may be -2: the second
+   * fluid cell lies in a ghost column.  periodic[0] is ignored. */
+  int32_t slab;
+  int32_t x_offset;
+  int32_t global_nx;
+  const uint8_t* ghost_flags_lo;
+  const uint8_t* ghost_flags_hi;
+} pgpu_geometry;
+
+/* SteadyConfig (simulation.hpp:118-123) */
+typedef struct {
+  double tolerance;
+  int32_t check_interval;
+  int64_t max_steps;
+  double max_speed;
+} pgpu_steady_config;
+
+/* RunStats (simulation.hpp:125-132) */
+typedef struct {
+  int64_t steps;
+  double mlups;
+  double seconds;
+  int32_t converged;
+  double residual;
+  int32_t cli_fallbacks;
+} pgpu_run_stats;
+
+/* ProfileData metadata (profile.hpp:12-34); the arrays are caller-provided
+ * with capacity nz and n_planes entries are written. */
+typedef struct {
+  int32_t n_planes;
+  double u_max, height, z0, nu;
+  double body_force[3];
+  int32_t stream_axis;
+} pgpu_profile_meta;
+
+/* Sphere list (geometry.hpp:14-32) for the voxelizer. */
+typedef struct {
+  int64_t n_spheres;
+  const double* cx;
+  const double* cy;
+  const double* cz;
+  const double* radius;
+  double box[3];
+  double bottom_plate_z;
+} pgpu_sphere_pack;
+
+/* VoxelizeOptions, geometry.hpp:51-57 */
+typedef struct {
+  uint8_t periodic[3];
+  uint8_t wall_z_lo, wall_z_hi;
+  double q_clamp_min;
+} pgpu_voxelize_options;
+
+/* ---- errors / library ---------------------------------------------------- */
+const char* pgpu_last_error(void);
+int pgpu_abi_version(void);
+/* Number of visible CUDA devices (0 without a GPU; never fails). */
+int pgpu_device_count(void);
+
+/* ---- lattice-level host functions (bit-identical to the reference) -------- */
+int pgpu_relaxation_from_magic(double nu, double lambda_magic, pgpu_fluid_params* out);
+int pgpu_equilibrium(double delta_rho, const double u[3], double rho0, double out[19]);
+int pgpu_trt_collide(const double f[19], const pgpu_fluid_params* p, double out[19]);
+int pgpu_kozeny_carman(int32_t n, const double* eps, double grain_diameter,
+                       double free_threshold, double* K_out);
+int pgpu_make_glbm_params(int32_t n, const double* eps, const double* K, double c_F,
+                          double nu, double lambda_magic, int32_t viscosity_mode, double J,
+                          double* omega_plus_out, double* omega_minus_out);
+int pgpu_glbm_force_and_velocity(const double momentum[3], double eps, double K, double c_F,
+                                 const double g[3], double nu, double u_out[3],
+                                 double force_out[3]);
+
+/* ---- geometry (host, multi-threaded, bit-exact with voxelize) ------------ */
+int pgpu_voxelize(const pgpu_sphere_pack* pack, const int32_t dims[3],
+                  const pgpu_voxelize_options* opt, pgpu_voxel_geometry** out);
+/* Local x-slab [x0, x1) of the global voxelization plus ghost-column flags. */
+int pgpu_voxelize_slab(const pgpu_sphere_pack* pack, const int32_t dims[3],
+                       const pgpu_voxelize_options* opt, int32_t x0, int32_t x1,
+                       pgpu_voxel_geometry** out);
+int pgpu_make_box_geometry(const int32_t dims[3], const pgpu_voxelize_options* opt,
+                           pgpu_voxel_geometry** out);
+/* Fills a pgpu_geometry view whose arrays point into the handle (valid until
+ * pgpu_voxel_geometry_free). */
+int pgpu_voxel_geometry_view(const pgpu_voxel_geometry* g, pgpu_geometry* view,
+                             int32_t* q_fallback_count);
+void pgpu_voxel_geometry_free(pgpu_voxel_geometry* g);
+
+/* Seeded synthetic sphere lists for the benchmark configurations (the
+ * reference has no generator for them).  mode 0: random
+ * sequential addition (no overlap, min-image in periodic x/y); mode 1:
+ * Boolean model (overlap allowed).  Radii uniform in [r_min, r_max]; centres
+ * uniform in [0,lx)x[0,ly)x[z_lo,z_hi].  Stops when the analytic bed porosity
+ * (mode 0: 1 - sum V / V_bed; mode 1: exp(-sum V / V_bed)) reaches
+ * target_porosity or after max_attempts draws.  Capacity-limited output. */
+int pgpu_generate_spheres(int32_t mode, uint64_t seed, const double box[3], double z_lo,
+                          double z_hi, double r_min, double r_max, double bed_volume,
+                          double target_porosity, int64_t max_attempts, int64_t capacity,
+                          double* cx, double* cy, double* cz, double* r, int64_t* n_out,
+                          double* porosity_out);
+
+/* ---- simulation ------------------------------------------------------------ */
+int pgpu_create(const pgpu_geometry* geom, const pgpu_fluid_params* params, int32_t scheme,
+                int32_t device, pgpu_sim** out);
+int pgpu_destroy(pgpu_sim* sim);
+/* Run all device work of this simulation on `stream` (a cudaStream_t); NULL
+ * restores the simulation's own stream. */
+int pgpu_set_stream(pgpu_sim* sim, void* stream);
+int pgpu_get_stream(pgpu_sim* sim, void** stream);
+int pgpu_synchronize(pgpu_sim* sim);
+
+int pgpu_get_params(pgpu_sim* sim, pgpu_fluid_params* out);
+int pgpu_set_body_force(pgpu_sim* sim, const double g[3]);
+int pgpu_set_lid_velocity(pgpu_sim* sim, const double u[3]);
+/* GlbmPlaneParams (simulation.hpp:18-27); n must equal nz. */
+int pgpu_set_porous(pgpu_sim* sim, int32_t n, const double* eps, const double* K,
+                    const double* omega_plus, const double* omega_minus, double c_F,
+                    int32_t eps_in_equilibrium);
+int pgpu_initialize_equilibrium(pgpu_sim* sim, double delta_rho, const double u[3]);
+
+/* n time steps; asynchronous on the simulation's stream, ordered before any
+ * later read. */
+int pgpu_step(pgpu_sim* sim, int64_t n);
+int pgpu_steps_done(pgpu_sim* sim, int64_t* out);
+int pgpu_cli_fallback_count(pgpu_sim* sim, int32_t* out);
+int pgpu_fluid_cells(pgpu_sim* sim, int64_t* out);
+int pgpu_dims(pgpu_sim* sim, int32_t dims[3]);
+
+/* Pre-collision populations f(steps_done) in the reference layout
+ * (19*cells doubles).  Only fluid-cell slots are defined on output. */
+int pgpu_get_pdfs(pgpu_sim* sim, double* out);
+int pgpu_set_pdfs(pgpu_sim* sim, const double* in);
+int pgpu_get_cell_populations(pgpu_sim* sim, int64_t cell, double out[19]);
+int pgpu_set_cell_populations(pgpu_sim* sim, int64_t cell, const double in[19]);
+
+int pgpu_macroscopic(pgpu_sim* sim, int64_t cell, double* delta_rho, double u[3]);
+/* Any output may be NULL; non-fluid cells are written as 0. */
+int pgpu_macroscopic_fields(pgpu_sim* sim, double* delta_rho, double* ux, double* uy,
+                            double* uz);
+/* Arrays need nz capacity; meta->n_planes entries are written. */
+int pgpu_planar_profile(pgpu_sim* sim, int32_t stream_axis, double* z, double* u_superficial,
+                        double* u_intrinsic, double* epsilon, double* u_normalized,
+                        pgpu_profile_meta* meta);
+/* Per-plane sums of the stream-axis velocity over fluid cells, in the
+ * reference's sequential cell order (building block for multi-GPU profiles). */
+int pgpu_plane_sums(pgpu_sim* sim, int32_t stream_axis, double* sums_nz);
+int pgpu_max_speed(pgpu_sim* sim, double* out);
+/* Max of |u|^2 plus a finiteness flag (building block for multi-GPU guards). */
+int pgpu_max_speed2(pgpu_sim* sim, double* vmax2, int32_t* finite);
+
+int pgpu_run_to_steady_state(pgpu_sim* sim, const pgpu_steady_config* cfg,
+                             pgpu_run_stats* stats, double* z, double* u_superficial,
+                             double* u_intrinsic, double* epsilon, double* u_normalized,
+                             pgpu_profile_meta* meta);
+
+/* ---- instrumentation ------------------------------------------------------- */
+/* Kernels launched by this simulation so far. */
+int pgpu_launch_count(pgpu_sim* sim, int64_t* out);
+/* Bytes per step the hot kernel must move by the 304 B/fluid-cell ledger. */
+int pgpu_algorithmic_bytes_per_step(pgpu_sim* sim, double* out);
+
+/* ---- multi-GPU halo (x-slab, 5 PDFs per face) ------------------------------ */
+/* Element count of one face buffer: 5*ny*nz doubles. */
+int pgpu_halo_elems(pgpu_sim* sim, int64_t* out);
+/* Device buffers owned by the caller (e.g. torch tensors):
+ *   send_lo: values leaving through x=0      (directions 2,8,10,12,14)
+ *   send_hi: values leaving through x=nx-1   (directions 1,7,9,11,13)
+ *   recv_lo[2], recv_hi[2]: ghost columns, double-buffered by step parity. */
+int pgpu_set_halo_buffers(pgpu_sim* sim, double* send_lo, double* send_hi, double* recv_lo0,
+                          double* recv_lo1, double* recv_hi0, double* recv_hi1);
+/* Which recv parity the next kernel reads (the exchange must fill the other). */
+int pgpu_halo_parity(pgpu_sim* sim, int32_t* parity);
+/* Split step for overlap: part 0 = edge columns (fills send buffers),
+ * part 1 = interior; pgpu_step_finish advances the step counter. */
+int pgpu_step_part(pgpu_sim* sim, int32_t part);
+int pgpu_step_finish(pgpu_sim* sim);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POROLB_GPU_H */

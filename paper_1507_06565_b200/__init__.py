@@ -1,0 +1,39 @@
+"""B200-native (sm_100a) D3Q19 TRT time stepper for arXiv 1507.06565's pore-scale
+lattice Boltzmann runs: a drop-in for the reference porolb Simulation path.
+
+The compute lives in libporolb_cuda.so (CUDA kernels + C ABI,
+include/porolb_gpu.h); this package is its Python mirror of the reference API.
+"""
+from .porolb import (  # noqa: F401
+    OPPOSITE,
+    Q,
+    VELOCITIES,
+    WEIGHTS,
+    ConfigError,
+    CudaError,
+    FluidParams,
+    GeometryError,
+    GlbmPlaneParams,
+    GlbmViscosity,
+    NumericalInstability,
+    ProfileData,
+    RunStats,
+    Simulation,
+    SpherePack,
+    VoxelGeometry,
+    WallScheme,
+    device_count,
+    equilibrium,
+    generate_spheres,
+    glbm_force_and_velocity,
+    kozeny_carman,
+    make_box_geometry,
+    make_glbm_params,
+    relaxation_from_magic,
+    run_to_steady,
+    trt_collide,
+    voxelize,
+    voxelize_slab,
+)
+
+__version__ = "0.1.0"

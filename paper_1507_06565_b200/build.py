@@ -1,0 +1,96 @@
+"""In-tree build of libporolb_cuda.so (sm_100a) and the oracle libraries.
+
+    python -m paper_1507_06565_b200.build          # product library
+    python -m paper_1507_06565_b200.build --all    # + oracle/ (+ oracle/_ref when
+                                                   #   /root/reference is present)
+
+The product is compiled with nvcc for ``-gencode arch=compute_100a,code=sm_100a``
+(kernels) and g++ ``-ffp-contract=off`` (host runtime; keeps every host-side
+constant bit-identical to the reference's inline arithmetic), and linked with
+the static CUDA runtime so the .so travels to the GPU box by itself.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OBJ = PKG / "_build"
+LIB = PKG / "libporolb_cuda.so"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_INC = "/usr/local/cuda/include"
+# The image's $CXX (/opt/gcc) lacks libgomp specs; the system g++ is used.
+CXX = shutil.which("g++") or "g++"
+
+CU_SOURCES = ["kernels.cu"]
+CPP_SOURCES = ["params.cpp", "voxelize.cpp", "synth.cpp", "sim.cpp"]
+HEADERS = ["kparams.h", "kernels.h", "host_common.h"]
+
+
+def _run(cmd: list[str]) -> None:
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("build failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build_product(force: bool = False) -> Path:
+    OBJ.mkdir(exist_ok=True)
+    hdrs = [CSRC / h for h in HEADERS] + [ROOT / "include" / "porolb_gpu.h"]
+    jobs = []
+    objs = []
+    for src in CU_SOURCES:
+        o = OBJ / (Path(src).stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [CSRC / src] + hdrs):
+            jobs.append([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                         "-Xptxas", "-warn-spills", "-c", str(CSRC / src), "-o", str(o)])
+    for src in CPP_SOURCES:
+        o = OBJ / (Path(src).stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [CSRC / src] + hdrs):
+            jobs.append([CXX, "-std=c++17", "-O3", "-fPIC", "-pthread", "-ffp-contract=off",
+                         "-Wall", "-Wno-unused-function", f"-I{CUDA_INC}", "-c",
+                         str(CSRC / src), "-o", str(o)])
+    if jobs:
+        with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
+            list(ex.map(_run, jobs))
+    if force or jobs or _stale(LIB, objs):
+        _run([NVCC, *GENCODE, "-shared", "-cudart", "static", "-o", str(LIB),
+              *[str(o) for o in objs], "-Xcompiler", "-pthread"])
+    return LIB
+
+
+def build_oracle() -> None:
+    """Test infrastructure: oracle/liboracle.so always, oracle/_ref when the
+    reference sources are present (this container; the GPU box gets the
+    prebuilt files)."""
+    _run(["make", "-s", "-C", str(ROOT / "oracle"), "all"])
+    if Path("/root/reference/proj/src/simulation.cpp").exists():
+        _run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"])
+
+
+def main(argv: list[str]) -> int:
+    lib = build_product(force="--force" in argv)
+    print(lib)
+    if "--all" in argv:
+        build_oracle()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main(sys.argv[1:]))

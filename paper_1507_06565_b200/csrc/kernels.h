@@ -1,0 +1,31 @@
+// Host-callable launchers of the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "kparams.h"
+
+namespace pgpu {
+
+struct SweepConfig {
+  int op = 0;        // 0: stream+collide (K1), 1: stream only (KP)
+  int part = 0;      // 0: all cells, 1: edge columns only, 2: interior only
+  bool glbm = false;
+  bool records = false;
+  bool slab = false;
+};
+
+void launch_sweep(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+                  cudaStream_t s);
+void launch_collide_inplace(bool glbm, bool slab, const KParams& p, double* buf,
+                            cudaStream_t s);
+void launch_macro_fields(bool glbm, const KParams& p, const double* f, double* drho,
+                         double* ux, double* uy, double* uz, int* err, cudaStream_t s);
+void launch_plane_sums(const KParams& p, const double* u, double* sums, cudaStream_t s);
+void launch_max_speed2(bool glbm, const KParams& p, const double* f,
+                       unsigned long long* vmax2_bits, int* nonfinite, int* err,
+                       cudaStream_t s);
+void launch_fill_equilibrium(const KParams& p, int64_t cells, double* f, const double* feq,
+                             cudaStream_t s);
+
+}  // namespace pgpu

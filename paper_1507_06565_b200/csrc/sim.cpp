@@ -1,0 +1,1031 @@
+// C-ABI runtime of the B200 time stepper: the drop-in for porolb::Simulation
+// (reference proj/include/porolb/simulation.hpp:53-111, proj/src/simulation.cpp).
+//
+// State machine.  The reference keeps pre-collision f(n) in
+// `cur` and runs collide -> push-stream -> links per step().  The device keeps
+// either
+//   pre : buffer[cur] holds f(n)            (after construction / set / materialise)
+//   post: buffer[cur] holds g(n-1) = C(f(n-1)), and f(n) = P(g(n-1))
+// step() from pre runs K0 (collide in place) and becomes post; step() from
+// post runs K1 (fused pull-stream + bounce + collide) into the other buffer.
+// Every observable first materialises f(n) = P(g) with KP (pre again), so
+// reads always see exactly the reference's f(steps_done).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <sstream>
+#include <vector>
+
+#include "host_common.h"
+#include "kernels.h"
+#include "kparams.h"
+
+namespace pgpu {
+void moments(const double f[19], double rho0, double& drho, double u[3]);
+void equilibrium(double drho, const double u[3], double rho0, double out[19]);
+void glbm_force_and_velocity(const double mom[3], double eps, double K, double cf,
+                             const double g[3], double nu, double u[3], double force[3]);
+}  // namespace pgpu
+
+using namespace pgpu;
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e__ = (call);                                                         \
+    if (e__ != cudaSuccess) {                                                         \
+      std::ostringstream os__;                                                        \
+      os__ << #call << " failed: " << cudaGetErrorString(e__) << " (" << __FILE__ << ":" \
+           << __LINE__ << ")";                                                        \
+      throw CudaError(os__.str());                                                    \
+    }                                                                                 \
+  } while (0)
+
+struct pgpu_sim {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int nx = 0, ny = 0, nz = 0;
+  bool per[3] = {true, true, false};
+  bool slab = false;
+  int x_offset = 0, global_nx = 0;
+  int64_t cells = 0, ks = 0;
+  pgpu_fluid_params params{};
+  int scheme = PGPU_SBB;
+  std::vector<double> porosity;
+  std::vector<int64_t> plane_fluid_count;
+  bool has_lo = false, has_hi = false;
+  double lo = 0.0, hi = 0.0;
+  int64_t fluid_cells = 0;
+  int32_t cli_fallbacks = 0;
+  // link structures (host mirror)
+  std::vector<uint32_t> cellword;
+  std::vector<int32_t> link_base;
+  std::vector<LinkRec> recs;
+  int64_t n_links = 0;
+  bool any_moving = false;
+  bool records_uploaded = false;
+  double lid[3] = {0.0, 0.0, 0.0};
+  // GLBM (set_porous)
+  bool porous = false, glbm_active = false;
+  std::vector<double> eps, K, gwp, gwm;
+  double cf = 0.0;
+  bool eps_in_eq = true;
+  // device memory
+  double* f[2] = {nullptr, nullptr};
+  uint32_t* d_cellword = nullptr;
+  int32_t* d_base = nullptr;
+  LinkRec* d_recs = nullptr;
+  PlaneCoef* d_planes = nullptr;
+  double* d_feq = nullptr;
+  int* d_flags = nullptr;  // [0] err, [1] nonfinite
+  unsigned long long* d_vmax = nullptr;
+  double* d_sums = nullptr;
+  // state
+  int cur = 0;
+  bool post = false;
+  int64_t steps = 0;
+  int64_t launches = 0;
+  // halo (slab mode)
+  double* send_lo = nullptr;
+  double* send_hi = nullptr;
+  double* recv_lo[2] = {nullptr, nullptr};
+  double* recv_hi[2] = {nullptr, nullptr};
+  int ghost_cur = 0;
+  int pending = 0;  // 0 none, 1 K0 issued, 2 K1 parts issued
+  // CUDA graphs of kGraphSteps K1 launches (one per starting buffer)
+  static constexpr int kGraphSteps = 16;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  cudaStream_t graph_stream = nullptr;
+  KParams kp{};
+
+  ~pgpu_sim() {
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
+    cudaSetDevice(device);
+    for (double* p : f) cudaFree(p);
+    cudaFree(d_cellword);
+    cudaFree(d_base);
+    cudaFree(d_recs);
+    cudaFree(d_planes);
+    cudaFree(d_feq);
+    cudaFree(d_flags);
+    cudaFree(d_vmax);
+    cudaFree(d_sums);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+
+  void drop_graphs() {
+    for (auto& g : graph)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+  }
+
+  int plane_of(int64_t c) const { return static_cast<int>(c / ((int64_t)nx * ny)); }
+
+  // ---- derived constants (host, reference operation order) ----------------
+  void refresh_params() {
+    const double* g = params.body_force;
+    const double rho0 = params.rho0;
+    kp.wp = params.omega_plus;
+    kp.wm = params.omega_minus;
+    kp.rho0 = rho0;
+    kp.nu = params.nu;
+    kp.cf = cf;
+    for (int q = 0; q < 9; ++q) {
+      const int k = 1 + 2 * q;
+      const double w = weight(k);
+      // simulation.cpp:183,185,190
+      const double eg = static_cast<double>(kE[k][0]) * g[0] +
+                        static_cast<double>(kE[k][1]) * g[1] +
+                        static_cast<double>(kE[k][2]) * g[2];
+      kp.fpop[q] = 3.0 * w * rho0 * eg;
+      kp.wr3[q] = w * rho0 * 3.0;
+    }
+    for (int k = 0; k < 19; ++k) {
+      // boundary.cpp:38-40 with m.inv_cs2 = 3.0
+      const double eu = kE[k][0] * lid[0] + kE[k][1] * lid[1] + kE[k][2] * lid[2];
+      kp.mw[k] = 2.0 * weight(k) * rho0 * 3.0 * eu;
+    }
+    for (int i = 0; i < 3; ++i) {
+      kp.hg[i] = 0.5 * g[i] / rho0;  // simulation.cpp:367
+      kp.g[i] = g[i];
+    }
+    if (porous) upload_planes();
+    drop_graphs();
+  }
+
+  void upload_planes() {
+    const double* g = params.body_force;
+    const double rho0 = params.rho0, nu = params.nu;
+    std::vector<PlaneCoef> pc(nz);
+    for (int z = 0; z < nz; ++z) {
+      PlaneCoef& c = pc[z];
+      const double e = eps[z], k = K[z];
+      c.eps = e;
+      c.K = k;
+      c.wp = gwp[z];
+      c.wm = gwm[z];
+      c.eq_eps = eps_in_eq ? e : 1.0;  // simulation.cpp:218
+      for (int i = 0; i < 3; ++i) {
+        c.half_eps_g[i] = 0.5 * e * g[i];  // :233-235
+        c.eps_g[i] = e * g[i];             // :248-250
+      }
+      c.c0 = 0.5 * (1.0 + e * nu / (2.0 * k));  // :236
+      c.denom_lin = 2.0 * c.c0;                 // :239
+      c.c1 = 0.5 * e * cf / std::sqrt(k);       // :241 and simulation.cpp:58
+      c.drag_lin = e * nu / k;                  // :247
+      c.drag_lin0 = c.drag_lin + 0.0;           // :247 with c_F == 0
+      c.drag_q = e * cf / std::sqrt(k);         // :247
+      c.force_pref = (1.0 - 0.5 * c.wm) * 3.0 * rho0;  // :253
+    }
+    if (!d_planes) CK(cudaMalloc(&d_planes, sizeof(PlaneCoef) * nz));
+    CK(cudaMemcpyAsync(d_planes, pc.data(), sizeof(PlaneCoef) * nz, cudaMemcpyHostToDevice,
+                       stream));
+    CK(cudaStreamSynchronize(stream));
+    kp.planes = d_planes;
+  }
+
+  bool records_needed() const { return scheme == PGPU_CLI || any_moving; }
+
+  void upload_records() {
+    if (n_links == 0) {
+      records_uploaded = true;
+      return;
+    }
+    if (!d_base) CK(cudaMalloc(&d_base, sizeof(int32_t) * cells));
+    if (!d_recs) CK(cudaMalloc(&d_recs, sizeof(LinkRec) * n_links));
+    CK(cudaMemcpyAsync(d_base, link_base.data(), sizeof(int32_t) * cells, cudaMemcpyHostToDevice,
+                       stream));
+    CK(cudaMemcpyAsync(d_recs, recs.data(), sizeof(LinkRec) * n_links, cudaMemcpyHostToDevice,
+                       stream));
+    CK(cudaStreamSynchronize(stream));
+    kp.link_base = d_base;
+    kp.links = d_recs;
+    records_uploaded = true;
+    drop_graphs();
+  }
+
+  SweepConfig sweep_cfg(int op, int part) const {
+    SweepConfig c;
+    c.op = op;
+    c.part = part;
+    c.glbm = glbm_active;
+    c.records = records_needed() && n_links > 0;
+    c.slab = slab;
+    return c;
+  }
+
+  void set_ghost_ptrs() {
+    if (!slab) return;
+    kp.ghost_lo = recv_lo[ghost_cur];
+    kp.ghost_hi = recv_hi[ghost_cur];
+    kp.send_lo = send_lo;
+    kp.send_hi = send_hi;
+  }
+
+  void check_launch() { CK(cudaGetLastError()); }
+
+  // ---- state transitions -----------------------------------------------------
+  void k0() {
+    set_ghost_ptrs();
+    launch_collide_inplace(glbm_active, slab, kp, f[cur], stream);
+    check_launch();
+    ++launches;
+  }
+  void k1(int part) {
+    set_ghost_ptrs();
+    launch_sweep(sweep_cfg(0, part), kp, f[cur], f[1 - cur], stream);
+    check_launch();
+    ++launches;
+  }
+  void ensure_pre() {
+    if (!post) return;
+    if (slab && pending) throw ConfigError("observable requested in the middle of a split step");
+    set_ghost_ptrs();
+    launch_sweep(sweep_cfg(1, 0), kp, f[cur], f[1 - cur], stream);
+    check_launch();
+    ++launches;
+    cur = 1 - cur;
+    post = false;
+  }
+
+  void build_graph(int start) {
+    // kGraphSteps ping-pong K1 launches; ends on the starting buffer.
+    cudaStream_t cs = stream;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int c = start;
+    for (int i = 0; i < kGraphSteps; ++i) {
+      launch_sweep(sweep_cfg(0, 0), kp, f[c], f[1 - c], cs);
+      c = 1 - c;
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(cs, &g);
+    if (e != cudaSuccess) throw CudaError(std::string("graph capture failed: ") + cudaGetErrorString(e));
+    CK(cudaGraphInstantiate(&graph[start], g, 0));
+    cudaGraphDestroy(g);
+    graph_stream = cs;
+  }
+
+  void step(int64_t n) {
+    if (slab) throw ConfigError("slab simulations step through pgpu_step_part + halo exchange");
+    if (records_needed() && !records_uploaded) upload_records();
+    for (int64_t i = 0; i < n;) {
+      if (!post) {
+        k0();
+        post = true;
+        ++steps;
+        ++i;
+        continue;
+      }
+      if (n - i >= kGraphSteps) {
+        if (graph_stream != stream) drop_graphs();
+        if (!graph[cur]) build_graph(cur);
+        CK(cudaGraphLaunch(graph[cur], stream));
+        launches += kGraphSteps;
+        steps += kGraphSteps;
+        i += kGraphSteps;
+        continue;
+      }
+      k1(0);
+      cur = 1 - cur;
+      ++steps;
+      ++i;
+    }
+  }
+
+  // ---- observables -------------------------------------------------------------
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+
+  void reset_flags() { CK(cudaMemsetAsync(d_flags, 0, sizeof(int) * 2, stream)); }
+
+  void check_err_flag() {
+    int h[2];
+    CK(cudaMemcpyAsync(h, d_flags, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (h[0]) throw NumericalInstability("negative discriminant in drag velocity solve");
+  }
+
+  void plane_sums(int axis, std::vector<double>& sums) {
+    if (axis < 0 || axis > 2) throw ConfigError("stream axis must be 0, 1 or 2");
+    ensure_pre();
+    reset_flags();
+    double* u = f[1 - cur];  // dead buffer in the pre state
+    launch_macro_fields(glbm_active, kp, f[cur], nullptr, axis == 0 ? u : nullptr,
+                        axis == 1 ? u : nullptr, axis == 2 ? u : nullptr, d_flags, stream);
+    check_launch();
+    launch_plane_sums(kp, u, d_sums, stream);
+    check_launch();
+    launches += 2;
+    sums.resize(nz);
+    CK(cudaMemcpyAsync(sums.data(), d_sums, sizeof(double) * nz, cudaMemcpyDeviceToHost, stream));
+    check_err_flag();
+  }
+
+  // simulation.cpp:371-417 + profile.cpp:10-19
+  void planar_profile(int axis, double* z_out, double* u_sup, double* u_int, double* eps_out,
+                      double* u_norm, pgpu_profile_meta* meta) {
+    int z_lo = nz, z_hi = -1;
+    for (int z = 0; z < nz; ++z)
+      if (plane_fluid_count[z] > 0) {
+        z_lo = std::min(z_lo, z);
+        z_hi = std::max(z_hi, z);
+      }
+    meta->n_planes = 0;
+    meta->u_max = 0.0;
+    meta->stream_axis = axis;
+    meta->nu = params.nu;
+    for (int i = 0; i < 3; ++i) meta->body_force[i] = params.body_force[i];
+    if (has_lo && has_hi) {
+      meta->z0 = lo;
+      meta->height = hi - lo;
+    } else {
+      meta->z0 = 0.0;
+      meta->height = nz;
+    }
+    if (z_hi < 0) return;
+    std::vector<double> sums;
+    plane_sums(axis, sums);
+    const int64_t plane = (int64_t)nx * ny;
+    for (int z = z_lo; z <= z_hi; ++z) {
+      const int i = z - z_lo;
+      z_out[i] = z + 0.5;
+      u_sup[i] = sums[z] / static_cast<double>(plane);
+      u_int[i] = plane_fluid_count[z] > 0 ? sums[z] / static_cast<double>(plane_fluid_count[z]) : 0.0;
+      eps_out[i] = porosity[z];
+    }
+    const int n = z_hi - z_lo + 1;
+    meta->n_planes = n;
+    double u_max = 0.0;
+    for (int i = 0; i < n; ++i)
+      if (std::abs(u_sup[i]) > std::abs(u_max)) u_max = u_sup[i];
+    for (int i = 0; i < n; ++i) u_norm[i] = (u_max != 0.0) ? u_sup[i] / u_max : 0.0;
+    meta->u_max = u_max;
+  }
+
+  void max_speed2(double& vmax2, bool& finite) {
+    ensure_pre();
+    reset_flags();
+    CK(cudaMemsetAsync(d_vmax, 0, sizeof(unsigned long long), stream));
+    launch_max_speed2(glbm_active, kp, f[cur], d_vmax, d_flags + 1, d_flags, stream);
+    check_launch();
+    ++launches;
+    unsigned long long bits = 0;
+    CK(cudaMemcpyAsync(&bits, d_vmax, sizeof(bits), cudaMemcpyDeviceToHost, stream));
+    int h[2];
+    CK(cudaMemcpyAsync(h, d_flags, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (h[0]) throw NumericalInstability("negative discriminant in drag velocity solve");
+    std::memcpy(&vmax2, &bits, sizeof(double));
+    finite = h[1] == 0;
+  }
+
+  double max_speed() {
+    double v2;
+    bool fin;
+    max_speed2(v2, fin);
+    if (!fin) return std::numeric_limits<double>::quiet_NaN();
+    return std::sqrt(v2);
+  }
+
+  void get_cell(int64_t cell, double out[19]) {
+    if (cell < 0 || cell >= cells) throw ConfigError("cell index out of range");
+    ensure_pre();
+    CK(cudaMemcpy2DAsync(out, sizeof(double), f[cur] + cell, ks * sizeof(double), sizeof(double),
+                         19, cudaMemcpyDeviceToHost, stream));
+    sync();
+  }
+
+  // simulation.cpp:354-369
+  void macroscopic(int64_t cell, double& drho, double u[3]) {
+    double fk[19], v[3];
+    get_cell(cell, fk);
+    moments(fk, params.rho0, drho, v);
+    if (glbm_active) {
+      const int z = plane_of(cell);
+      double force[3];
+      glbm_force_and_velocity(v, eps[z], K[z], cf, params.body_force, params.nu, u, force);
+    } else {
+      for (int i = 0; i < 3; ++i) u[i] = v[i] + 0.5 * params.body_force[i] / params.rho0;
+    }
+  }
+};
+
+namespace {
+
+inline int wrap(int v, int n, bool periodic) {
+  if (v >= 0 && v < n) return v;
+  if (!periodic) return -1;
+  return (v % n + n) % n;
+}
+
+void build_links(pgpu_sim* s, const pgpu_geometry* g) {
+  const int nx = s->nx, ny = s->ny, nz = s->nz;
+  const uint8_t* flags = g->flags;
+  // cellword: bit0 non-fluid; bit j: upstream x - e_j is non-fluid or outside
+  s->cellword.assign(s->cells, 0);
+  parallel_for(nz, [&](int64_t za, int64_t zb, int) {
+    for (int z = (int)za; z < (int)zb; ++z)
+      for (int y = 0; y < ny; ++y)
+        for (int x = 0; x < nx; ++x) {
+          const int64_t c = ((int64_t)z * ny + y) * nx + x;
+          if (flags[c] != 0) {
+            s->cellword[c] = 1u;
+            continue;
+          }
+          uint32_t w = 0;
+          for (int j = 1; j < 19; ++j) {
+            const int ys = wrap(y - kE[j][1], ny, s->per[1]);
+            const int zs = wrap(z - kE[j][2], nz, s->per[2]);
+            bool nonfluid;
+            if (ys < 0 || zs < 0) {
+              nonfluid = true;
+            } else {
+              const int xr = x - kE[j][0];
+              if (s->slab && xr < 0) {
+                nonfluid = g->ghost_flags_lo[(int64_t)zs * ny + ys] != 0;
+              } else if (s->slab && xr >= nx) {
+                nonfluid = g->ghost_flags_hi[(int64_t)zs * ny + ys] != 0;
+              } else {
+                const int xs = s->slab ? xr : wrap(xr, nx, s->per[0]);
+                nonfluid = xs < 0 || flags[((int64_t)zs * ny + ys) * nx + xs] != 0;
+              }
+            }
+            if (nonfluid) w |= 1u << j;
+          }
+          s->cellword[c] = w;
+        }
+  });
+  // per-cell record base (exclusive prefix of bounce counts)
+  s->link_base.assign(s->cells, 0);
+  int64_t total = 0;
+  for (int64_t c = 0; c < s->cells; ++c) {
+    s->link_base[c] = (int32_t)total;
+    const uint32_t w = s->cellword[c];
+    if (!(w & 1u)) total += __builtin_popcount(w);
+  }
+  if (total > std::numeric_limits<int32_t>::max()) throw ConfigError("too many boundary links");
+  if (g->n_links != total) {
+    std::ostringstream os;
+    os << "boundary links (" << g->n_links << ") do not match the fluid->non-fluid lattice "
+       << "directions of the flag field (" << total << "); links must close exactly those directions";
+    throw ConfigError(os.str());
+  }
+  s->n_links = total;
+  s->recs.assign(total, LinkRec{0.5f, kLinkSBB});
+  std::vector<uint8_t> seen(total, 0);
+  s->any_moving = false;
+  s->cli_fallbacks = 0;
+  for (int64_t i = 0; i < g->n_links; ++i) {
+    const int64_t c = g->link_fluid_cell[i];
+    const int k = g->link_direction[i];
+    if (c < 0 || c >= s->cells || flags[c] != 0) throw ConfigError("boundary link on a non-fluid or out-of-range cell");
+    if (k < 1 || k > 18) throw ConfigError("boundary link direction must be in 1..18");
+    const int j = opposite(k);
+    const uint32_t w = s->cellword[c];
+    if (!((w >> j) & 1u)) throw ConfigError("boundary link points to a fluid neighbour");
+    const int64_t r = s->link_base[c] + __builtin_popcount(w & ((1u << j) - 1u) & ~1u);
+    if (seen[r]) throw ConfigError("duplicate boundary link");
+    seen[r] = 1;
+    LinkRec rec{g->link_q[i], kLinkSBB};
+    const int64_t sf = g->link_second_fluid[i];
+    const bool moving = g->link_moving && g->link_moving[i];
+    if (s->scheme == PGPU_CLI && sf == -1) ++s->cli_fallbacks;  // simulation.cpp:97-101
+    if (moving) {
+      rec.kind = kLinkMoving;
+      s->any_moving = true;
+    } else if (s->scheme == PGPU_CLI && sf != -1) {
+      // second_fluid must be the upstream cell x - e_k, which is then fluid
+      if ((w >> k) & 1u) throw ConfigError("CLI second_fluid is not a fluid cell");
+      const int x = (int)(c % nx), y = (int)((c / nx) % ny), z = (int)(c / ((int64_t)nx * ny));
+      const int xr = x - kE[k][0];
+      const int ys = wrap(y - kE[k][1], ny, s->per[1]);
+      const int zs = wrap(z - kE[k][2], nz, s->per[2]);
+      bool ok;
+      if (s->slab && (xr < 0 || xr >= nx)) {
+        ok = sf == -2;
+      } else {
+        const int xs = s->slab ? xr : wrap(xr, nx, s->per[0]);
+        ok = sf == ((int64_t)zs * ny + ys) * nx + xs;
+      }
+      if (!ok) throw ConfigError("CLI second_fluid must be the cell x_f1 - e_k");
+      rec.kind = kLinkCLI;
+    }
+    s->recs[r] = rec;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int pgpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t scheme,
+                int32_t device, pgpu_sim** out) {
+  return guard([&] {
+    if (!g || !params || !out) throw std::invalid_argument("null pointer");
+    *out = nullptr;
+    if (g->dims[0] <= 0 || g->dims[1] <= 0 || g->dims[2] <= 0) throw ConfigError("voxel dims must be positive");
+    if (!g->flags || !g->porosity) throw std::invalid_argument("geometry needs flags and porosity");
+    if (g->n_links < 0 || (g->n_links > 0 && (!g->link_fluid_cell || !g->link_second_fluid ||
+                                              !g->link_direction || !g->link_q)))
+      throw std::invalid_argument("bad link arrays");
+    if (scheme != PGPU_SBB && scheme != PGPU_CLI) throw ConfigError("unknown wall scheme");
+    if (g->slab && (!g->ghost_flags_lo || !g->ghost_flags_hi)) throw ConfigError("slab geometry needs ghost flags");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw CudaError("no CUDA device available: the B200 path has no CPU fallback");
+    }
+    if (device < 0 || device >= ndev) throw CudaError("device index out of range");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+      std::ostringstream os;
+      os << "device " << device << " is sm_" << prop.major << prop.minor
+         << "; this library is built for sm_100a (B200) only";
+      throw CudaError(os.str());
+    }
+    std::unique_ptr<pgpu_sim> s(new pgpu_sim());
+    s->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
+    s->stream = s->own_stream;
+    s->nx = g->dims[0];
+    s->ny = g->dims[1];
+    s->nz = g->dims[2];
+    for (int a = 0; a < 3; ++a) s->per[a] = g->periodic[a] != 0;
+    s->slab = g->slab != 0;
+    s->x_offset = g->x_offset;
+    s->global_nx = g->slab ? g->global_nx : g->dims[0];
+    s->cells = (int64_t)s->nx * s->ny * s->nz;
+    if (s->cells > (int64_t)std::numeric_limits<int32_t>::max()) throw ConfigError("domain too large for one device");
+    s->ks = (s->cells + 31) / 32 * 32;
+    s->params = *params;
+    s->scheme = scheme;
+    s->porosity.assign(g->porosity, g->porosity + s->nz);
+    s->plane_fluid_count.assign(s->nz, 0);
+    for (int z = 0; z < s->nz; ++z)  // simulation.cpp:93-96
+      s->plane_fluid_count[z] = static_cast<int64_t>(
+          std::llround(s->porosity[z] * static_cast<double>(s->nx) * s->ny));
+    s->has_lo = g->has_wall_plane_lo != 0;
+    s->has_hi = g->has_wall_plane_hi != 0;
+    s->lo = g->wall_plane_lo;
+    s->hi = g->wall_plane_hi;
+    s->fluid_cells = g->fluid_cells;
+    build_links(s.get(), g);
+
+    // device buffers: two full PDF grids, zero-filled like the reference
+    const size_t fbytes = sizeof(double) * 19 * (size_t)s->ks;
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaMalloc(&s->f[b], fbytes));
+      CK(cudaMemsetAsync(s->f[b], 0, fbytes, s->stream));
+    }
+    CK(cudaMalloc(&s->d_cellword, sizeof(uint32_t) * s->cells));
+    CK(cudaMemcpyAsync(s->d_cellword, s->cellword.data(), sizeof(uint32_t) * s->cells,
+                       cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMalloc(&s->d_feq, sizeof(double) * 19));
+    CK(cudaMalloc(&s->d_flags, sizeof(int) * 2));
+    CK(cudaMalloc(&s->d_vmax, sizeof(unsigned long long)));
+    CK(cudaMalloc(&s->d_sums, sizeof(double) * s->nz));
+    KParams& kp = s->kp;
+    kp.nx = s->nx;
+    kp.ny = s->ny;
+    kp.nz = s->nz;
+    kp.px = s->per[0];
+    kp.py = s->per[1];
+    kp.pz = s->per[2];
+    kp.ks = s->ks;
+    kp.cellword = s->d_cellword;
+    s->refresh_params();
+    if (s->records_needed()) s->upload_records();
+    CK(cudaStreamSynchronize(s->stream));
+    *out = s.release();
+  });
+}
+
+int pgpu_destroy(pgpu_sim* sim) {
+  return guard([&] { delete sim; });
+}
+
+#define SIM_CHECK() \
+  if (!sim) throw std::invalid_argument("null simulation handle"); \
+  CK(cudaSetDevice(sim->device))
+
+int pgpu_set_stream(pgpu_sim* sim, void* stream) {
+  return guard([&] {
+    SIM_CHECK();
+    CK(cudaStreamSynchronize(sim->stream));
+    sim->stream = stream ? static_cast<cudaStream_t>(stream) : sim->own_stream;
+    sim->drop_graphs();
+  });
+}
+
+int pgpu_get_stream(pgpu_sim* sim, void** stream) {
+  return guard([&] {
+    SIM_CHECK();
+    *stream = sim->stream;
+  });
+}
+
+int pgpu_synchronize(pgpu_sim* sim) {
+  return guard([&] {
+    SIM_CHECK();
+    sim->sync();
+  });
+}
+
+int pgpu_get_params(pgpu_sim* sim, pgpu_fluid_params* out) {
+  return guard([&] {
+    SIM_CHECK();
+    *out = sim->params;
+  });
+}
+
+int pgpu_set_body_force(pgpu_sim* sim, const double g[3]) {
+  return guard([&] {
+    SIM_CHECK();
+    sim->sync();
+    for (int i = 0; i < 3; ++i) sim->params.body_force[i] = g[i];
+    sim->refresh_params();
+  });
+}
+
+// simulation.cpp:104-112
+int pgpu_set_lid_velocity(pgpu_sim* sim, const double u[3]) {
+  return guard([&] {
+    SIM_CHECK();
+    sim->sync();
+    for (int i = 0; i < 3; ++i) sim->lid[i] = u[i];
+    const int nx = sim->nx, ny = sim->ny, nz = sim->nz;
+    for (int64_t c = 0; c < sim->cells; ++c) {
+      const uint32_t w = sim->cellword[c];
+      if ((w & 1u) || w == 0) continue;
+      int64_t r = sim->link_base[c];
+      const int z = (int)(c / ((int64_t)nx * ny));
+      for (int j = 1; j < 19; ++j) {
+        if (!((w >> j) & 1u)) continue;
+        const int k = opposite(j);
+        if (z + kE[k][2] == nz - 1) {
+          sim->recs[r].kind = kLinkMoving;
+          sim->any_moving = true;
+        }
+        ++r;
+      }
+    }
+    sim->refresh_params();
+    if (sim->records_needed()) sim->upload_records();
+  });
+}
+
+// simulation.cpp:114-119 (+ all_free, :12-21)
+int pgpu_set_porous(pgpu_sim* sim, int32_t n, const double* eps, const double* K,
+                    const double* wp, const double* wm, double c_F, int32_t eps_in_eq) {
+  return guard([&] {
+    SIM_CHECK();
+    if (n != sim->nz) throw ConfigError("GLBM plane parameters must cover every z-plane");
+    if (!eps || !K || !wp || !wm) throw std::invalid_argument("null array");
+    sim->sync();
+    sim->porous = true;
+    sim->eps.assign(eps, eps + n);
+    sim->K.assign(K, K + n);
+    sim->gwp.assign(wp, wp + n);
+    sim->gwm.assign(wm, wm + n);
+    sim->cf = c_F;
+    sim->eps_in_eq = eps_in_eq != 0;
+    bool free = c_F == 0.0;
+    for (double e : sim->eps)
+      if (e != 1.0) free = false;
+    for (double k : sim->K)
+      if (std::isfinite(k)) free = false;
+    sim->glbm_active = !free;
+    sim->refresh_params();
+  });
+}
+
+// simulation.cpp:121-128
+int pgpu_initialize_equilibrium(pgpu_sim* sim, double delta_rho, const double u[3]) {
+  return guard([&] {
+    SIM_CHECK();
+    if (sim->slab && sim->pending) throw ConfigError("split step in progress");
+    double feq[19];
+    equilibrium(delta_rho, u, sim->params.rho0, feq);
+    if (sim->post) {  // the dead buffer becomes the pre-collision state
+      sim->cur = 1 - sim->cur;
+      sim->post = false;
+    }
+    CK(cudaMemcpyAsync(sim->d_feq, feq, sizeof(feq), cudaMemcpyHostToDevice, sim->stream));
+    launch_fill_equilibrium(sim->kp, sim->cells, sim->f[sim->cur], sim->d_feq, sim->stream);
+    sim->check_launch();
+    ++sim->launches;
+    sim->sync();
+  });
+}
+
+int pgpu_step(pgpu_sim* sim, int64_t n) {
+  return guard([&] {
+    SIM_CHECK();
+    if (n < 0) throw ConfigError("step count must be non-negative");
+    sim->step(n);
+  });
+}
+
+int pgpu_steps_done(pgpu_sim* sim, int64_t* out) {
+  return guard([&] {
+    SIM_CHECK();
+    *out = sim->steps;
+  });
+}
+
+int pgpu_cli_fallback_count(pgpu_sim* sim, int32_t* out) {
+  return guard([&] {
+    SIM_CHECK();
+    *out = sim->scheme == PGPU_CLI ? sim->cli_fallbacks : 0;
+  });
+}
+
+int pgpu_fluid_cells(pgpu_sim* sim, int64_t* out) {
+  return guard([&] {
+    SIM_CHECK();
+    *out = sim->fluid_cells;
+  });
+}
+
+int pgpu_dims(pgpu_sim* sim, int32_t dims[3]) {
+  return guard([&] {
+    SIM_CHECK();
+    dims[0] = sim->nx;
+    dims[1] = sim->ny;
+    dims[2] = sim->nz;
+  });
+}
+
+int pgpu_get_pdfs(pgpu_sim* sim, double* out) {
+  return guard([&] {
+    SIM_CHECK();
+    if (!out) throw std::invalid_argument("null output");
+    sim->ensure_pre();
+    CK(cudaMemcpy2DAsync(out, sim->cells * sizeof(double), sim->f[sim->cur],
+                         sim->ks * sizeof(double), sim->cells * sizeof(double), 19,
+                         cudaMemcpyDeviceToHost, sim->stream));
+    sim->sync();
+  });
+}
+
+int pgpu_set_pdfs(pgpu_sim* sim, const double* in) {
+  return guard([&] {
+    SIM_CHECK();
+    if (!in) throw std::invalid_argument("null input");
+    if (sim->slab && sim->pending) throw ConfigError("split step in progress");
+    sim->sync();
+    if (sim->post) sim->cur = 1 - sim->cur;
+    sim->post = false;
+    CK(cudaMemcpy2DAsync(sim->f[sim->cur], sim->ks * sizeof(double), in,
+                         sim->cells * sizeof(double), sim->cells * sizeof(double), 19,
+                         cudaMemcpyHostToDevice, sim->stream));
+    sim->sync();
+  });
+}
+
+int pgpu_get_cell_populations(pgpu_sim* sim, int64_t cell, double out[19]) {
+  return guard([&] {
+    SIM_CHECK();
+    sim->get_cell(cell, out);
+  });
+}
+
+int pgpu_set_cell_populations(pgpu_sim* sim, int64_t cell, const double in[19]) {
+  return guard([&] {
+    SIM_CHECK();
+    if (cell < 0 || cell >= sim->cells) throw ConfigError("cell index out of range");
+    sim->ensure_pre();
+    CK(cudaMemcpy2DAsync(sim->f[sim->cur] + cell, sim->ks * sizeof(double), in, sizeof(double),
+                         sizeof(double), 19, cudaMemcpyHostToDevice, sim->stream));
+    sim->sync();
+  });
+}
+
+int pgpu_macroscopic(pgpu_sim* sim, int64_t cell, double* delta_rho, double u[3]) {
+  return guard([&] {
+    SIM_CHECK();
+    sim->macroscopic(cell, *delta_rho, u);
+  });
+}
+
+int pgpu_macroscopic_fields(pgpu_sim* sim, double* drho, double* ux, double* uy, double* uz) {
+  return guard([&] {
+    SIM_CHECK();
+    sim->ensure_pre();
+    sim->reset_flags();
+    double* scratch = sim->f[1 - sim->cur];
+    double* outs[4] = {drho, ux, uy, uz};
+    double* dev[4];
+    for (int i = 0; i < 4; ++i) dev[i] = outs[i] ? scratch + (int64_t)i * sim->ks : nullptr;
+    launch_macro_fields(sim->glbm_active, sim->kp, sim->f[sim->cur], dev[0], dev[1], dev[2],
+                        dev[3], sim->d_flags, sim->stream);
+    sim->check_launch();
+    ++sim->launches;
+    for (int i = 0; i < 4; ++i)
+      if (outs[i])
+        CK(cudaMemcpyAsync(outs[i], dev[i], sizeof(double) * sim->cells, cudaMemcpyDeviceToHost,
+                           sim->stream));
+    sim->check_err_flag();
+  });
+}
+
+int pgpu_planar_profile(pgpu_sim* sim, int32_t axis, double* z, double* u_sup, double* u_int,
+                        double* eps, double* u_norm, pgpu_profile_meta* meta) {
+  return guard([&] {
+    SIM_CHECK();
+    if (!z || !u_sup || !u_int || !eps || !u_norm || !meta) throw std::invalid_argument("null output");
+    sim->planar_profile(axis, z, u_sup, u_int, eps, u_norm, meta);
+  });
+}
+
+int pgpu_plane_sums(pgpu_sim* sim, int32_t axis, double* sums_nz) {
+  return guard([&] {
+    SIM_CHECK();
+    std::vector<double> s;
+    sim->plane_sums(axis, s);
+    std::memcpy(sums_nz, s.data(), sizeof(double) * s.size());
+  });
+}
+
+int pgpu_max_speed(pgpu_sim* sim, double* out) {
+  return guard([&] {
+    SIM_CHECK();
+    *out = sim->max_speed();
+  });
+}
+
+int pgpu_max_speed2(pgpu_sim* sim, double* vmax2, int32_t* finite) {
+  return guard([&] {
+    SIM_CHECK();
+    bool fin;
+    sim->max_speed2(*vmax2, fin);
+    *finite = fin ? 1 : 0;
+  });
+}
+
+// simulation.cpp:441-480
+int pgpu_run_to_steady_state(pgpu_sim* sim, const pgpu_steady_config* cfg,
+                             pgpu_run_stats* stats, double* z, double* u_sup, double* u_int,
+                             double* eps, double* u_norm, pgpu_profile_meta* meta) {
+  return guard([&] {
+    SIM_CHECK();
+    if (!cfg || !stats) throw std::invalid_argument("null pointer");
+    const int nz = sim->nz;
+    std::vector<double> pz(nz), ps(nz), pi(nz), pe(nz), pn(nz);
+    std::vector<double> cz(nz), cs(nz), ci(nz), ce(nz), cn(nz);
+    pgpu_profile_meta pm{}, cm{};
+    *stats = pgpu_run_stats{};
+    stats->cli_fallbacks = sim->scheme == PGPU_CLI ? sim->cli_fallbacks : 0;
+    sim->planar_profile(0, pz.data(), ps.data(), pi.data(), pe.data(), pn.data(), &pm);
+    const auto t0 = std::chrono::steady_clock::now();
+    int64_t done = 0;
+    while (done < cfg->max_steps) {
+      const int64_t burst = std::min<int64_t>(cfg->check_interval, cfg->max_steps - done);
+      sim->step(burst);
+      done += burst;
+      const double vmax = sim->max_speed();
+      if (!std::isfinite(vmax) || vmax > cfg->max_speed) {
+        std::ostringstream os;
+        os << "instability after " << done << " steps: max |u| = " << vmax;
+        throw NumericalInstability(os.str());
+      }
+      sim->planar_profile(0, cz.data(), cs.data(), ci.data(), ce.data(), cn.data(), &cm);
+      double diff = 0.0, scale = 0.0;
+      for (int i = 0; i < cm.n_planes; ++i) {
+        diff = std::max(diff, std::abs(cs[i] - ps[i]));
+        scale = std::max(scale, std::abs(cs[i]));
+      }
+      stats->residual = scale > 0.0 ? diff / scale : diff;
+      std::swap(pz, cz);
+      std::swap(ps, cs);
+      std::swap(pi, ci);
+      std::swap(pe, ce);
+      std::swap(pn, cn);
+      pm = cm;
+      if (stats->residual < cfg->tolerance) {
+        stats->converged = 1;
+        break;
+      }
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    stats->steps = done;
+    stats->seconds = std::chrono::duration<double>(t1 - t0).count();
+    stats->mlups = stats->seconds > 0.0
+                       ? static_cast<double>(sim->cells) * done / stats->seconds / 1e6
+                       : 0.0;
+    if (meta) {
+      *meta = pm;
+      for (int i = 0; i < pm.n_planes; ++i) {
+        if (z) z[i] = pz[i];
+        if (u_sup) u_sup[i] = ps[i];
+        if (u_int) u_int[i] = pi[i];
+        if (eps) eps[i] = pe[i];
+        if (u_norm) u_norm[i] = pn[i];
+      }
+    }
+  });
+}
+
+int pgpu_launch_count(pgpu_sim* sim, int64_t* out) {
+  return guard([&] {
+    SIM_CHECK();
+    *out = sim->launches;
+  });
+}
+
+int pgpu_algorithmic_bytes_per_step(pgpu_sim* sim, double* out) {
+  return guard([&] {
+    SIM_CHECK();
+    *out = 304.0 * static_cast<double>(sim->fluid_cells);
+  });
+}
+
+// ---- multi-GPU halo ---------------------------------------------------------
+int pgpu_halo_elems(pgpu_sim* sim, int64_t* out) {
+  return guard([&] {
+    SIM_CHECK();
+    *out = 5 * (int64_t)sim->ny * sim->nz;
+  });
+}
+
+int pgpu_set_halo_buffers(pgpu_sim* sim, double* send_lo, double* send_hi, double* recv_lo0,
+                          double* recv_lo1, double* recv_hi0, double* recv_hi1) {
+  return guard([&] {
+    SIM_CHECK();
+    if (!sim->slab) throw ConfigError("halo buffers need a slab geometry");
+    if (!send_lo || !send_hi || !recv_lo0 || !recv_lo1 || !recv_hi0 || !recv_hi1)
+      throw std::invalid_argument("null halo buffer");
+    sim->send_lo = send_lo;
+    sim->send_hi = send_hi;
+    sim->recv_lo[0] = recv_lo0;
+    sim->recv_lo[1] = recv_lo1;
+    sim->recv_hi[0] = recv_hi0;
+    sim->recv_hi[1] = recv_hi1;
+  });
+}
+
+int pgpu_halo_parity(pgpu_sim* sim, int32_t* parity) {
+  return guard([&] {
+    SIM_CHECK();
+    *parity = 1 - sim->ghost_cur;
+  });
+}
+
+int pgpu_step_part(pgpu_sim* sim, int32_t part) {
+  return guard([&] {
+    SIM_CHECK();
+    if (!sim->slab) throw ConfigError("split steps need a slab geometry");
+    if (!sim->send_lo) throw ConfigError("halo buffers not set");
+    if (sim->records_needed() && !sim->records_uploaded) sim->upload_records();
+    if (part == 0) {
+      if (sim->pending) throw ConfigError("previous split step not finished");
+      if (!sim->post) {
+        sim->k0();  // collide-only, fills the send buffers; no ghost reads
+        sim->pending = 1;
+      } else {
+        sim->k1(1);  // edge columns: read ghosts, fill send buffers
+        sim->pending = 2;
+      }
+    } else if (part == 1) {
+      if (!sim->pending) throw ConfigError("step part 0 must come first");
+      if (sim->pending == 2) sim->k1(2);  // interior columns
+    } else {
+      throw ConfigError("part must be 0 or 1");
+    }
+  });
+}
+
+int pgpu_step_finish(pgpu_sim* sim) {
+  return guard([&] {
+    SIM_CHECK();
+    if (!sim->pending) throw ConfigError("no split step in progress");
+    if (sim->pending == 1)
+      sim->post = true;
+    else
+      sim->cur = 1 - sim->cur;
+    sim->pending = 0;
+    sim->ghost_cur = 1 - sim->ghost_cur;
+    ++sim->steps;
+  });
+}
+
+}  // extern "C"
