@@ -1,0 +1,342 @@
+"""Benchmark: D3Q19 TRT fp64 fluid MLUPS on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--scaling weak|strong]
+    python bench.py --impl reference ...     # the reference CPU solver (oracle/_ref)
+
+Workload: config C4 (512x256x512 pore-scale bed, CLI, the largest single-GPU
+BASELINE config and the one its 1/2/4/8-GPU scaling is quoted on); N>1 runs
+one rank per GPU over an x-slab split with the 5-PDF halo (weak scaling:
+512x256x512 cells per GPU).  The 20 GB of PDFs are far larger than the 126 MB
+L2, so no flush is needed between timed steps.
+
+One JSON line on rank 0.  `value` = fluid cells x K / device time (max over
+ranks), inputs resident in HBM; `e2e` = the same metric through the C ABI
+from host buffers (geometry upload + K steps + download of f(K) and the
+profile inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM_GBS = 6650.0
+BYTES_PER_FLUID_CELL = 304  # 19 fp64 reads + 19 fp64 writes
+
+
+def hbm_peak():
+    try:
+        pk = json.loads(PEAKS_FILE.read_text())
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def ncu_traffic(config_name: str):
+    """dram bytes per launch of the hot kernel from the committed ncu capture."""
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        d = json.loads(f.read_text())
+        e = d.get(config_name)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference timing (oracle/_ref: the reference compiled from its sources)
+# ---------------------------------------------------------------------------
+def reference_cpu_run(workload, geom, steps: int, warmup: int):
+    from oracle.oracle import RefLib
+
+    ref = RefLib()
+    threads = ref.set_threads(os.cpu_count() or 1)
+    params = workload.params()
+    sim = ref.simulation(geom, params.nu, params.omega_plus, params.omega_minus,
+                         params.lambda_magic, params.body_force, int(workload.scheme))
+    gp = workload.glbm_params()
+    if gp is not None:
+        sim.set_porous(gp.eps, gp.permeability, gp.omega_plus, gp.omega_minus, 0.0, True)
+    sim.step(warmup)
+    t0 = time.perf_counter()
+    sim.step(steps)
+    dt = time.perf_counter() - t0
+    return geom.fluid_cells * steps / dt / 1e6, threads, dt
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1507_06565_b200 import configs
+
+    w = configs.ALL[args.config]()
+    geom = w.geometry()  # bit-identical to the reference voxelizer (tests/test_voxelize.py)
+    mlups, threads, dt = reference_cpu_run(w, geom, args.steps, args.warmup)
+    sample = (f"{w.name}: {args.steps} full time steps of the reference Simulation::step() "
+              f"after {args.warmup} warm-up steps, OpenMP {threads} threads")
+    line = {
+        "metric": "D3Q19 TRT fp64 fluid MLUPS", "value": mlups, "unit": "MLUPS",
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "fluid_cells": geom.fluid_cells, "cells": geom.cells,
+                   "links": geom.n_links, "scheme": w.scheme.name, **w.meta},
+        "cpu_baseline": {"value": mlups, "unit": "MLUPS", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1507_06565_b200 as pg
+    from paper_1507_06565_b200 import configs
+
+    if world > 1:
+        from paper_1507_06565_b200.dist import SlabSimulation
+
+        w = configs.c4(nx_scale=world) if (args.config == "C4" and args.scaling == "weak") \
+            else configs.ALL[args.config]()
+        sim_obj = SlabSimulation(w, rank, world, device=local)
+        sim = sim_obj.sim
+        fluid_local = sim.fluid_cells
+        stepper = sim_obj.step
+        geom = None
+    else:
+        w = configs.ALL[args.config]()
+        if args.scheme:
+            w.scheme = pg.WallScheme[args.scheme]
+            w.name += f"_{args.scheme.lower()}_override"
+        geom = w.geometry()
+        sim = configs.make_simulation(w, geom, device=local)
+        fluid_local = geom.fluid_cells
+        stepper = sim.step
+    stream = torch.cuda.Stream(device=local)
+    if world > 1:
+        sim_obj.set_stream(stream)
+    else:
+        sim.set_stream(stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        stepper(args.warmup)
+    torch.cuda.synchronize()
+    fluid_total = fluid_local
+    if dist is not None:
+        t = torch.tensor([fluid_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        fluid_total = int(t.item())
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = sim.launch_count
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        stepper(args.steps)
+        ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = sim.launch_count - launches0
+    clk = clocks.stop()
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = fluid_total * args.steps / (ms * 1e-3) / 1e6
+
+    # roofline of the hot kernel (one K1 launch per step, timed on its stream)
+    peak, peak_src = hbm_peak()
+    bytes_per_launch = BYTES_PER_FLUID_CELL * fluid_local
+    achieved = bytes_per_launch / (ms_per_step * 1e-3) / 1e9
+    traffic = ncu_traffic(w.name) if world == 1 else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_per_launch}
+
+    # e2e through the C ABI with host buffers (N=1; other ranks mirror it)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        del sim
+        torch.cuda.empty_cache()
+        e2e = e2e_run(pg, configs, w, geom, args.steps, local)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu_steps = args.cpu_steps
+            mlups, threads, dt = reference_cpu_run(w, geom, cpu_steps, 1)
+            cpu = {"value": mlups, "unit": "MLUPS", "cores": threads, "kind": "reference",
+                   "sample": f"{w.name}: {cpu_steps} time steps of the reference "
+                             f"Simulation::step() (oracle/_ref, OpenMP) after 1 warm-up step, "
+                             f"{dt:.1f} s"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "MLUPS", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "D3Q19 TRT fp64 fluid MLUPS", "value": value, "unit": "MLUPS",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": w.name, "fluid_cells": fluid_total,
+                       "cells": int(np.prod(w.dims)), "scheme": w.scheme.name,
+                       "l2": "inputs larger than L2 (2 x 19 x cells x 8 B >> 126 MB)",
+                       "parallelism": f"x-slab{world}" if world > 1 else "single", **w.meta},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "total_cell_mlups": int(np.prod(w.dims)) * args.steps / (ms * 1e-3) / 1e6,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_run(pg, configs, w, geom, steps, device):
+    """Timed: create from host geometry (H2D) + steps + f(N) and profile back (D2H)."""
+    import torch
+
+    cells = geom.cells
+    pdf_host = torch.empty(19 * cells, dtype=torch.float64, pin_memory=True).numpy()
+    h2d = (geom.flags.nbytes + geom.n_links * (8 + 8 + 4 + 4 + 1) + geom.porosity.nbytes)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sim = configs.make_simulation(w, geom, device=device)
+    sim.step(steps)
+    sim.get_pdfs(pdf_host.reshape(19, *geom.dims[::-1]))
+    prof = sim.planar_profile()
+    t1 = time.perf_counter()
+    d2h = pdf_host.nbytes + 5 * prof.z.nbytes
+    del sim
+    torch.cuda.empty_cache()
+    return {"value": geom.fluid_cells * steps / (t1 - t0) / 1e6, "unit": "MLUPS",
+            "h2d_bytes_per_step": h2d / steps, "d2h_bytes_per_step": d2h / steps,
+            "seconds": t1 - t0,
+            "what": "pgpu_create from host geometry + K steps + pgpu_get_pdfs (pinned) + "
+                    "pgpu_planar_profile"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scheme", default=None, choices=["SBB", "CLI"],
+                    help="override the config's wall scheme (experiments only)")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -9,7 +9,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libporolb_cuda.so"
+import os
+
+# PGPU_LIB selects an experiment build (paper_1507_06565_b200.build --variant=...).
+LIB_PATH = Path(os.environ.get("PGPU_LIB") or Path(__file__).resolve().parent / "libporolb_cuda.so")
 
 i32, i64, u8, u64, f32, f64 = C.c_int32, C.c_int64, C.c_uint8, C.c_uint64, C.c_float, C.c_double
 P = C.POINTER

@@ -48,8 +48,14 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build_product(force: bool = False) -> Path:
-    OBJ.mkdir(exist_ok=True)
+def build_product(force: bool = False, defines: tuple = (), lib: Path = LIB,
+                  obj: Path = OBJ) -> Path:
+    """Compile and link the product library.  `defines` (e.g. ("PGPU_POOL=64",))
+    and an alternative `lib`/`obj` path build experiment variants side by side."""
+    OBJ = obj
+    LIB = lib
+    OBJ.mkdir(parents=True, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     hdrs = [CSRC / h for h in HEADERS] + [ROOT / "include" / "porolb_gpu.h"]
     jobs = []
     objs = []
@@ -58,7 +64,7 @@ def build_product(force: bool = False) -> Path:
         objs.append(o)
         if force or _stale(o, [CSRC / src] + hdrs):
             jobs.append([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                         "-Xptxas", "-warn-spills", "-c", str(CSRC / src), "-o", str(o)])
+                         "-Xptxas", "-warn-spills", *dflags, "-c", str(CSRC / src), "-o", str(o)])
     for src in CPP_SOURCES:
         o = OBJ / (Path(src).stem + ".o")
         objs.append(o)
@@ -84,7 +90,20 @@ def build_oracle() -> None:
         _run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"])
 
 
+def build_variant(name: str, defines: tuple) -> Path:
+    """Experiment build: paper_1507_06565_b200/_variants/<name>/libporolb_cuda.so,
+    selected at run time with PGPU_LIB=<that path>."""
+    d = PKG / "_variants" / name
+    return build_product(defines=defines, lib=d / "libporolb_cuda.so", obj=d / "obj")
+
+
 def main(argv: list[str]) -> int:
+    variants = [a.split("=", 1)[1] for a in argv if a.startswith("--variant=")]
+    for v in variants:  # --variant=name:DEF1,DEF2
+        name, defs = v.split(":", 1)
+        print(build_variant(name, tuple(x for x in defs.split(",") if x)))
+    if variants:
+        return 0
     lib = build_product(force="--force" in argv)
     print(lib)
     if "--all" in argv:

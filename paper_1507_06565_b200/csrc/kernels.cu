@@ -13,7 +13,9 @@
 // so no FMA is ever contracted and the result is bit-identical to the
 // reference CPU solver (x86-64 baseline, which has no FMA).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "kparams.h"
@@ -154,93 +156,83 @@ __device__ __forceinline__ void collide_glbm(double (&fk)[19], const KParams& p,
 //   SBB    f_j(x) = g_k(x)
 //   CLI    f_j(x) = c*g_k(x - e_k) - c*g_j(x) + g_k(x),  c = (1-2q)/(1+2q)
 //   moving f_j(x) = g_k(x) - 2 w_k rho0 3 (e_k . u_w)
-// and g_k(x - e_k) is exactly the pull value of direction k at x.
+// g_k(x - e_k) is exactly the pull value of direction k at x, and g_k(x) of
+// a bounce direction is read by nobody else, so every post-collision value is
+// read exactly once per sweep: one load per direction, its address selected by
+// the cell's bounce bit.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
 template <int J, bool SLAB>
-__device__ __forceinline__ double pull(const double* __restrict__ src, int x, int y, int z,
-                                       const KParams& p) {
+__device__ __forceinline__ const double* pull_addr(const double* __restrict__ src, int x, int y,
+                                                   int z, int64_t c, const KParams& p,
+                                                   uint32_t w) {
   constexpr int ex = EX[J], ey = EY[J], ez = EZ[J];
+  if (J != 0 && ((w >> J) & 1u)) return src + (int64_t)opp(J) * p.ks + c;  // bounce: g_k(x)
   int ys = y - ey, zs = z - ez;
   if (ey == 1 && y == 0) ys = p.ny - 1;
   if (ey == -1 && y == p.ny - 1) ys = 0;
   if (ez == 1 && z == 0) zs = p.nz - 1;
   if (ez == -1 && z == p.nz - 1) zs = 0;
   int xs = x - ex;
-  const double* plane = src + (int64_t)J * p.ks;
-  if (ex == 1) {
-    if (x == 0) {
-      if (SLAB) return ldg(p.ghost_lo + (int64_t)halo_slot(J) * p.ny * p.nz + zs * p.ny + ys);
-      xs = p.nx - 1;
-    }
-  } else if (ex == -1) {
-    if (x == p.nx - 1) {
-      if (SLAB) return ldg(p.ghost_hi + (int64_t)halo_slot(J) * p.ny * p.nz + zs * p.ny + ys);
-      xs = 0;
-    }
+  if (ex == 1 && x == 0) {
+    if (SLAB) return p.ghost_lo + (int64_t)halo_slot(J) * p.ny * p.nz + zs * p.ny + ys;
+    xs = p.nx - 1;
   }
-  return ldg(plane + ((int64_t)zs * p.ny + ys) * p.nx + xs);
+  if (ex == -1 && x == p.nx - 1) {
+    if (SLAB) return p.ghost_hi + (int64_t)halo_slot(J) * p.ny * p.nz + zs * p.ny + ys;
+    xs = 0;
+  }
+  return src + (int64_t)J * p.ks + ((int64_t)zs * p.ny + ys) * p.nx + xs;
 }
 
 template <int J, bool SLAB>
-__device__ __forceinline__ void pull_all(double (&f)[19], const double* __restrict__ src, int x,
-                                         int y, int z, const KParams& p, uint32_t w) {
+__device__ __forceinline__ void load_all(double (&f)[19], const double* __restrict__ src, int x,
+                                         int y, int z, int64_t c, const KParams& p, uint32_t w) {
   if constexpr (J < 19) {
-    if (J == 0 || !((w >> J) & 1u)) f[J] = pull<J, SLAB>(src, x, y, z, p);
-    pull_all<J + 1, SLAB>(f, src, x, y, z, p, w);
+    f[J] = ldg(pull_addr<J, SLAB>(src, x, y, z, c, p, w));
+    load_all<J + 1, SLAB>(f, src, x, y, z, c, p, w);
   }
 }
 
-template <int J, bool SLAB>
-__device__ __forceinline__ void pull_all_fast(double (&f)[19], const double* __restrict__ src,
-                                              int x, int y, int z, const KParams& p) {
-  if constexpr (J < 19) {
-    f[J] = pull<J, SLAB>(src, x, y, z, p);
-    pull_all_fast<J + 1, SLAB>(f, src, x, y, z, p);
-  }
-}
-
-template <int J, bool RECORDS>
-__device__ __forceinline__ void bounce_all(double (&f)[19], const double* __restrict__ src,
-                                           int64_t c, const KParams& p, uint32_t w, int32_t base) {
+// Second phase for CLI / moving-wall links: f[J] already holds g_k(x).
+template <int J>
+__device__ __forceinline__ void links_all(double (&f)[19], const double* __restrict__ src,
+                                          int64_t c, const KParams& p, uint32_t w, int32_t base) {
   if constexpr (J < 19) {
     if ((w >> J) & 1u) {
       constexpr int K = opp(J);
-      const double gk = ldg(src + (int64_t)K * p.ks + c);  // g_k(x)
-      double v = gk;                                        // SBB, boundary.cpp:19-22
-      if (RECORDS) {
-        const int32_t r = base + __popc(w & ((1u << J) - 1u) & ~1u);
-        const LinkRec rec = p.links[r];
-        if (rec.kind == kLinkCLI) {  // boundary.cpp:24-32
-          const double q = (double)rec.q;
-          const double cc = DDIV(DSUB(1.0, DMUL(2.0, q)), DADD(1.0, DMUL(2.0, q)));
-          const double gj = ldg(src + (int64_t)J * p.ks + c);  // g_kb(x_f1)
-          v = DADD(DSUB(DMUL(cc, f[K]), DMUL(cc, gj)), gk);
-        } else if (rec.kind == kLinkMoving) {  // boundary.cpp:34-41
-          v = DSUB(gk, p.mw[K]);
+      const int32_t r = base + __popc(w & ((1u << J) - 1u) & kBounceMask);
+      const double rec = __ldg(p.links + r);
+      const double gj = ldg(src + (int64_t)J * p.ks + c);  // g_kb(x_f1), boundary.cpp:29-31
+      if (rec == rec) {
+        if (!isinf(rec)) {  // CLI, boundary.cpp:24-32: ((c*a) - (c*b)) + d
+          f[J] = DADD(DSUB(DMUL(rec, f[K]), DMUL(rec, gj)), f[J]);
+        } else {  // moving wall, boundary.cpp:34-41
+          f[J] = DSUB(f[J], p.mw[K]);
         }
-      }
-      f[J] = v;
+      }  // NaN: simple bounce-back, f[J] = g_k(x) already
     }
-    bounce_all<J + 1, RECORDS>(f, src, c, p, w, base);
+    links_all<J + 1>(f, src, c, p, w, base);
   }
 }
 
 template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __device__ __forceinline__ void sweep_cell(const KParams& p, const double* __restrict__ src,
-                                           double* __restrict__ dst, int x, int y, int z) {
+                                           double* __restrict__ dst, int x, int y, int z,
+                                           CellWord cw) {
   const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
-  const uint32_t w = __ldg(p.cellword + c);
-  if (w & 1u) return;  // solid / wall: never read, never written
-  double f[19];
-  if (w == 0u) {
-    pull_all_fast<0, SLAB>(f, src, x, y, z, p);
-  } else {
-    pull_all<0, SLAB>(f, src, x, y, z, p, w);
-    const int32_t base = RECORDS ? __ldg(p.link_base + c) : 0;
-    bounce_all<1, RECORDS>(f, src, c, p, w, base);
+  const uint32_t w = cw.w;
+  if (w & kNonFluid) {  // solid / wall: never read; optionally completes a sector
+    if (w & kFillSector) {
+#pragma unroll
+      for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, 0.0);
+    }
+    return;
   }
+  double f[19];
+  load_all<0, SLAB>(f, src, x, y, z, c, p, w);
+  if (RECORDS && (w & kBounceMask)) links_all<1>(f, src, c, p, w, cw.base);
   if (OP == OP_STREAM_COLLIDE) {
     if (GLBM)
       collide_glbm<RHO1>(f, p, z);
@@ -269,14 +261,470 @@ __device__ __forceinline__ void sweep_cell(const KParams& p, const double* __res
   }
 }
 
+__device__ __forceinline__ CellWord ld_cw(const CellWord* p) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  return CellWord{v.x, (int32_t)v.y};
+}
+
+// Each block sweeps kZPer consecutive z-planes of one (x-segment, y) column;
+// the next cell word is prefetched while the current cell is processed.
+constexpr int kZPer = 4;
+#ifndef PGPU_SWEEP_MINB
+#define PGPU_SWEEP_MINB 5
+#endif
+
 template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
-__global__ void __launch_bounds__(128) k_sweep(const KParams p, const double* __restrict__ src,
+__global__ void __launch_bounds__(128, PGPU_SWEEP_MINB) k_sweep(const KParams p, const double* __restrict__ src,
                                                double* __restrict__ dst, int part) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
+  const int y = blockIdx.y;
+  const int z0 = blockIdx.z * kZPer;
   if (x >= p.nx) return;
   if (part == PART_INTERIOR && (x == 0 || x == p.nx - 1)) return;
-  sweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z);
+  const int z1 = min(z0 + kZPer, p.nz);
+  CellWord next = ld_cw(p.cells + ((int64_t)z0 * p.ny + y) * p.nx + x);
+  for (int z = z0; z < z1; ++z) {
+    const CellWord cw = next;
+    if (z + 1 < z1) next = ld_cw(p.cells + ((int64_t)(z + 1) * p.ny + y) * p.nx + x);
+    sweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z, cw);
+  }
+}
+
+// Asynchronous-copy pipeline helpers (k_sweep_pipe / k_sweep_tile).
+constexpr int kPipeBX = 128;
+constexpr int kStages = 2;
+#ifndef PGPU_POOL
+#define PGPU_POOL 96
+#endif
+constexpr int kPool = PGPU_POOL;  // per-warp, per-stage slots for CLI / moving-wall extras
+constexpr int pipe_smem(bool records) {
+  return kStages * (19 * kPipeBX + (records ? (kPipeBX / 32) * kPool : 0)) * (int)sizeof(double);
+}
+
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int J, bool SLAB>
+__device__ __forceinline__ void issue_all(double* stage, const double* __restrict__ src, int x,
+                                          int y, int z, int64_t c, const KParams& p,
+                                          uint32_t w) {
+  if constexpr (J < 19) {
+    cp_async8(stage + J * kPipeBX, pull_addr<J, SLAB>(src, x, y, z, c, p, w));
+    issue_all<J + 1, SLAB>(stage, src, x, y, z, c, p, w);
+  }
+}
+
+// Warp-exclusive prefix sum of n; returns the warp total in *total.
+__device__ __forceinline__ int warp_excl_scan(int n, int lane, int* total) {
+  int v = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  *total = __shfl_sync(0xffffffffu, v, 31);
+  return v - n;
+}
+
+// Extras of the bounce directions of one cell (ascending j): the link record
+// and g_j(x), two pool slots per bounce direction.
+__device__ __forceinline__ void issue_extras(double* pool, const double* __restrict__ src,
+                                             int64_t c, const KParams& p, uint32_t w,
+                                             int32_t base) {
+  uint32_t m = w & kBounceMask;
+  int i = 0;
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    cp_async8(pool + 2 * i, p.links + base + i);
+    cp_async8(pool + 2 * i + 1, src + (int64_t)j * p.ks + c);
+    ++i;
+  }
+}
+
+// CLI / moving-wall closure applied in shared memory before the gather: the
+// stage slot of bounce direction j holds g_k(x) and the slot of k = opp(j)
+// holds the pull value g_k(x - e_k) (boundary.cpp:24-41, same arithmetic as
+// links_all).  Records and g_j(x) come from the pool, or directly from global
+// memory for lanes whose pool allocation overflowed.  A loop over the set
+// bits keeps the code small.
+__device__ __forceinline__ void links_smem(double* slot, const double* pool, bool from_pool,
+                                           const double* __restrict__ src, int64_t c,
+                                           const KParams& p, uint32_t w, int32_t base) {
+  uint32_t m = w & kBounceMask;
+  int i = 0;
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    const int k = (j & 1) ? j + 1 : j - 1;
+    const double rec = from_pool ? pool[2 * i] : __ldg(p.links + base + i);
+    if (rec == rec) {
+      const double gk = slot[j * kPipeBX];
+      if (!isinf(rec)) {
+        const double gj = from_pool ? pool[2 * i + 1] : __ldg(src + (int64_t)j * p.ks + c);
+        slot[j * kPipeBX] = DADD(DSUB(DMUL(rec, slot[k * kPipeBX]), DMUL(rec, gj)), gk);
+      } else {
+        slot[j * kPipeBX] = DSUB(gk, p.mw[k]);
+      }
+    }
+    ++i;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1 main sweep: asynchronous-copy pipeline.  A block owns a 128-cell x
+// segment of one (y) row and marches through `zper` consecutive z-planes.
+// While plane z is collided from shared memory, each thread's loads for plane
+// z+1 are already in flight as cp.async (LDGSTS) copies into the other stage:
+// the 19 population loads (predicated per cell, address selected by the
+// bounce bit exactly as in sweep_cell) and, for cells with CLI / moving-wall
+// links, the link records and g_j(x) into a per-warp pool allocated by a warp
+// prefix sum (cells that overflow it load those directly).  In-flight bytes
+// therefore cost no registers.  Non-fluid cells that share a 32-byte sector
+// with fluid cells write zeros so no DRAM sector is ever partially written.
+// ---------------------------------------------------------------------------
+template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+__global__ void __launch_bounds__(kPipeBX, 4)
+    k_sweep_pipe(const KParams p, const double* __restrict__ src, double* __restrict__ dst,
+                 int part, int zper) {
+  extern __shared__ double smem[];
+  const int tx = threadIdx.x;
+  const int lane = tx & 31, warp = tx >> 5;
+  const int x = blockIdx.x * kPipeBX + tx;
+  const int y = blockIdx.y;
+  const int z0 = blockIdx.z * zper;
+  const int z1 = min(z0 + zper, p.nz);
+  const bool active = x < p.nx && !(part == PART_INTERIOR && (x == 0 || x == p.nx - 1));
+  const int xx = active ? x : 0;
+  double* const main0 = smem + tx;
+  double* const pool0 = smem + 2 * 19 * kPipeBX + warp * kPool;
+  constexpr int kMainStride = 19 * kPipeBX, kPoolStride = (kPipeBX / 32) * kPool;
+  auto cidx = [&](int z) { return ((int64_t)z * p.ny + y) * p.nx + xx; };
+  const CellWord kSkip{kNonFluid, 0};
+
+  // issue plane z into stage s; returns this lane's pool offset (-1: overflow)
+  auto issue = [&](int z, int s, CellWord cw) -> int {
+    const bool fluid = !(cw.w & kNonFluid);
+    if (fluid) issue_all<0, SLAB>(main0 + s * kMainStride, src, xx, y, z, cidx(z), p, cw.w);
+    int off = 0;
+    if (RECORDS) {
+      const int n = fluid ? 2 * __popc(cw.w & kBounceMask) : 0;
+      int total;
+      off = warp_excl_scan(n, lane, &total);
+      if (n) {
+        if (off + n <= kPool)
+          issue_extras(pool0 + s * kPoolStride + off, src, cidx(z), p, cw.w, cw.base);
+        else
+          off = -1;
+      }
+    }
+    return off;
+  };
+
+  CellWord cw_cur = active ? ld_cw(p.cells + cidx(z0)) : kSkip;
+  int off_cur = issue(z0, 0, cw_cur);
+  cp_async_commit();
+  CellWord cw_next = (active && z0 + 1 < z1) ? ld_cw(p.cells + cidx(z0 + 1)) : kSkip;
+  int s = 0;
+  for (int z = z0; z < z1; ++z) {
+    int off_next = 0;
+    if (z + 1 < z1) off_next = issue(z + 1, s ^ 1, cw_next);
+    cp_async_commit();
+    const CellWord cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
+    cp_async_wait<1>();  // this thread's copies for plane z have landed
+    const uint32_t w = cw_cur.w;
+    if (w & kFillSector) {
+      const int64_t c = cidx(z);
+#pragma unroll
+      for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, 0.0);
+    } else if (!(w & kNonFluid)) {
+      double* st = main0 + s * kMainStride;
+      const int64_t c = cidx(z);
+      if (RECORDS && (w & kBounceMask))
+        links_smem(st, pool0 + s * kPoolStride + (off_cur >= 0 ? off_cur : 0), off_cur >= 0,
+                   src, c, p, w, cw_cur.base);
+      double f[19];
+#pragma unroll
+      for (int j = 0; j < 19; ++j) f[j] = st[j * kPipeBX];
+      if (OP == OP_STREAM_COLLIDE) {
+        if (GLBM)
+          collide_glbm<RHO1>(f, p, z);
+        else
+          collide_core<RHO1>(f, p);
+      }
+#pragma unroll
+      for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, f[j]);
+      if (SLAB && OP == OP_STREAM_COLLIDE) {
+        const int64_t hp = (int64_t)p.ny * p.nz;
+        const int64_t h = (int64_t)z * p.ny + y;
+        if (xx == 0) {
+          p.send_lo[0 * hp + h] = f[2];
+          p.send_lo[1 * hp + h] = f[8];
+          p.send_lo[2 * hp + h] = f[10];
+          p.send_lo[3 * hp + h] = f[12];
+          p.send_lo[4 * hp + h] = f[14];
+        }
+        if (xx == p.nx - 1) {
+          p.send_hi[0 * hp + h] = f[1];
+          p.send_hi[1 * hp + h] = f[7];
+          p.send_hi[2 * hp + h] = f[9];
+          p.send_hi[3 * hp + h] = f[11];
+          p.send_hi[4 * hp + h] = f[13];
+        }
+      }
+    }
+    cw_cur = cw_next;
+    cw_next = cw_nn;
+    off_cur = off_next;
+    s ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// K1 main sweep, tile form (default).  Each WARP owns 32 consecutive cells of
+// one x row and marches through `zper` z-planes on its own (no block
+// barriers).  For every direction plane j it copies the 36-cell source span
+// [x0-2, x0+34) of row (y-e_jy, z-e_jz) into shared memory with 16-byte
+// cp.async.cg copies (L2 -> smem, no L1 allocation), predicated per cell pair
+// by a warp ballot of the lanes whose pull needs that pair -- solid stretches
+// are not fetched.  Bounce-closure values (g_k(x), the link record, g_j(x))
+// go through a per-warp pool allocated by a warp prefix sum.  Two stages:
+// plane z+1 is in flight while plane z is collided.
+// ---------------------------------------------------------------------------
+constexpr int kTileW = 36;                  // doubles per plane span per warp
+constexpr int kTilePool = 128;              // pool slots per warp per stage
+constexpr int kTileStage = 19 * kTileW + kTilePool;  // doubles per warp per stage
+constexpr int kTileWarps = 4;               // warps per block
+constexpr int kTileSmem = 2 * kTileStage * kTileWarps * (int)sizeof(double);
+
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
+// Source row of plane J for row (y, z) (periodic wrap in y/z).
+template <int J>
+__device__ __forceinline__ int64_t src_row(int y, int z, const KParams& p) {
+  constexpr int ey = EY[J], ez = EZ[J];
+  int ys = y - ey, zs = z - ez;
+  if (ey == 1 && y == 0) ys = p.ny - 1;
+  if (ey == -1 && y == p.ny - 1) ys = 0;
+  if (ez == 1 && z == 0) zs = p.nz - 1;
+  if (ez == -1 && z == p.nz - 1) zs = 0;
+  return (int64_t)zs * p.ny + ys;
+}
+
+template <int J, bool SLAB>
+__device__ __forceinline__ void tile_issue_plane(double* tile, const double* __restrict__ src,
+                                                 int x0w, int y, int z, int lane, uint32_t need,
+                                                 const KParams& p) {
+  constexpr int ex = EX[J];
+  // ballot bit l: lane l pulls direction J, source cell x0w + l - ex (tile index l - ex + 2)
+  const unsigned m = __ballot_sync(0xffffffffu, need);
+  if (lane < kTileW / 2 && m) {
+    const int q = lane;  // pair q covers tile indices 2q, 2q+1
+    const int l0 = 2 * q - 2 + ex, l1 = l0 + 1;  // consumer lanes of the pair's cells
+    const bool needed = ((l0 >= 0 && l0 < 32) && ((m >> l0) & 1u)) ||
+                        ((l1 >= 0 && l1 < 32) && ((m >> l1) & 1u));
+    if (needed) {
+      const int64_t row = src_row<J>(y, z, p);
+      int s0 = x0w - 2 + 2 * q;  // global x of the pair's first cell
+      double* dst = tile + J * kTileW + 2 * q;
+      if (s0 >= 0 && s0 + 1 < p.nx) {
+        cp_async16(dst, src + (int64_t)J * p.ks + row * p.nx + s0);
+      } else if (!SLAB) {
+        s0 = s0 < 0 ? s0 + p.nx : s0 - p.nx;  // periodic wrap; nx is even
+        cp_async16(dst, src + (int64_t)J * p.ks + row * p.nx + s0);
+      } else {
+        // slab: the needed out-of-domain cell comes from the ghost column
+        const int64_t g = (int64_t)halo_slot(J) * p.ny * p.nz + row;
+        if (s0 < 0) {
+          if (((m >> 0) & 1u) && ex == 1) cp_async8(dst + 1, p.ghost_lo + g);  // x = -1
+        } else {
+          if (((m >> 31) & 1u) && ex == -1) cp_async8(dst, p.ghost_hi + g);   // x = nx
+        }
+      }
+    }
+  }
+}
+
+template <int J, bool SLAB>
+__device__ __forceinline__ void tile_issue_all(double* tile, const double* __restrict__ src,
+                                               int x0w, int y, int z, int lane, uint32_t w,
+                                               const KParams& p) {
+  if constexpr (J < 19) {
+    const bool need = !(w & kNonFluid) && (J == 0 || !((w >> J) & 1u));
+    tile_issue_plane<J, SLAB>(tile, src, x0w, y, z, lane, need, p);
+    tile_issue_all<J + 1, SLAB>(tile, src, x0w, y, z, lane, w, p);
+  }
+}
+
+// Pool layout per bounce direction (ascending j): g_k(x) [, record, g_j(x)].
+template <bool RECORDS>
+__device__ __forceinline__ void tile_issue_bounce(double* pool, const double* __restrict__ src,
+                                                  int64_t c, const KParams& p, uint32_t w,
+                                                  int32_t base) {
+  uint32_t m = w & kBounceMask;
+  int i = 0;
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    const int k = (j & 1) ? j + 1 : j - 1;
+    if (RECORDS) {
+      cp_async8(pool + 3 * i, src + (int64_t)k * p.ks + c);
+      cp_async8(pool + 3 * i + 1, p.links + base + i);
+      cp_async8(pool + 3 * i + 2, src + (int64_t)j * p.ks + c);
+    } else {
+      cp_async8(pool + i, src + (int64_t)k * p.ks + c);
+    }
+    ++i;
+  }
+}
+
+template <int J, bool RECORDS>
+__device__ __forceinline__ void tile_gather(double (&f)[19], const double* tile,
+                                            const double* pool, int lane, uint32_t w,
+                                            const KParams& p, int i) {
+  if constexpr (J < 19) {
+    constexpr int ex = EX[J];
+    if (J != 0 && ((w >> J) & 1u)) {
+      constexpr int K = opp(J);
+      if (RECORDS) {
+        const double gk = pool[3 * i], rec = pool[3 * i + 1];
+        double v = gk;  // SBB (NaN record)
+        if (rec == rec) {
+          if (!isinf(rec))
+            v = DADD(DSUB(DMUL(rec, f[K]), DMUL(rec, pool[3 * i + 2])), gk);  // CLI
+          else
+            v = DSUB(gk, p.mw[K]);  // moving wall
+        }
+        f[J] = v;
+      } else {
+        f[J] = pool[i];
+      }
+      ++i;
+    } else {
+      f[J] = tile[J * kTileW + lane - ex + 2];
+    }
+    tile_gather<J + 1, RECORDS>(f, tile, pool, lane, w, p, i);
+  }
+}
+
+template <int J, bool SLAB>
+__device__ __forceinline__ void direct_bounce(double (&f)[19], const double* __restrict__ src,
+                                              int64_t c, const KParams& p, uint32_t w) {
+  if constexpr (J < 19) {
+    if ((w >> J) & 1u) f[J] = ldg(src + (int64_t)opp(J) * p.ks + c);
+    direct_bounce<J + 1, SLAB>(f, src, c, p, w);
+  }
+}
+
+template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+__global__ void __launch_bounds__(32 * kTileWarps, 4)
+    k_sweep_tile(const KParams p, const double* __restrict__ src, double* __restrict__ dst,
+                 int part, int zper) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x0w = (blockIdx.x * kTileWarps + warp) * 32;
+  const int x = x0w + lane;
+  const int y = blockIdx.y;
+  const int z0 = blockIdx.z * zper;
+  const int z1 = min(z0 + zper, p.nz);
+  if (x0w >= p.nx) return;  // whole warp outside (nx is a multiple of 32)
+  const bool active = !(part == PART_INTERIOR && (x == 0 || x == p.nx - 1));
+  double* const st0 = smem + (size_t)warp * 2 * kTileStage;
+  constexpr int kPoolPer = RECORDS ? 3 : 1;
+  auto cidx = [&](int z) { return ((int64_t)z * p.ny + y) * p.nx + x; };
+  const CellWord kSkip{kNonFluid, 0};
+
+  auto issue = [&](int z, int s, CellWord cw) -> int {
+    double* tile = st0 + s * kTileStage;
+    tile_issue_all<0, SLAB>(tile, src, x0w, y, z, lane, cw.w, p);
+    const bool fluid = !(cw.w & kNonFluid);
+    const int n = fluid ? kPoolPer * __popc(cw.w & kBounceMask) : 0;
+    int total;
+    int off = warp_excl_scan(n, lane, &total);
+    if (n) {
+      if (off + n <= kTilePool)
+        tile_issue_bounce<RECORDS>(tile + 19 * kTileW + off, src, cidx(z), p, cw.w, cw.base);
+      else
+        off = -1;
+    }
+    return off;
+  };
+
+  CellWord cw_cur = active ? ld_cw(p.cells + cidx(z0)) : kSkip;
+  int off_cur = issue(z0, 0, cw_cur);
+  cp_async_commit();
+  CellWord cw_next = (active && z0 + 1 < z1) ? ld_cw(p.cells + cidx(z0 + 1)) : kSkip;
+  int s = 0;
+  for (int z = z0; z < z1; ++z) {
+    int off_next = 0;
+    if (z + 1 < z1) off_next = issue(z + 1, s ^ 1, cw_next);
+    cp_async_commit();
+    const CellWord cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
+    cp_async_wait<1>();
+    __syncwarp();  // other lanes' copies of plane z are visible
+    const uint32_t w = cw_cur.w;
+    if (w & kFillSector) {
+      const int64_t c = cidx(z);
+#pragma unroll
+      for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, 0.0);
+    } else if (!(w & kNonFluid)) {
+      const double* tile = st0 + s * kTileStage;
+      const int64_t c = cidx(z);
+      double f[19];
+      if (off_cur >= 0) {
+        tile_gather<0, RECORDS>(f, tile, tile + 19 * kTileW + off_cur, lane, w, p, 0);
+      } else {  // pool overflow: bounce values loaded directly
+        tile_gather<0, false>(f, tile, tile, lane, 0u, p, 0);
+        direct_bounce<1, SLAB>(f, src, c, p, w);
+        if (RECORDS) links_all<1>(f, src, c, p, w, cw_cur.base);
+      }
+      if (OP == OP_STREAM_COLLIDE) {
+        if (GLBM)
+          collide_glbm<RHO1>(f, p, z);
+        else
+          collide_core<RHO1>(f, p);
+      }
+#pragma unroll
+      for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, f[j]);
+      if (SLAB && OP == OP_STREAM_COLLIDE) {
+        const int64_t hp = (int64_t)p.ny * p.nz;
+        const int64_t h = (int64_t)z * p.ny + y;
+        if (x == 0) {
+          p.send_lo[0 * hp + h] = f[2];
+          p.send_lo[1 * hp + h] = f[8];
+          p.send_lo[2 * hp + h] = f[10];
+          p.send_lo[3 * hp + h] = f[12];
+          p.send_lo[4 * hp + h] = f[14];
+        }
+        if (x == p.nx - 1) {
+          p.send_hi[0 * hp + h] = f[1];
+          p.send_hi[1 * hp + h] = f[7];
+          p.send_hi[2 * hp + h] = f[9];
+          p.send_hi[3 * hp + h] = f[11];
+          p.send_hi[4 * hp + h] = f[13];
+        }
+      }
+    }
+    __syncwarp();  // all lanes done reading stage s before it is refilled
+    cw_cur = cw_next;
+    cw_next = cw_nn;
+    off_cur = off_next;
+    s ^= 1;
+  }
+  cp_async_wait<0>();
 }
 
 // Edge columns x = 0 and x = nx-1 only (slab overlap path).
@@ -292,7 +740,8 @@ __global__ void __launch_bounds__(128) k_sweep_edges(const KParams p,
   const int z = (int)(h / p.ny), y = (int)(h - (int64_t)z * p.ny);
   const int x = side ? p.nx - 1 : 0;
   if (side == 1 && p.nx == 1) return;
-  sweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z);
+  const CellWord cw = ld_cw(p.cells + ((int64_t)z * p.ny + y) * p.nx + x);
+  sweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z, cw);
 }
 
 // K0: collide every fluid cell in place (first step from a pre-collision state).
@@ -302,7 +751,7 @@ __global__ void __launch_bounds__(128) k_collide_inplace(const KParams p, double
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= p.nx) return;
   const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
-  if (__ldg(p.cellword + c) & 1u) return;
+  if (p.cells[c].w & kNonFluid) return;
   double f[19];
 #pragma unroll
   for (int j = 0; j < 19; ++j) f[j] = buf[(int64_t)j * p.ks + c];
@@ -379,7 +828,7 @@ __global__ void k_macro_fields(const KParams p, const double* __restrict__ f, do
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= p.nx) return;
   const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
-  if (__ldg(p.cellword + c) & 1u) {
+  if (p.cells[c].w & kNonFluid) {
     if (drho) drho[c] = 0.0;
     if (ux) ux[c] = 0.0;
     if (uy) uy[c] = 0.0;
@@ -396,7 +845,7 @@ __global__ void k_macro_fields(const KParams p, const double* __restrict__ f, do
 
 // Sequential per-plane sum in ascending cell order (simulation.cpp:400-407),
 // one thread per plane so the rounding sequence is the reference's.
-__global__ void k_plane_sums(const uint32_t* __restrict__ cellword,
+__global__ void k_plane_sums(const CellWord* __restrict__ cells,
                              const double* __restrict__ u, int64_t plane, int nz,
                              double* sums) {
   const int z = blockIdx.x * blockDim.x + threadIdx.x;
@@ -404,7 +853,7 @@ __global__ void k_plane_sums(const uint32_t* __restrict__ cellword,
   double s = 0.0;
   const int64_t c0 = plane * z;
   for (int64_t i = 0; i < plane; ++i) {
-    if (__ldg(cellword + c0 + i) & 1u) continue;
+    if (cells[c0 + i].w & kNonFluid) continue;
     s = DADD(s, __ldg(u + c0 + i));
   }
   sums[z] = s;
@@ -420,7 +869,7 @@ __global__ void k_max_speed2(const KParams p, const double* __restrict__ f,
   bool bad = false;
   if (x < p.nx) {
     const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
-    if (!(__ldg(p.cellword + c) & 1u)) {
+    if (!(p.cells[c].w & kNonFluid)) {
       double d, u[3];
       if (!macro_cell<GLBM>(p, f, c, z, d, u)) atomicOr(err, 1);
       m2 = DADD(DADD(DMUL(u[0], u[0]), DMUL(u[1], u[1])), DMUL(u[2], u[2]));
@@ -442,11 +891,11 @@ __global__ void k_max_speed2(const KParams p, const double* __restrict__ f,
   }
 }
 
-__global__ void k_fill_equilibrium(const uint32_t* __restrict__ cellword, int64_t cells,
+__global__ void k_fill_equilibrium(const CellWord* __restrict__ cw, int64_t cells,
                                    int64_t ks, double* f, const double* feq /*19*/) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cells) return;
-  if (cellword[c] & 1u) return;
+  if (cw[c].w & kNonFluid) return;
 #pragma unroll
   for (int k = 0; k < 19; ++k) f[(int64_t)k * ks + c] = feq[k];
 }
@@ -462,6 +911,26 @@ dim3 cell_grid2(const KParams& p) {
   const int bx = cell_block(p).x;
   return dim3((p.nx + bx - 1) / bx, p.ny, p.nz);
 }
+// z-planes per block: long marching columns, but at least ~4 waves of blocks
+// over 148 SMs x 4 resident blocks.
+int pipe_zper(const KParams& p) {
+  if (const char* e = std::getenv("PGPU_ZPER")) return std::max(1, std::min(atoi(e), p.nz));
+  const int64_t cols = (int64_t)((p.nx + kPipeBX - 1) / kPipeBX) * p.ny;
+  int zper = (int)std::min<int64_t>(4, std::max<int64_t>(1, cols * p.nz / (148 * 4 * 4)));
+  return std::min(zper, p.nz);
+}
+// PGPU_SWEEP=pipe (default) | tile | plain -- kernel variant (experiments)
+int g_sweep_mode = [] {
+  const char* e = std::getenv("PGPU_SWEEP");
+  if (!e) return 1;
+  if (e[0] == 't') return 0;
+  if (e[0] == 'p' && e[1] == 'l') return 2;
+  return 1;
+}();
+dim3 sweep_grid(const KParams& p) {
+  const int bx = cell_block(p).x;
+  return dim3((p.nx + bx - 1) / bx, p.ny, (p.nz + kZPer - 1) / kZPer);
+}
 
 template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
 void launch_sweep_t(const KParams& p, const double* src, double* dst, int part,
@@ -470,8 +939,31 @@ void launch_sweep_t(const KParams& p, const double* src, double* dst, int part,
     const int64_t n = 2 * (int64_t)p.ny * p.nz;
     k_sweep_edges<RHO1, GLBM, RECORDS, SLAB, OP>
         <<<(unsigned)((n + kBX - 1) / kBX), kBX, 0, s>>>(p, src, dst);
+  } else if (g_sweep_mode == 0 && p.nx % 32 == 0) {
+    const int zper = pipe_zper(p);
+    const int bx = 32 * kTileWarps;
+    const dim3 grid((p.nx + bx - 1) / bx, p.ny, (p.nz + zper - 1) / zper);
+    static bool attr = [] {
+      cudaFuncSetAttribute(k_sweep_tile<RHO1, GLBM, RECORDS, SLAB, OP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
+      return true;
+    }();
+    (void)attr;
+    k_sweep_tile<RHO1, GLBM, RECORDS, SLAB, OP><<<grid, bx, kTileSmem, s>>>(p, src, dst, part,
+                                                                            zper);
+  } else if (g_sweep_mode <= 1) {
+    const int zper = pipe_zper(p);
+    const dim3 grid((p.nx + kPipeBX - 1) / kPipeBX, p.ny, (p.nz + zper - 1) / zper);
+    static bool attr = [] {
+      cudaFuncSetAttribute(k_sweep_pipe<RHO1, GLBM, RECORDS, SLAB, OP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, pipe_smem(RECORDS));
+      return true;
+    }();
+    (void)attr;
+    k_sweep_pipe<RHO1, GLBM, RECORDS, SLAB, OP><<<grid, kPipeBX, pipe_smem(RECORDS), s>>>(p, src, dst,
+                                                                                 part, zper);
   } else {
-    k_sweep<RHO1, GLBM, RECORDS, SLAB, OP><<<cell_grid2(p), cell_block(p), 0, s>>>(p, src, dst,
+    k_sweep<RHO1, GLBM, RECORDS, SLAB, OP><<<sweep_grid(p), cell_block(p), 0, s>>>(p, src, dst,
                                                                                   part);
   }
 }
@@ -543,7 +1035,7 @@ void launch_macro_fields(bool glbm, const KParams& p, const double* f, double* d
 
 void launch_plane_sums(const KParams& p, const double* u, double* sums, cudaStream_t s) {
   const int64_t plane = (int64_t)p.nx * p.ny;
-  k_plane_sums<<<(p.nz + 31) / 32, 32, 0, s>>>(p.cellword, u, plane, p.nz, sums);
+  k_plane_sums<<<(p.nz + 31) / 32, 32, 0, s>>>(p.cells, u, plane, p.nz, sums);
 }
 
 void launch_max_speed2(bool glbm, const KParams& p, const double* f,
@@ -558,7 +1050,7 @@ void launch_max_speed2(bool glbm, const KParams& p, const double* f,
 
 void launch_fill_equilibrium(const KParams& p, int64_t cells, double* f, const double* feq,
                              cudaStream_t s) {
-  k_fill_equilibrium<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(p.cellword, cells, p.ks, f,
+  k_fill_equilibrium<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(p.cells, cells, p.ks, f,
                                                                      feq);
 }
 

@@ -7,13 +7,24 @@ namespace pgpu {
 
 constexpr int kQ = 19;
 
-// Per-link record, stored in (cell, incoming direction j) order so that the
-// kernel finds the record of bounce direction j of cell c at
-//   link_base[c] + popcount(cellword[c] & ((1u << j) - 1) & ~1u).
+// Per-link record, one double in (cell, incoming direction j) order so that
+// the kernel finds the record of bounce direction j of cell c at
+//   cell.base + popcount(cell.w & ((1u << j) - 1) & kBounceMask).
+// CLI links store c = (1-2q)/(1+2q) computed on the host exactly like
+// boundary.cpp:27-28 (q the fp32 value of geometry.cpp:625); SBB links store
+// a quiet NaN, moving-wall links +infinity.
 enum LinkKind : uint32_t { kLinkSBB = 0, kLinkCLI = 1, kLinkMoving = 2 };
-struct LinkRec {
-  float q;        // fp32 wall distance exactly as stored by voxelize (geometry.cpp:625)
-  uint32_t kind;  // LinkKind
+typedef double LinkRec;
+
+// Per-cell word: bit 0 = not fluid; bits 1..18 = f_j comes from a link;
+// bit 19 = non-fluid cell that shares a 32-byte sector with a fluid cell
+// (written with zeros so no sector is ever partially written).
+constexpr uint32_t kNonFluid = 1u;
+constexpr uint32_t kBounceMask = 0x7FFFEu;
+constexpr uint32_t kFillSector = 1u << 19;
+struct alignas(8) CellWord {
+  uint32_t w;
+  int32_t base;  // first link record of the cell
 };
 
 // GLBM per-plane coefficients (simulation.cpp:213-253), evaluated on the host
@@ -36,9 +47,9 @@ struct KParams {
   int32_t nx, ny, nz;
   int32_t px, py, pz;  // periodic flags (x ignored in slab mode)
   int64_t ks;          // element stride between the 19 direction planes
-  const uint32_t* cellword;  // bit0: not fluid; bit j (1..18): f_j comes from a link
-  const int32_t* link_base;  // per-cell first record (only with records)
+  const CellWord* cells;     // per-cell word + link base
   const LinkRec* links;
+  int32_t fill_sectors;      // write zeros into fill-flagged non-fluid cells
   double wp, wm, rho0, nu, cf;
   double fpop[9];   // core force term ((3*w)*rho0)*eg per pair (simulation.cpp:190)
   double wr3[9];    // (w*rho0)*3 per pair                      (simulation.cpp:185)

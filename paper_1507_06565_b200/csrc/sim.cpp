@@ -16,6 +16,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -64,9 +65,10 @@ struct pgpu_sim {
   int64_t fluid_cells = 0;
   int32_t cli_fallbacks = 0;
   // link structures (host mirror)
-  std::vector<uint32_t> cellword;
-  std::vector<int32_t> link_base;
-  std::vector<LinkRec> recs;
+  std::vector<CellWord> cellword;  // w + link base (kparams.h)
+  std::vector<LinkRec> recs;       // host-computed CLI coefficient / NaN / +inf
+  std::vector<uint8_t> rec_kind;   // LinkKind per record
+  std::vector<float> rec_q;
   int64_t n_links = 0;
   bool any_moving = false;
   bool records_uploaded = false;
@@ -78,8 +80,7 @@ struct pgpu_sim {
   bool eps_in_eq = true;
   // device memory
   double* f[2] = {nullptr, nullptr};
-  uint32_t* d_cellword = nullptr;
-  int32_t* d_base = nullptr;
+  CellWord* d_cellword = nullptr;
   LinkRec* d_recs = nullptr;
   PlaneCoef* d_planes = nullptr;
   double* d_feq = nullptr;
@@ -110,7 +111,6 @@ struct pgpu_sim {
     cudaSetDevice(device);
     for (double* p : f) cudaFree(p);
     cudaFree(d_cellword);
-    cudaFree(d_base);
     cudaFree(d_recs);
     cudaFree(d_planes);
     cudaFree(d_feq);
@@ -195,19 +195,31 @@ struct pgpu_sim {
 
   bool records_needed() const { return scheme == PGPU_CLI || any_moving; }
 
+  // boundary.cpp:27-28 on the host: c = (1 - 2q)/(1 + 2q) from the fp32 q.
+  void encode_records() {
+    recs.resize(n_links);
+    for (int64_t r = 0; r < n_links; ++r) {
+      if (rec_kind[r] == kLinkCLI) {
+        const double q = rec_q[r];
+        recs[r] = (1.0 - 2.0 * q) / (1.0 + 2.0 * q);
+      } else if (rec_kind[r] == kLinkMoving) {
+        recs[r] = std::numeric_limits<double>::infinity();
+      } else {
+        recs[r] = std::numeric_limits<double>::quiet_NaN();
+      }
+    }
+  }
+
   void upload_records() {
     if (n_links == 0) {
       records_uploaded = true;
       return;
     }
-    if (!d_base) CK(cudaMalloc(&d_base, sizeof(int32_t) * cells));
+    encode_records();
     if (!d_recs) CK(cudaMalloc(&d_recs, sizeof(LinkRec) * n_links));
-    CK(cudaMemcpyAsync(d_base, link_base.data(), sizeof(int32_t) * cells, cudaMemcpyHostToDevice,
-                       stream));
     CK(cudaMemcpyAsync(d_recs, recs.data(), sizeof(LinkRec) * n_links, cudaMemcpyHostToDevice,
                        stream));
     CK(cudaStreamSynchronize(stream));
-    kp.link_base = d_base;
     kp.links = d_recs;
     records_uploaded = true;
     drop_graphs();
@@ -426,18 +438,18 @@ inline int wrap(int v, int n, bool periodic) {
   return (v % n + n) % n;
 }
 
-void build_links(pgpu_sim* s, const pgpu_geometry* g) {
+void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
   const int nx = s->nx, ny = s->ny, nz = s->nz;
   const uint8_t* flags = g->flags;
-  // cellword: bit0 non-fluid; bit j: upstream x - e_j is non-fluid or outside
-  s->cellword.assign(s->cells, 0);
+  // bit0 non-fluid; bit j: upstream x - e_j is non-fluid or outside the domain
+  s->cellword.assign(s->cells, CellWord{0u, 0});
   parallel_for(nz, [&](int64_t za, int64_t zb, int) {
     for (int z = (int)za; z < (int)zb; ++z)
       for (int y = 0; y < ny; ++y)
         for (int x = 0; x < nx; ++x) {
           const int64_t c = ((int64_t)z * ny + y) * nx + x;
           if (flags[c] != 0) {
-            s->cellword[c] = 1u;
+            s->cellword[c].w = kNonFluid;
             continue;
           }
           uint32_t w = 0;
@@ -460,18 +472,29 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g) {
             }
             if (nonfluid) w |= 1u << j;
           }
-          s->cellword[c] = w;
+          s->cellword[c].w = w;
         }
   });
+  // non-fluid cells sharing an aligned 4-cell (32-byte) group with fluid
+  // cells are zero-filled by the sweep, so no DRAM sector is partly written
+  if (fill_sectors) {
+    for (int64_t c0 = 0; c0 < s->cells; c0 += 4) {
+      const int64_t c1 = std::min<int64_t>(c0 + 4, s->cells);
+      bool anyfluid = false;
+      for (int64_t c = c0; c < c1; ++c) anyfluid |= !(s->cellword[c].w & kNonFluid);
+      if (!anyfluid) continue;
+      for (int64_t c = c0; c < c1; ++c)
+        if (s->cellword[c].w & kNonFluid) s->cellword[c].w |= kFillSector;
+    }
+  }
   // per-cell record base (exclusive prefix of bounce counts)
-  s->link_base.assign(s->cells, 0);
   int64_t total = 0;
   for (int64_t c = 0; c < s->cells; ++c) {
-    s->link_base[c] = (int32_t)total;
-    const uint32_t w = s->cellword[c];
-    if (!(w & 1u)) total += __builtin_popcount(w);
+    s->cellword[c].base = (int32_t)total;
+    const uint32_t w = s->cellword[c].w;
+    if (!(w & kNonFluid)) total += __builtin_popcount(w & kBounceMask);
+    if (total > std::numeric_limits<int32_t>::max()) throw ConfigError("too many boundary links");
   }
-  if (total > std::numeric_limits<int32_t>::max()) throw ConfigError("too many boundary links");
   if (g->n_links != total) {
     std::ostringstream os;
     os << "boundary links (" << g->n_links << ") do not match the fluid->non-fluid lattice "
@@ -479,7 +502,8 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g) {
     throw ConfigError(os.str());
   }
   s->n_links = total;
-  s->recs.assign(total, LinkRec{0.5f, kLinkSBB});
+  s->rec_kind.assign(total, kLinkSBB);
+  s->rec_q.assign(total, 0.5f);
   std::vector<uint8_t> seen(total, 0);
   s->any_moving = false;
   s->cli_fallbacks = 0;
@@ -489,17 +513,17 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g) {
     if (c < 0 || c >= s->cells || flags[c] != 0) throw ConfigError("boundary link on a non-fluid or out-of-range cell");
     if (k < 1 || k > 18) throw ConfigError("boundary link direction must be in 1..18");
     const int j = opposite(k);
-    const uint32_t w = s->cellword[c];
+    const uint32_t w = s->cellword[c].w;
     if (!((w >> j) & 1u)) throw ConfigError("boundary link points to a fluid neighbour");
-    const int64_t r = s->link_base[c] + __builtin_popcount(w & ((1u << j) - 1u) & ~1u);
+    const int64_t r = s->cellword[c].base + __builtin_popcount(w & ((1u << j) - 1u) & kBounceMask);
     if (seen[r]) throw ConfigError("duplicate boundary link");
     seen[r] = 1;
-    LinkRec rec{g->link_q[i], kLinkSBB};
+    s->rec_q[r] = g->link_q[i];
     const int64_t sf = g->link_second_fluid[i];
     const bool moving = g->link_moving && g->link_moving[i];
     if (s->scheme == PGPU_CLI && sf == -1) ++s->cli_fallbacks;  // simulation.cpp:97-101
     if (moving) {
-      rec.kind = kLinkMoving;
+      s->rec_kind[r] = kLinkMoving;
       s->any_moving = true;
     } else if (s->scheme == PGPU_CLI && sf != -1) {
       // second_fluid must be the upstream cell x - e_k, which is then fluid
@@ -516,9 +540,8 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g) {
         ok = sf == ((int64_t)zs * ny + ys) * nx + xs;
       }
       if (!ok) throw ConfigError("CLI second_fluid must be the cell x_f1 - e_k");
-      rec.kind = kLinkCLI;
+      s->rec_kind[r] = kLinkCLI;
     }
-    s->recs[r] = rec;
   }
 }
 
@@ -588,7 +611,8 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     s->lo = g->wall_plane_lo;
     s->hi = g->wall_plane_hi;
     s->fluid_cells = g->fluid_cells;
-    build_links(s.get(), g);
+    const char* fill_env = std::getenv("PGPU_FILL_SECTORS");
+    build_links(s.get(), g, !(fill_env && fill_env[0] == '0'));
 
     // device buffers: two full PDF grids, zero-filled like the reference
     const size_t fbytes = sizeof(double) * 19 * (size_t)s->ks;
@@ -596,8 +620,8 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
       CK(cudaMalloc(&s->f[b], fbytes));
       CK(cudaMemsetAsync(s->f[b], 0, fbytes, s->stream));
     }
-    CK(cudaMalloc(&s->d_cellword, sizeof(uint32_t) * s->cells));
-    CK(cudaMemcpyAsync(s->d_cellword, s->cellword.data(), sizeof(uint32_t) * s->cells,
+    CK(cudaMalloc(&s->d_cellword, sizeof(CellWord) * s->cells));
+    CK(cudaMemcpyAsync(s->d_cellword, s->cellword.data(), sizeof(CellWord) * s->cells,
                        cudaMemcpyHostToDevice, s->stream));
     CK(cudaMalloc(&s->d_feq, sizeof(double) * 19));
     CK(cudaMalloc(&s->d_flags, sizeof(int) * 2));
@@ -611,7 +635,7 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     kp.py = s->per[1];
     kp.pz = s->per[2];
     kp.ks = s->ks;
-    kp.cellword = s->d_cellword;
+    kp.cells = s->d_cellword;
     s->refresh_params();
     if (s->records_needed()) s->upload_records();
     CK(cudaStreamSynchronize(s->stream));
@@ -674,15 +698,15 @@ int pgpu_set_lid_velocity(pgpu_sim* sim, const double u[3]) {
     for (int i = 0; i < 3; ++i) sim->lid[i] = u[i];
     const int nx = sim->nx, ny = sim->ny, nz = sim->nz;
     for (int64_t c = 0; c < sim->cells; ++c) {
-      const uint32_t w = sim->cellword[c];
-      if ((w & 1u) || w == 0) continue;
-      int64_t r = sim->link_base[c];
+      const uint32_t w = sim->cellword[c].w;
+      if ((w & kNonFluid) || !(w & kBounceMask)) continue;
+      int64_t r = sim->cellword[c].base;
       const int z = (int)(c / ((int64_t)nx * ny));
       for (int j = 1; j < 19; ++j) {
         if (!((w >> j) & 1u)) continue;
         const int k = opposite(j);
         if (z + kE[k][2] == nz - 1) {
-          sim->recs[r].kind = kLinkMoving;
+          sim->rec_kind[r] = kLinkMoving;
           sim->any_moving = true;
         }
         ++r;
