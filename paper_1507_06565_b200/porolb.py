@@ -597,10 +597,13 @@ class Simulation:
         _check(lib.pgpu_halo_elems(self._h, C.byref(v)))
         return v.value
 
-    def set_halo_buffers(self, send_lo: int, send_hi: int, recv_lo0: int, recv_lo1: int,
-                         recv_hi0: int, recv_hi1: int) -> None:
-        _check(lib.pgpu_set_halo_buffers(self._h, *[C.c_void_p(p) for p in (
-            send_lo, send_hi, recv_lo0, recv_lo1, recv_hi0, recv_hi1)]))
+    def set_halo_buffers(self, send_lo, send_hi, recv_lo0, recv_lo1, recv_hi0, recv_hi1) -> None:
+        """Device buffers of halo_elems doubles each: raw pointers or CUDA tensors
+        (kept alive by this object)."""
+        bufs = (send_lo, send_hi, recv_lo0, recv_lo1, recv_hi0, recv_hi1)
+        self._halo_keep = bufs
+        ptrs = [b if isinstance(b, int) else b.data_ptr() for b in bufs]
+        _check(lib.pgpu_set_halo_buffers(self._h, *[C.c_void_p(p) for p in ptrs]))
 
     @property
     def halo_parity(self) -> int:
