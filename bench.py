@@ -202,10 +202,10 @@ def run_ours(args):
         sim = configs.make_simulation(w, geom, device=local)
         fluid_local = geom.fluid_cells
         stepper = sim.step
-    stream = torch.cuda.Stream(device=local)
     if world > 1:
-        sim_obj.set_stream(stream)
+        stream = sim_obj.me.stream
     else:
+        stream = torch.cuda.Stream(device=local)
         sim.set_stream(stream.cuda_stream)
     with torch.cuda.stream(stream):
         stepper(args.warmup)

@@ -44,14 +44,27 @@ def slab_ranges(nx: int, world: int) -> List[tuple]:
     return [(r * w, (r + 1) * w) for r in range(world)]
 
 
+def _on(stream):
+    """Context that makes `stream` torch's current stream (no-op on CPU)."""
+    import contextlib
+
+    if stream is None:
+        return contextlib.nullcontext()
+    import torch
+
+    return torch.cuda.stream(stream)
+
+
 class SlabRank:
     """One slab: a slab-mode Simulation (or a compatible engine) plus its
     send/receive halo buffers (torch tensors on the engine's device)."""
 
-    def __init__(self, workload, rank: int, world: int, device=0, engine: Optional[Callable] = None):
+    def __init__(self, workload, rank: int, world: int, device=0, engine: Optional[Callable] = None,
+                 stream=None):
         import torch
 
         self.rank, self.world = rank, world
+        self.stream = None
         self.workload = workload
         self.x0, self.x1 = slab_ranges(workload.dims[0], world)[rank]
         self.geometry = workload.geometry_slab(self.x0, self.x1)
@@ -62,6 +75,9 @@ class SlabRank:
             if gp is not None:
                 self.sim.set_porous(gp)
             tdev = torch.device("cuda", int(device))
+            # kernels, halo copies and NCCL calls are ordered on one torch stream
+            self.stream = stream if stream is not None else torch.cuda.Stream(device=tdev)
+            self.sim.set_stream(self.stream.cuda_stream)
         else:
             self.sim = engine(self.geometry, workload)
             tdev = torch.device("cpu")
@@ -87,6 +103,10 @@ class DistTransport:
         self.right = (rank.rank + 1) % rank.world
 
     def step(self, n: int = 1) -> None:
+        with _on(self.me.stream):
+            self._step(n)
+
+    def _step(self, n: int) -> None:
         me, dist = self.me, self.dist
         for _ in range(int(n)):
             me.sim.step_part(0)  # edge columns -> send buffers
@@ -161,6 +181,7 @@ class SlabSimulation(DistTransport):
         self.sim = self.me.sim
 
     def set_stream(self, stream) -> None:
+        self.me.stream = stream
         self.sim.set_stream(stream.cuda_stream)
 
 
@@ -171,10 +192,18 @@ class LocalTransport:
     verify the decomposition bit-for-bit on one GPU (and on CPU engines)."""
 
     def __init__(self, workload, world: int, device=0, engine=None):
-        self.ranks = [SlabRank(workload, r, world, device, engine) for r in range(world)]
+        import torch
+
+        self.stream = None if engine is not None else torch.cuda.Stream(device=int(device))
+        self.ranks = [SlabRank(workload, r, world, device, engine, self.stream)
+                      for r in range(world)]
         self.world = world
 
     def step(self, n: int = 1) -> None:
+        with _on(self.stream):
+            self._step(n)
+
+    def _step(self, n: int) -> None:
         R, W = self.ranks, self.world
         for _ in range(int(n)):
             for r in R:
