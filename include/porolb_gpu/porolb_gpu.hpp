@@ -1,0 +1,365 @@
+// porolb_gpu.hpp -- header-only C++ mirror of the reference porolb API for the
+// time-step path, implemented over the C ABI of libporolb_cuda.so
+// (include/porolb_gpu.h).  A caller of porolb::Simulation (reference
+// proj/include/porolb/simulation.hpp:53-111) switches by including this header
+// and linking libporolb_cuda.so; names, argument meaning and the exception
+// types (errors.hpp:9-21) are the reference's.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../porolb_gpu.h"
+
+namespace porolb_gpu {
+
+using Vec3 = std::array<double, 3>;  // lattice.hpp:10
+inline constexpr int kQ = 19;
+
+struct ConfigError : std::runtime_error {  // errors.hpp:9-12
+  explicit ConfigError(const std::string& m) : std::runtime_error(m) {}
+};
+struct NumericalInstability : std::runtime_error {  // errors.hpp:14-17
+  explicit NumericalInstability(const std::string& m) : std::runtime_error(m) {}
+};
+struct GeometryError : std::runtime_error {  // errors.hpp:19-22
+  explicit GeometryError(const std::string& m) : std::runtime_error(m) {}
+};
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+
+inline void check(int status) {
+  if (status == PGPU_OK) return;
+  const std::string msg = pgpu_last_error();
+  switch (status) {
+    case PGPU_ERR_CONFIG: throw ConfigError(msg);
+    case PGPU_ERR_INSTABILITY: throw NumericalInstability(msg);
+    case PGPU_ERR_GEOMETRY: throw GeometryError(msg);
+    case PGPU_ERR_CUDA: throw CudaError(msg);
+    default: throw std::invalid_argument(msg);
+  }
+}
+
+enum class WallScheme : std::uint8_t { SBB = PGPU_SBB, CLI = PGPU_CLI };  // boundary.hpp:12
+enum class GlbmViscosity { Plain, Rescaled, ConstantRatio };               // simulation.hpp:29
+
+struct FluidParams {  // lattice.hpp:32-39
+  double nu = 1.0 / 6.0;
+  double omega_plus = 1.0;
+  double omega_minus = 1.0;
+  double lambda_magic = 3.0 / 16.0;
+  double rho0 = 1.0;
+  Vec3 body_force{0.0, 0.0, 0.0};
+
+  pgpu_fluid_params c() const {
+    return pgpu_fluid_params{nu, omega_plus, omega_minus, lambda_magic, rho0,
+                             {body_force[0], body_force[1], body_force[2]}};
+  }
+};
+
+inline FluidParams relaxation_from_magic(double nu, double lambda_magic) {  // lattice.hpp:42-44
+  pgpu_fluid_params p;
+  check(pgpu_relaxation_from_magic(nu, lambda_magic, &p));
+  FluidParams f;
+  f.nu = p.nu;
+  f.omega_plus = p.omega_plus;
+  f.omega_minus = p.omega_minus;
+  f.lambda_magic = p.lambda_magic;
+  f.rho0 = p.rho0;
+  return f;
+}
+
+struct Sphere {  // geometry.hpp:14-17
+  Vec3 center{0.0, 0.0, 0.0};
+  double radius = 0.0;
+};
+struct Box3 {
+  double lx = 0.0, ly = 0.0, lz = 0.0;
+};
+struct SpherePack {  // geometry.hpp:25-32
+  std::vector<Sphere> spheres;
+  Box3 box;
+  double bottom_plate_z = 0.0;
+};
+struct Dims {
+  int nx = 0, ny = 0, nz = 0;
+  std::int64_t cells() const { return static_cast<std::int64_t>(nx) * ny * nz; }
+  std::int64_t index(int x, int y, int z) const {
+    return (static_cast<std::int64_t>(z) * ny + y) * nx + x;
+  }
+};
+struct VoxelizeOptions {  // geometry.hpp:51-57
+  std::array<bool, 3> periodic{true, true, false};
+  bool wall_z_lo = false;
+  bool wall_z_hi = false;
+  double q_clamp_min = 0.05;
+};
+
+// VoxelGeometry (geometry.hpp:62-73): owns the voxelizer's arrays.
+class VoxelGeometry {
+ public:
+  VoxelGeometry() = default;
+  explicit VoxelGeometry(pgpu_voxel_geometry* h) : h_(h, pgpu_voxel_geometry_free) {
+    check(pgpu_voxel_geometry_view(h, &view_, &q_fallback_count_));
+  }
+  const pgpu_geometry& c() const { return view_; }
+  Dims dims() const { return Dims{view_.dims[0], view_.dims[1], view_.dims[2]}; }
+  std::int64_t fluid_cells() const { return view_.fluid_cells; }
+  std::int64_t n_links() const { return view_.n_links; }
+  int q_fallback_count() const { return q_fallback_count_; }
+  std::uint8_t flag(std::int64_t cell) const { return view_.flags[cell]; }
+  double porosity(int z) const { return view_.porosity[z]; }
+
+ private:
+  std::shared_ptr<pgpu_voxel_geometry> h_;
+  pgpu_geometry view_{};
+  int q_fallback_count_ = 0;
+};
+
+namespace detail {
+struct PackArrays {
+  std::vector<double> x, y, z, r;
+  pgpu_sphere_pack c{};
+  explicit PackArrays(const SpherePack& p) {
+    for (const Sphere& s : p.spheres) {
+      x.push_back(s.center[0]);
+      y.push_back(s.center[1]);
+      z.push_back(s.center[2]);
+      r.push_back(s.radius);
+    }
+    c.n_spheres = static_cast<std::int64_t>(p.spheres.size());
+    c.cx = x.data();
+    c.cy = y.data();
+    c.cz = z.data();
+    c.radius = r.data();
+    c.box[0] = p.box.lx;
+    c.box[1] = p.box.ly;
+    c.box[2] = p.box.lz;
+    c.bottom_plate_z = p.bottom_plate_z;
+  }
+};
+inline pgpu_voxelize_options opts(const VoxelizeOptions& o) {
+  pgpu_voxelize_options c{};
+  for (int a = 0; a < 3; ++a) c.periodic[a] = o.periodic[a] ? 1 : 0;
+  c.wall_z_lo = o.wall_z_lo ? 1 : 0;
+  c.wall_z_hi = o.wall_z_hi ? 1 : 0;
+  c.q_clamp_min = o.q_clamp_min;
+  return c;
+}
+}  // namespace detail
+
+inline VoxelGeometry voxelize(const SpherePack& pack, Dims dims, const VoxelizeOptions& opt) {
+  detail::PackArrays pa(pack);
+  const int32_t d[3] = {dims.nx, dims.ny, dims.nz};
+  const pgpu_voxelize_options o = detail::opts(opt);
+  pgpu_voxel_geometry* h = nullptr;
+  check(pgpu_voxelize(&pa.c, d, &o, &h));
+  return VoxelGeometry(h);
+}
+
+inline VoxelGeometry make_box_geometry(Dims dims, const VoxelizeOptions& opt) {
+  const int32_t d[3] = {dims.nx, dims.ny, dims.nz};
+  const pgpu_voxelize_options o = detail::opts(opt);
+  pgpu_voxel_geometry* h = nullptr;
+  check(pgpu_make_box_geometry(d, &o, &h));
+  return VoxelGeometry(h);
+}
+
+struct GlbmPlaneParams {  // simulation.hpp:18-27
+  std::vector<double> eps, permeability, omega_plus, omega_minus;
+  double forchheimer_cf = 0.0;
+  bool eps_in_equilibrium = true;
+};
+
+inline std::vector<double> kozeny_carman(const std::vector<double>& eps, double d,
+                                         double free_threshold = 0.999) {
+  std::vector<double> K(eps.size());
+  check(pgpu_kozeny_carman(static_cast<int32_t>(eps.size()), eps.data(), d, free_threshold,
+                           K.data()));
+  return K;
+}
+
+inline GlbmPlaneParams make_glbm_params(const std::vector<double>& eps,
+                                        const std::vector<double>& K, double c_F, double nu,
+                                        double lambda, GlbmViscosity mode, double J = 1.0) {
+  if (eps.size() != K.size())
+    throw ConfigError("porosity and permeability profiles must have equal length");
+  GlbmPlaneParams p{eps, K, std::vector<double>(eps.size()), std::vector<double>(eps.size()),
+                    c_F, true};
+  check(pgpu_make_glbm_params(static_cast<int32_t>(eps.size()), eps.data(), K.data(), c_F, nu,
+                              lambda, static_cast<int32_t>(mode), J, p.omega_plus.data(),
+                              p.omega_minus.data()));
+  return p;
+}
+
+struct ProfileData {  // profile.hpp:12-34
+  std::vector<double> z, u_superficial, u_intrinsic, epsilon, u_normalized;
+  double u_max = 0.0, height = 0.0, z0 = 0.0, nu = 0.0;
+  Vec3 body_force{0.0, 0.0, 0.0};
+  int stream_axis = 0;
+  std::size_t size() const { return z.size(); }
+};
+
+struct SteadyConfig {  // simulation.hpp:118-123
+  double tolerance = 1e-8;
+  int check_interval = 1000;
+  long max_steps = 2000000;
+  double max_speed = 0.3 / 1.7320508075688772;
+};
+
+struct RunStats {  // simulation.hpp:125-132
+  long steps = 0;
+  double mlups = 0.0;
+  double seconds = 0.0;
+  bool converged = false;
+  double residual = 0.0;
+  int cli_fallbacks = 0;
+};
+
+namespace detail {
+inline ProfileData profile_from(std::vector<double> b[5], const pgpu_profile_meta& m) {
+  ProfileData p;
+  const std::size_t n = static_cast<std::size_t>(m.n_planes);
+  for (auto* v : {&b[0], &b[1], &b[2], &b[3], &b[4]}) v->resize(n);
+  p.z = b[0];
+  p.u_superficial = b[1];
+  p.u_intrinsic = b[2];
+  p.epsilon = b[3];
+  p.u_normalized = b[4];
+  p.u_max = m.u_max;
+  p.height = m.height;
+  p.z0 = m.z0;
+  p.nu = m.nu;
+  p.body_force = {m.body_force[0], m.body_force[1], m.body_force[2]};
+  p.stream_axis = m.stream_axis;
+  return p;
+}
+}  // namespace detail
+
+// porolb::Simulation on the B200 (simulation.hpp:53-111).
+class Simulation {
+ public:
+  Simulation(const VoxelGeometry& geom, const FluidParams& params, WallScheme scheme,
+             int device = 0)
+      : dims_(geom.dims()) {
+    const pgpu_fluid_params p = params.c();
+    pgpu_sim* s = nullptr;
+    check(pgpu_create(&geom.c(), &p, static_cast<int32_t>(scheme), device, &s));
+    h_.reset(s);
+  }
+
+  void set_body_force(const Vec3& g) { check(pgpu_set_body_force(h(), g.data())); }
+  FluidParams params() const {
+    pgpu_fluid_params p;
+    check(pgpu_get_params(h(), &p));
+    FluidParams f;
+    f.nu = p.nu;
+    f.omega_plus = p.omega_plus;
+    f.omega_minus = p.omega_minus;
+    f.lambda_magic = p.lambda_magic;
+    f.rho0 = p.rho0;
+    f.body_force = {p.body_force[0], p.body_force[1], p.body_force[2]};
+    return f;
+  }
+  void set_lid_velocity(const Vec3& u) { check(pgpu_set_lid_velocity(h(), u.data())); }
+  void set_porous(const GlbmPlaneParams& g) {
+    check(pgpu_set_porous(h(), static_cast<int32_t>(g.eps.size()), g.eps.data(),
+                          g.permeability.data(), g.omega_plus.data(), g.omega_minus.data(),
+                          g.forchheimer_cf, g.eps_in_equilibrium ? 1 : 0));
+    porous_ = true;
+  }
+  bool porous() const { return porous_; }
+  void step() { check(pgpu_step(h(), 1)); }
+  void step(long n) { check(pgpu_step(h(), n)); }
+  long steps_done() const {
+    int64_t n;
+    check(pgpu_steps_done(h(), &n));
+    return static_cast<long>(n);
+  }
+  const Dims& dims() const { return dims_; }
+  int cli_fallback_count() const {
+    int32_t n;
+    check(pgpu_cli_fallback_count(h(), &n));
+    return n;
+  }
+  std::int64_t fluid_cells() const {
+    int64_t n;
+    check(pgpu_fluid_cells(h(), &n));
+    return n;
+  }
+  void macroscopic(std::int64_t cell, double& delta_rho, Vec3& u) const {
+    check(pgpu_macroscopic(h(), cell, &delta_rho, u.data()));
+  }
+  ProfileData planar_profile(int stream_axis = 0) const {
+    std::vector<double> b[5];
+    for (auto& v : b) v.resize(static_cast<std::size_t>(dims_.nz));
+    pgpu_profile_meta m;
+    check(pgpu_planar_profile(h(), stream_axis, b[0].data(), b[1].data(), b[2].data(),
+                              b[3].data(), b[4].data(), &m));
+    return detail::profile_from(b, m);
+  }
+  double max_speed() const {
+    double v;
+    check(pgpu_max_speed(h(), &v));
+    return v;
+  }
+  void initialize_equilibrium(double delta_rho, const Vec3& u) {
+    check(pgpu_initialize_equilibrium(h(), delta_rho, u.data()));
+  }
+  // field().cur(k) / cell_populations (field.hpp:48-60) as explicit copies
+  std::vector<double> pdfs() const {
+    std::vector<double> f(static_cast<std::size_t>(kQ * dims_.cells()));
+    check(pgpu_get_pdfs(h(), f.data()));
+    return f;
+  }
+  void set_pdfs(const std::vector<double>& f) { check(pgpu_set_pdfs(h(), f.data())); }
+  std::array<double, kQ> cell_populations(std::int64_t cell) const {
+    std::array<double, kQ> f;
+    check(pgpu_get_cell_populations(h(), cell, f.data()));
+    return f;
+  }
+  void set_cell_populations(std::int64_t cell, const std::array<double, kQ>& f) {
+    check(pgpu_set_cell_populations(h(), cell, f.data()));
+  }
+  void synchronize() const { check(pgpu_synchronize(h())); }
+  pgpu_sim* handle() const { return h(); }
+
+ private:
+  struct Del {
+    void operator()(pgpu_sim* s) const { pgpu_destroy(s); }
+  };
+  pgpu_sim* h() const { return h_.get(); }
+  std::unique_ptr<pgpu_sim, Del> h_;
+  Dims dims_;
+  bool porous_ = false;
+};
+
+// simulation.hpp:134-138
+inline RunStats run_to_steady_state(Simulation& sim, const SteadyConfig& cfg,
+                                    ProfileData* final_profile = nullptr) {
+  pgpu_steady_config c{cfg.tolerance, cfg.check_interval, cfg.max_steps, cfg.max_speed};
+  pgpu_run_stats s;
+  std::vector<double> b[5];
+  for (auto& v : b) v.resize(static_cast<std::size_t>(sim.dims().nz));
+  pgpu_profile_meta m;
+  check(pgpu_run_to_steady_state(sim.handle(), &c, &s, b[0].data(), b[1].data(), b[2].data(),
+                                 b[3].data(), b[4].data(), &m));
+  if (final_profile) *final_profile = detail::profile_from(b, m);
+  RunStats r;
+  r.steps = static_cast<long>(s.steps);
+  r.mlups = s.mlups;
+  r.seconds = s.seconds;
+  r.converged = s.converged != 0;
+  r.residual = s.residual;
+  r.cli_fallbacks = s.cli_fallbacks;
+  return r;
+}
+
+}  // namespace porolb_gpu

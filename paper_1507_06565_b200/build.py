@@ -81,6 +81,20 @@ def build_product(force: bool = False, defines: tuple = (), lib: Path = LIB,
     return LIB
 
 
+DEMO_SRC = ROOT / "tools" / "porolb_gpu_demo.cpp"
+DEMO_BIN = ROOT / "tools" / "porolb_gpu_demo"
+
+
+def build_demo() -> Path:
+    """The C++ drop-in demo (include/porolb_gpu/porolb_gpu.hpp over the C ABI)."""
+    deps = [DEMO_SRC, ROOT / "include" / "porolb_gpu" / "porolb_gpu.hpp", LIB]
+    if _stale(DEMO_BIN, deps):
+        _run([CXX, "-std=c++17", "-O2", f"-I{ROOT / 'include'}", str(DEMO_SRC), "-o",
+              str(DEMO_BIN), f"-L{PKG}", "-lporolb_cuda", f"-Wl,-rpath,$ORIGIN/../{PKG.name}",
+              "-pthread"])
+    return DEMO_BIN
+
+
 def build_oracle() -> None:
     """Test infrastructure: oracle/liboracle.so always, oracle/_ref when the
     reference sources are present (this container; the GPU box gets the
@@ -106,6 +120,7 @@ def main(argv: list[str]) -> int:
         return 0
     lib = build_product(force="--force" in argv)
     print(lib)
+    print(build_demo())
     if "--all" in argv:
         build_oracle()
     return 0
