@@ -46,6 +46,27 @@ enum SweepPart { PART_ALL = 0, PART_EDGES = 1, PART_INTERIOR = 2 };
 // ---------------------------------------------------------------------------
 // Collision: simulation.cpp:150-196 (core) and :198-274 (GLBM), literal order.
 // ---------------------------------------------------------------------------
+// Multiply-add of a lattice-constant coefficient e in {-1, 0, 1}: acc + e*v.
+// The reference multiplies literally (its pair table is a runtime array);
+// with e = 0 the term e*v is a signed zero and acc + (+-0) == acc whenever acc
+// is not -0.  In the rho0 == 1 core path every accumulator starts at +0 and a
+// round-to-nearest sum is -0 only if both addends are -0, so acc is never -0
+// and dropping the zero terms is bit-identical for every finite state (a
+// non-finite population makes the cell non-finite either way).  e = +-1 terms
+// are exact (x*1 = x, x*-1 = -x, a + -b == a - b).
+// (e is a compile-time constant after unrolling; the branches fold away.)
+__device__ __forceinline__ double macc(int e, double acc, double v) {
+  if (e == 0) return acc;
+  if (e == 1) return DADD(acc, v);
+  return DSUB(acc, v);
+}
+// First term of a dot product e.u started from a literal (+0 + e*v).
+__device__ __forceinline__ double mfirst(int e, double v) {
+  if (e == 0) return 0.0;
+  if (e == 1) return DADD(0.0, v);
+  return DSUB(0.0, v);
+}
+
 template <bool RHO1>
 __device__ __forceinline__ void collide_core(double (&fk)[19], const KParams& p) {
   const double wp = p.wp, wm = p.wm, rho0 = p.rho0;
@@ -56,9 +77,15 @@ __device__ __forceinline__ void collide_core(double (&fk)[19], const KParams& p)
     const double a = fk[1 + 2 * q], b = fk[2 + 2 * q];
     drho = DADD(drho, DADD(a, b));
     const double d = DSUB(a, b);
-    vx = DADD(vx, DMUL((double)EX[1 + 2 * q], d));
-    vy = DADD(vy, DMUL((double)EY[1 + 2 * q], d));
-    vz = DADD(vz, DMUL((double)EZ[1 + 2 * q], d));
+    if (RHO1) {
+      vx = macc(EX[1 + 2 * q], vx, d);
+      vy = macc(EY[1 + 2 * q], vy, d);
+      vz = macc(EZ[1 + 2 * q], vz, d);
+    } else {
+      vx = DADD(vx, DMUL((double)EX[1 + 2 * q], d));
+      vy = DADD(vy, DMUL((double)EY[1 + 2 * q], d));
+      vz = DADD(vz, DMUL((double)EZ[1 + 2 * q], d));
+    }
   }
   const double ux = RHO1 ? vx : DDIV(vx, rho0);
   const double uy = RHO1 ? vy : DDIV(vy, rho0);
@@ -70,8 +97,13 @@ __device__ __forceinline__ void collide_core(double (&fk)[19], const KParams& p)
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
     const int k = 1 + 2 * q, kb = k + 1;
-    const double eu = DADD(DADD(DMUL((double)EX[k], ux), DMUL((double)EY[k], uy)),
-                           DMUL((double)EZ[k], uz));
+    double eu;
+    if (RHO1) {
+      // ((ex*ux + ey*uy) + ez*uz) with the zero terms dropped (see macc)
+      eu = macc(EZ[k], macc(EY[k], mfirst(EX[k], ux), uy), uz);
+    } else {
+      eu = DADD(DADD(DMUL((double)EX[k], ux), DMUL((double)EY[k], uy)), DMUL((double)EZ[k], uz));
+    }
     double t = DSUB(DMUL(DMUL(4.5, eu), eu), uu15);
     if (!RHO1) t = DMUL(rho0, t);
     const double feq_p = DMUL(pair_w(q), DADD(drho, t));
@@ -292,13 +324,19 @@ __global__ void __launch_bounds__(128, PGPU_SWEEP_MINB) k_sweep(const KParams p,
 
 // Asynchronous-copy pipeline helpers (k_sweep_pipe / k_sweep_tile).
 constexpr int kPipeBX = 128;
-constexpr int kStages = 2;
+// Pipeline depth per variant (measured on C4, round 1): SBB sweeps keep two
+// shared-memory stages at 4 blocks/SM; sweeps with link records (CLI /
+// moving walls) use one stage (the landed plane is moved to registers and the
+// stage refilled) at 5 blocks/SM, which leaves L1 room for the pooled extras.
+__host__ __device__ constexpr int pipe_stages(bool records) { return records ? 1 : 2; }
+__host__ __device__ constexpr int pipe_minb(bool records) { return records ? 5 : 4; }
 #ifndef PGPU_POOL
 #define PGPU_POOL 96
 #endif
 constexpr int kPool = PGPU_POOL;  // per-warp, per-stage slots for CLI / moving-wall extras
-constexpr int pipe_smem(bool records) {
-  return kStages * (19 * kPipeBX + (records ? (kPipeBX / 32) * kPool : 0)) * (int)sizeof(double);
+__host__ __device__ constexpr int pipe_smem(bool records) {
+  return pipe_stages(records) * (19 * kPipeBX + (records ? (kPipeBX / 32) * kPool : 0)) *
+         (int)sizeof(double);
 }
 
 __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
@@ -320,6 +358,21 @@ __device__ __forceinline__ void issue_all(double* stage, const double* __restric
   if constexpr (J < 19) {
     cp_async8(stage + J * kPipeBX, pull_addr<J, SLAB>(src, x, y, z, c, p, w));
     issue_all<J + 1, SLAB>(stage, src, x, y, z, c, p, w);
+  }
+}
+
+// Cells off every periodic wrap face: source = cell + constant offset, the
+// offset picked by the bounce bit (host-precomputed, KParams).
+template <int J>
+__device__ __forceinline__ void issue_fast(double* stage, const double* cellp,
+                                           const KParams& p, uint32_t w) {
+  if constexpr (J < 19) {
+    const double* a = cellp + p.pull_off[J];
+#ifndef PGPU_EXPERIMENT_NOBOUNCE  // traffic-attribution experiment only (wrong results)
+    if (J != 0 && ((w >> J) & 1u)) a += p.bounce_delta[J];
+#endif
+    cp_async8(stage + J * kPipeBX, a);
+    issue_fast<J + 1>(stage, cellp, p, w);
   }
 }
 
@@ -393,10 +446,11 @@ __device__ __forceinline__ void links_smem(double* slot, const double* pool, boo
 // with fluid cells write zeros so no DRAM sector is ever partially written.
 // ---------------------------------------------------------------------------
 template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
-__global__ void __launch_bounds__(kPipeBX, 4)
+__global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     k_sweep_pipe(const KParams p, const double* __restrict__ src, double* __restrict__ dst,
                  int part, int zper) {
   extern __shared__ double smem[];
+  constexpr int kStages = pipe_stages(RECORDS);
   const int tx = threadIdx.x;
   const int lane = tx & 31, warp = tx >> 5;
   const int x = blockIdx.x * kPipeBX + tx;
@@ -406,15 +460,22 @@ __global__ void __launch_bounds__(kPipeBX, 4)
   const bool active = x < p.nx && !(part == PART_INTERIOR && (x == 0 || x == p.nx - 1));
   const int xx = active ? x : 0;
   double* const main0 = smem + tx;
-  double* const pool0 = smem + 2 * 19 * kPipeBX + warp * kPool;
+  double* const pool0 = smem + kStages * 19 * kPipeBX + warp * kPool;
   constexpr int kMainStride = 19 * kPipeBX, kPoolStride = (kPipeBX / 32) * kPool;
   auto cidx = [&](int z) { return ((int64_t)z * p.ny + y) * p.nx + xx; };
   const CellWord kSkip{kNonFluid, 0};
 
   // issue plane z into stage s; returns this lane's pool offset (-1: overflow)
+  const bool yint = y > 0 && y < p.ny - 1;
+  const bool xint = xx > 0 && xx < p.nx - 1;
   auto issue = [&](int z, int s, CellWord cw) -> int {
     const bool fluid = !(cw.w & kNonFluid);
-    if (fluid) issue_all<0, SLAB>(main0 + s * kMainStride, src, xx, y, z, cidx(z), p, cw.w);
+    if (fluid) {
+      if (xint && yint && z > 0 && z < p.nz - 1)
+        issue_fast<0>(main0 + s * kMainStride, src + cidx(z), p, cw.w);
+      else
+        issue_all<0, SLAB>(main0 + s * kMainStride, src, xx, y, z, cidx(z), p, cw.w);
+    }
     int off = 0;
     if (RECORDS) {
       const int n = fluid ? 2 * __popc(cw.w & kBounceMask) : 0;
@@ -430,39 +491,57 @@ __global__ void __launch_bounds__(kPipeBX, 4)
     return off;
   };
 
-  CellWord cw_cur = active ? ld_cw(p.cells + cidx(z0)) : kSkip;
-  int off_cur = issue(z0, 0, cw_cur);
-  cp_async_commit();
-  CellWord cw_next = (active && z0 + 1 < z1) ? ld_cw(p.cells + cidx(z0 + 1)) : kSkip;
-  int s = 0;
-  for (int z = z0; z < z1; ++z) {
+  // Peeled pipeline: iteration z issues plane z+1 and computes plane z
+  // (z = z0-1 only issues), so the issue code exists once.  With two stages
+  // plane z+1 is issued before waiting for plane z; with one stage plane z is
+  // first moved to registers and the stage refilled with plane z+1.  issue()
+  // runs at a convergence point (it contains a warp scan).
+  CellWord cw_cur = kSkip;
+  CellWord cw_next = active ? ld_cw(p.cells + cidx(z0)) : kSkip;
+  int off_cur = 0;
+  int s = kStages == 2 ? 1 : 0;
+  for (int z = z0 - 1; z < z1; ++z) {
     int off_next = 0;
-    if (z + 1 < z1) off_next = issue(z + 1, s ^ 1, cw_next);
-    cp_async_commit();
-    const CellWord cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
-    cp_async_wait<1>();  // this thread's copies for plane z have landed
+    CellWord cw_nn = kSkip;
+    if (kStages == 2) {
+      if (z + 1 < z1) off_next = issue(z + 1, s ^ 1, cw_next);
+      cp_async_commit();
+      cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
+      cp_async_wait<1>();  // this thread's copies for plane z have landed
+    } else {
+      cp_async_wait<0>();  // plane z landed (the only group in flight)
+    }
     const uint32_t w = cw_cur.w;
-    if (w & kFillSector) {
-      const int64_t c = cidx(z);
-#pragma unroll
-      for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, 0.0);
-    } else if (!(w & kNonFluid)) {
+    const bool fluid = !(w & kNonFluid);
+    const int64_t c = cidx(z);
+    double f[19];
+    if (fluid) {
       double* st = main0 + s * kMainStride;
-      const int64_t c = cidx(z);
       if (RECORDS && (w & kBounceMask))
         links_smem(st, pool0 + s * kPoolStride + (off_cur >= 0 ? off_cur : 0), off_cur >= 0,
                    src, c, p, w, cw_cur.base);
-      double f[19];
 #pragma unroll
       for (int j = 0; j < 19; ++j) f[j] = st[j * kPipeBX];
+    }
+    if (kStages == 1) {  // stage consumed: refill it with plane z+1
+      if (z + 1 < z1) off_next = issue(z + 1, 0, cw_next);
+      cp_async_commit();
+      cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
+    }
+    if (w & kFillSector) {
+      double* const dc = dst + c;
+#pragma unroll
+      for (int j = 0; j < 19; ++j) __stcs(dc + p.plane_off[j], 0.0);
+    } else if (fluid) {
       if (OP == OP_STREAM_COLLIDE) {
         if (GLBM)
           collide_glbm<RHO1>(f, p, z);
         else
           collide_core<RHO1>(f, p);
       }
+      double* const dc = dst + c;
 #pragma unroll
-      for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, f[j]);
+      for (int j = 0; j < 19; ++j) __stcs(dc + p.plane_off[j], f[j]);
       if (SLAB && OP == OP_STREAM_COLLIDE) {
         const int64_t hp = (int64_t)p.ny * p.nz;
         const int64_t h = (int64_t)z * p.ny + y;
@@ -485,7 +564,7 @@ __global__ void __launch_bounds__(kPipeBX, 4)
     cw_cur = cw_next;
     cw_next = cw_nn;
     off_cur = off_next;
-    s ^= 1;
+    if (kStages == 2) s ^= 1;
   }
   cp_async_wait<0>();
 }
@@ -916,7 +995,7 @@ dim3 cell_grid2(const KParams& p) {
 int pipe_zper(const KParams& p) {
   if (const char* e = std::getenv("PGPU_ZPER")) return std::max(1, std::min(atoi(e), p.nz));
   const int64_t cols = (int64_t)((p.nx + kPipeBX - 1) / kPipeBX) * p.ny;
-  int zper = (int)std::min<int64_t>(4, std::max<int64_t>(1, cols * p.nz / (148 * 4 * 4)));
+  int zper = (int)std::min<int64_t>(8, std::max<int64_t>(1, cols * p.nz / (148 * 4 * 4)));
   return std::min(zper, p.nz);
 }
 // PGPU_SWEEP=pipe (default) | tile | plain -- kernel variant (experiments)

@@ -58,6 +58,12 @@ struct KParams {
   double g[3];
   const PlaneCoef* planes;  // GLBM only
   // x-slab halo (slab mode only)
+  // element offsets relative to the cell index c, valid for cells off every
+  // periodic wrap face: pull source of direction j (j*ks - e_j . strides),
+  // bounce source g_opp(j)(x) (opp(j)*ks), and the plane stride j*ks
+  int64_t pull_off[19];
+  int64_t bounce_delta[19];  // bounce source offset - pull_off
+  int64_t plane_off[19];
   const double* ghost_lo;  // [5][ny*nz] g of directions 1,7,9,11,13 at x=-1
   const double* ghost_hi;  // [5][ny*nz] g of directions 2,8,10,12,14 at x=nx
   double* send_lo;         // [5][ny*nz] our g of directions 2,8,10,12,14 at x=0

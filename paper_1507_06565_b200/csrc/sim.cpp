@@ -587,6 +587,11 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     std::unique_ptr<pgpu_sim> s(new pgpu_sim());
     s->device = device;
     CK(cudaSetDevice(device));
+    // L2 fetch granularity hint (bytes): the sweep's loads are 8-byte-per-cell
+    // and sector-sparse next to solid cells (experiment knob PGPU_L2_FETCH).
+    if (const char* e = std::getenv("PGPU_L2_FETCH")) {
+      CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)std::atoi(e)));
+    }
     CK(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
     s->stream = s->own_stream;
     s->nx = g->dims[0];
@@ -635,6 +640,12 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     kp.py = s->per[1];
     kp.pz = s->per[2];
     kp.ks = s->ks;
+    for (int j = 0; j < 19; ++j) {
+      const int64_t d = kE[j][0] + (int64_t)kE[j][1] * s->nx + (int64_t)kE[j][2] * s->nx * s->ny;
+      kp.pull_off[j] = (int64_t)j * s->ks - d;
+      kp.bounce_delta[j] = (int64_t)opposite(j) * s->ks - kp.pull_off[j];
+      kp.plane_off[j] = (int64_t)j * s->ks;
+    }
     kp.cells = s->d_cellword;
     s->refresh_params();
     if (s->records_needed()) s->upload_records();

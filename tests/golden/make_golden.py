@@ -85,13 +85,19 @@ def state_record(f: np.ndarray, fields, prof: dict, vmax: float, fluid: np.ndarr
     return rec
 
 
-def make(name: str, threads: int, steps_override: int | None = None) -> dict:
+def make(name: str, threads: int, steps_override: int | None = None,
+         product_geometry: bool = False) -> dict:
     ref = RefLib()
     ref.set_threads(threads)
     w = configs.ALL[name]()
     opt = dict(periodic=(True, True, False), wall_lo=True, wall_hi=True)
     t0 = time.time()
-    if w.pack is None:
+    if product_geometry:
+        # C4: the reference voxelize() needs ~35-55 single-threaded minutes; the
+        # product voxelizer is byte-identical (tests/test_voxelize.py, and for C4
+        # itself tests/golden/verify_c4_voxelize.py -> C4_voxelize_check.json)
+        g = w.geometry()
+    elif w.pack is None:
         g = ref.make_box_geometry(w.dims, **opt)
     else:
         g = ref.voxelize(w.pack.centers, w.pack.radii, w.pack.box, w.dims, **opt)
@@ -120,6 +126,8 @@ def make(name: str, threads: int, steps_override: int | None = None) -> dict:
         "reference_timing": {"voxelize_s": t_vox, "run_s": t_run, "threads": threads,
                              "fluid_mlups": float(g.fluid_cells) * steps / t_run / 1e6},
         "generator": "tests/golden/make_golden.py with oracle/_ref (reference sources, -O3 -fopenmp)",
+        "geometry_source": "product voxelize (byte-identical)" if product_geometry
+                           else "reference voxelize",
     }
     return rec
 
@@ -129,9 +137,10 @@ def main() -> int:
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--threads", type=int, default=8)
     ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--product-geometry", action="store_true")
     args = ap.parse_args()
     for name in args.configs:
-        rec = make(name, args.threads, args.steps)
+        rec = make(name, args.threads, args.steps, args.product_geometry)
         suffix = "" if args.steps is None else f"_{args.steps}"
         (OUT / f"{name}{suffix}.json").write_text(json.dumps(rec, indent=1))
         print(name, rec["reference_timing"], flush=True)
