@@ -305,8 +305,10 @@ def e2e_run(pg, configs, w, geom, steps, device):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     sim = configs.make_simulation(w, geom, device=device)
+    tc = time.perf_counter()
     sim.step(steps)
     sim.get_pdfs(pdf_host.reshape(19, *geom.dims[::-1]))
+    td = time.perf_counter()
     prof = sim.planar_profile()
     t1 = time.perf_counter()
     d2h = pdf_host.nbytes + 5 * prof.z.nbytes
@@ -314,7 +316,8 @@ def e2e_run(pg, configs, w, geom, steps, device):
     torch.cuda.empty_cache()
     return {"value": geom.fluid_cells * steps / (t1 - t0) / 1e6, "unit": "MLUPS",
             "h2d_bytes_per_step": h2d / steps, "d2h_bytes_per_step": d2h / steps,
-            "seconds": t1 - t0,
+            "seconds": t1 - t0, "create_s": tc - t0, "steps_and_pdf_download_s": td - tc,
+            "profile_s": t1 - td,
             "what": "pgpu_create from host geometry + K steps + pgpu_get_pdfs (pinned) + "
                     "pgpu_planar_profile"}
 

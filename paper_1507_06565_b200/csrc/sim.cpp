@@ -16,6 +16,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -198,16 +199,18 @@ struct pgpu_sim {
   // boundary.cpp:27-28 on the host: c = (1 - 2q)/(1 + 2q) from the fp32 q.
   void encode_records() {
     recs.resize(n_links);
-    for (int64_t r = 0; r < n_links; ++r) {
-      if (rec_kind[r] == kLinkCLI) {
-        const double q = rec_q[r];
-        recs[r] = (1.0 - 2.0 * q) / (1.0 + 2.0 * q);
-      } else if (rec_kind[r] == kLinkMoving) {
-        recs[r] = std::numeric_limits<double>::infinity();
-      } else {
-        recs[r] = std::numeric_limits<double>::quiet_NaN();
+    parallel_for(n_links, [&](int64_t a, int64_t b, int) {
+      for (int64_t r = a; r < b; ++r) {
+        if (rec_kind[r] == kLinkCLI) {
+          const double q = rec_q[r];
+          recs[r] = (1.0 - 2.0 * q) / (1.0 + 2.0 * q);
+        } else if (rec_kind[r] == kLinkMoving) {
+          recs[r] = std::numeric_limits<double>::infinity();
+        } else {
+          recs[r] = std::numeric_limits<double>::quiet_NaN();
+        }
       }
-    }
+    });
   }
 
   void upload_records() {
@@ -441,60 +444,100 @@ inline int wrap(int v, int n, bool periodic) {
 void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
   const int nx = s->nx, ny = s->ny, nz = s->nz;
   const uint8_t* flags = g->flags;
-  // bit0 non-fluid; bit j: upstream x - e_j is non-fluid or outside the domain
-  s->cellword.assign(s->cells, CellWord{0u, 0});
-  parallel_for(nz, [&](int64_t za, int64_t zb, int) {
-    for (int z = (int)za; z < (int)zb; ++z)
-      for (int y = 0; y < ny; ++y)
-        for (int x = 0; x < nx; ++x) {
-          const int64_t c = ((int64_t)z * ny + y) * nx + x;
-          if (flags[c] != 0) {
-            s->cellword[c].w = kNonFluid;
-            continue;
-          }
-          uint32_t w = 0;
-          for (int j = 1; j < 19; ++j) {
+  // bit0 non-fluid; bit j: upstream x - e_j is non-fluid or outside the domain.
+  // Row-wise: the 18 source rows of row (y, z) are resolved once, then a
+  // tight loop over x; only x = 0 and x = nx-1 need the wrap / ghost rules.
+  s->cellword.resize(s->cells);
+  parallel_for((int64_t)nz * ny, [&](int64_t ra, int64_t rb, int) {
+    const uint8_t* srow[19];
+    bool srow_ok[19];
+    for (int64_t r = ra; r < rb; ++r) {
+      const int z = (int)(r / ny), y = (int)(r % ny);
+      const int64_t row = r * nx;
+      for (int j = 1; j < 19; ++j) {
+        const int ys = wrap(y - kE[j][1], ny, s->per[1]);
+        const int zs = wrap(z - kE[j][2], nz, s->per[2]);
+        srow_ok[j] = ys >= 0 && zs >= 0;
+        srow[j] = srow_ok[j] ? flags + ((int64_t)zs * ny + ys) * nx : nullptr;
+      }
+      auto edge_word = [&](int x) -> uint32_t {
+        uint32_t w = 0;
+        for (int j = 1; j < 19; ++j) {
+          bool nonfluid;
+          if (!srow_ok[j]) {
+            nonfluid = true;
+          } else {
+            const int xr = x - kE[j][0];
             const int ys = wrap(y - kE[j][1], ny, s->per[1]);
             const int zs = wrap(z - kE[j][2], nz, s->per[2]);
-            bool nonfluid;
-            if (ys < 0 || zs < 0) {
-              nonfluid = true;
+            if (s->slab && xr < 0) {
+              nonfluid = g->ghost_flags_lo[(int64_t)zs * ny + ys] != 0;
+            } else if (s->slab && xr >= nx) {
+              nonfluid = g->ghost_flags_hi[(int64_t)zs * ny + ys] != 0;
             } else {
-              const int xr = x - kE[j][0];
-              if (s->slab && xr < 0) {
-                nonfluid = g->ghost_flags_lo[(int64_t)zs * ny + ys] != 0;
-              } else if (s->slab && xr >= nx) {
-                nonfluid = g->ghost_flags_hi[(int64_t)zs * ny + ys] != 0;
-              } else {
-                const int xs = s->slab ? xr : wrap(xr, nx, s->per[0]);
-                nonfluid = xs < 0 || flags[((int64_t)zs * ny + ys) * nx + xs] != 0;
-              }
+              const int xs = s->slab ? xr : wrap(xr, nx, s->per[0]);
+              nonfluid = xs < 0 || srow[j][xs] != 0;
             }
-            if (nonfluid) w |= 1u << j;
           }
-          s->cellword[c].w = w;
+          if (nonfluid) w |= 1u << j;
         }
+        return w;
+      };
+      for (int x = 0; x < nx; ++x) {
+        CellWord& cw = s->cellword[row + x];
+        cw.base = 0;
+        if (flags[row + x] != 0) {
+          cw.w = kNonFluid;
+          continue;
+        }
+        if (x == 0 || x == nx - 1) {
+          cw.w = edge_word(x);
+          continue;
+        }
+        uint32_t w = 0;
+        for (int j = 1; j < 19; ++j)
+          w |= (uint32_t)(!srow_ok[j] || srow[j][x - kE[j][0]] != 0) << j;
+        cw.w = w;
+      }
+    }
   });
   // non-fluid cells sharing an aligned 4-cell (32-byte) group with fluid
   // cells are zero-filled by the sweep, so no DRAM sector is partly written
+  const int64_t ngroups = (s->cells + 3) / 4;
   if (fill_sectors) {
-    for (int64_t c0 = 0; c0 < s->cells; c0 += 4) {
-      const int64_t c1 = std::min<int64_t>(c0 + 4, s->cells);
-      bool anyfluid = false;
-      for (int64_t c = c0; c < c1; ++c) anyfluid |= !(s->cellword[c].w & kNonFluid);
-      if (!anyfluid) continue;
-      for (int64_t c = c0; c < c1; ++c)
-        if (s->cellword[c].w & kNonFluid) s->cellword[c].w |= kFillSector;
-    }
+    parallel_for(ngroups, [&](int64_t a, int64_t b, int) {
+      for (int64_t gi = a; gi < b; ++gi) {
+        const int64_t c0 = gi * 4, c1 = std::min<int64_t>(c0 + 4, s->cells);
+        bool anyfluid = false;
+        for (int64_t c = c0; c < c1; ++c) anyfluid |= !(s->cellword[c].w & kNonFluid);
+        if (!anyfluid) continue;
+        for (int64_t c = c0; c < c1; ++c)
+          if (s->cellword[c].w & kNonFluid) s->cellword[c].w |= kFillSector;
+      }
+    });
   }
-  // per-cell record base (exclusive prefix of bounce counts)
-  int64_t total = 0;
-  for (int64_t c = 0; c < s->cells; ++c) {
-    s->cellword[c].base = (int32_t)total;
+  // per-cell record base: exclusive prefix of bounce counts (two-pass parallel scan)
+  const int nt = hw_threads();
+  std::vector<int64_t> part(nt + 1, 0);
+  auto count_of = [&](int64_t c) -> int64_t {
     const uint32_t w = s->cellword[c].w;
-    if (!(w & kNonFluid)) total += __builtin_popcount(w & kBounceMask);
-    if (total > std::numeric_limits<int32_t>::max()) throw ConfigError("too many boundary links");
-  }
+    return (w & kNonFluid) ? 0 : __builtin_popcount(w & kBounceMask);
+  };
+  parallel_for(s->cells, [&](int64_t a, int64_t b, int t) {
+    int64_t acc = 0;
+    for (int64_t c = a; c < b; ++c) acc += count_of(c);
+    part[t + 1] = acc;
+  }, nt);
+  for (int t = 0; t < nt; ++t) part[t + 1] += part[t];
+  const int64_t total = part[nt];
+  if (total > std::numeric_limits<int32_t>::max()) throw ConfigError("too many boundary links");
+  parallel_for(s->cells, [&](int64_t a, int64_t b, int t) {
+    int64_t acc = part[t];
+    for (int64_t c = a; c < b; ++c) {
+      s->cellword[c].base = (int32_t)acc;
+      acc += count_of(c);
+    }
+  }, nt);
   if (g->n_links != total) {
     std::ostringstream os;
     os << "boundary links (" << g->n_links << ") do not match the fluid->non-fluid lattice "
@@ -505,43 +548,59 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
   s->rec_kind.assign(total, kLinkSBB);
   s->rec_q.assign(total, 0.5f);
   std::vector<uint8_t> seen(total, 0);
+  std::vector<int64_t> fallbacks(nt, 0);
+  std::vector<uint8_t> moving_any(nt, 0);
+  std::vector<std::string> errs(nt);
+  parallel_for(g->n_links, [&](int64_t a, int64_t b, int t) {
+    try {
+      for (int64_t i = a; i < b; ++i) {
+        const int64_t c = g->link_fluid_cell[i];
+        const int k = g->link_direction[i];
+        if (c < 0 || c >= s->cells || flags[c] != 0)
+          throw ConfigError("boundary link on a non-fluid or out-of-range cell");
+        if (k < 1 || k > 18) throw ConfigError("boundary link direction must be in 1..18");
+        const int j = opposite(k);
+        const uint32_t w = s->cellword[c].w;
+        if (!((w >> j) & 1u)) throw ConfigError("boundary link points to a fluid neighbour");
+        const int64_t r = s->cellword[c].base + __builtin_popcount(w & ((1u << j) - 1u) & kBounceMask);
+        if (__atomic_exchange_n(&seen[r], (uint8_t)1, __ATOMIC_RELAXED))
+          throw ConfigError("duplicate boundary link");
+        s->rec_q[r] = g->link_q[i];
+        const int64_t sf = g->link_second_fluid[i];
+        const bool moving = g->link_moving && g->link_moving[i];
+        if (s->scheme == PGPU_CLI && sf == -1) ++fallbacks[t];  // simulation.cpp:97-101
+        if (moving) {
+          s->rec_kind[r] = kLinkMoving;
+          moving_any[t] = 1;
+        } else if (s->scheme == PGPU_CLI && sf != -1) {
+          // second_fluid must be the upstream cell x - e_k, which is then fluid
+          if ((w >> k) & 1u) throw ConfigError("CLI second_fluid is not a fluid cell");
+          const int x = (int)(c % nx), y = (int)((c / nx) % ny), z = (int)(c / ((int64_t)nx * ny));
+          const int xr = x - kE[k][0];
+          const int ys = wrap(y - kE[k][1], ny, s->per[1]);
+          const int zs = wrap(z - kE[k][2], nz, s->per[2]);
+          bool ok;
+          if (s->slab && (xr < 0 || xr >= nx)) {
+            ok = sf == -2;
+          } else {
+            const int xs = s->slab ? xr : wrap(xr, nx, s->per[0]);
+            ok = sf == ((int64_t)zs * ny + ys) * nx + xs;
+          }
+          if (!ok) throw ConfigError("CLI second_fluid must be the cell x_f1 - e_k");
+          s->rec_kind[r] = kLinkCLI;
+        }
+      }
+    } catch (const std::exception& e) {
+      errs[t] = e.what();
+    }
+  }, nt);
+  for (const std::string& e : errs)
+    if (!e.empty()) throw ConfigError(e);
   s->any_moving = false;
   s->cli_fallbacks = 0;
-  for (int64_t i = 0; i < g->n_links; ++i) {
-    const int64_t c = g->link_fluid_cell[i];
-    const int k = g->link_direction[i];
-    if (c < 0 || c >= s->cells || flags[c] != 0) throw ConfigError("boundary link on a non-fluid or out-of-range cell");
-    if (k < 1 || k > 18) throw ConfigError("boundary link direction must be in 1..18");
-    const int j = opposite(k);
-    const uint32_t w = s->cellword[c].w;
-    if (!((w >> j) & 1u)) throw ConfigError("boundary link points to a fluid neighbour");
-    const int64_t r = s->cellword[c].base + __builtin_popcount(w & ((1u << j) - 1u) & kBounceMask);
-    if (seen[r]) throw ConfigError("duplicate boundary link");
-    seen[r] = 1;
-    s->rec_q[r] = g->link_q[i];
-    const int64_t sf = g->link_second_fluid[i];
-    const bool moving = g->link_moving && g->link_moving[i];
-    if (s->scheme == PGPU_CLI && sf == -1) ++s->cli_fallbacks;  // simulation.cpp:97-101
-    if (moving) {
-      s->rec_kind[r] = kLinkMoving;
-      s->any_moving = true;
-    } else if (s->scheme == PGPU_CLI && sf != -1) {
-      // second_fluid must be the upstream cell x - e_k, which is then fluid
-      if ((w >> k) & 1u) throw ConfigError("CLI second_fluid is not a fluid cell");
-      const int x = (int)(c % nx), y = (int)((c / nx) % ny), z = (int)(c / ((int64_t)nx * ny));
-      const int xr = x - kE[k][0];
-      const int ys = wrap(y - kE[k][1], ny, s->per[1]);
-      const int zs = wrap(z - kE[k][2], nz, s->per[2]);
-      bool ok;
-      if (s->slab && (xr < 0 || xr >= nx)) {
-        ok = sf == -2;
-      } else {
-        const int xs = s->slab ? xr : wrap(xr, nx, s->per[0]);
-        ok = sf == ((int64_t)zs * ny + ys) * nx + xs;
-      }
-      if (!ok) throw ConfigError("CLI second_fluid must be the cell x_f1 - e_k");
-      s->rec_kind[r] = kLinkCLI;
-    }
+  for (int t = 0; t < nt; ++t) {
+    s->cli_fallbacks += (int32_t)fallbacks[t];
+    s->any_moving = s->any_moving || moving_any[t];
   }
 }
 
@@ -616,8 +675,18 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     s->lo = g->wall_plane_lo;
     s->hi = g->wall_plane_hi;
     s->fluid_cells = g->fluid_cells;
+    const bool trace = std::getenv("PGPU_TRACE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!trace) return;
+      const auto t1 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[pgpu] create %-22s %8.1f ms\n", what,
+                   std::chrono::duration<double, std::milli>(t1 - t0).count());
+      t0 = t1;
+    };
     const char* fill_env = std::getenv("PGPU_FILL_SECTORS");
     build_links(s.get(), g, !(fill_env && fill_env[0] == '0'));
+    lap("build_links");
 
     // device buffers: two full PDF grids, zero-filled like the reference
     const size_t fbytes = sizeof(double) * 19 * (size_t)s->ks;
@@ -647,9 +716,11 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
       kp.plane_off[j] = (int64_t)j * s->ks;
     }
     kp.cells = s->d_cellword;
+    lap("alloc+upload cellword");
     s->refresh_params();
     if (s->records_needed()) s->upload_records();
     CK(cudaStreamSynchronize(s->stream));
+    lap("records");
     *out = s.release();
   });
 }
