@@ -1036,6 +1036,9 @@ void launch_sweep_t(const KParams& p, const double* src, double* dst, int part,
     static bool attr = [] {
       cudaFuncSetAttribute(k_sweep_pipe<RHO1, GLBM, RECORDS, SLAB, OP>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, pipe_smem(RECORDS));
+      if (const char* e = std::getenv("PGPU_CARVEOUT"))  // experiment knob (percent)
+        cudaFuncSetAttribute(k_sweep_pipe<RHO1, GLBM, RECORDS, SLAB, OP>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
       return true;
     }();
     (void)attr;
