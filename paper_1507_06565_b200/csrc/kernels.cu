@@ -12,6 +12,7 @@
 // intrinsics (__dadd_rn, __dmul_rn, ...) in the reference's expression order,
 // so no FMA is ever contracted and the result is bit-identical to the
 // reference CPU solver (x86-64 baseline, which has no FMA).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
@@ -21,6 +22,7 @@
 #include "kparams.h"
 
 namespace pgpu {
+namespace cg = cooperative_groups;
 
 #define DADD(a, b) __dadd_rn((a), (b))
 #define DSUB(a, b) __dsub_rn((a), (b))
@@ -194,6 +196,12 @@ __device__ __forceinline__ void collide_glbm(double (&fk)[19], const KParams& p,
 // the cell's bounce bit.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+// L2-coherent load for state written earlier in the same (persistent) kernel.
+template <bool COHERENT>
+__device__ __forceinline__ double ldstate(const double* p) {
+  if constexpr (COHERENT) return __ldcg(p);
+  else return __ldg(p);
+}
 
 template <int J, bool SLAB>
 __device__ __forceinline__ const double* pull_addr(const double* __restrict__ src, int x, int y,
@@ -218,17 +226,17 @@ __device__ __forceinline__ const double* pull_addr(const double* __restrict__ sr
   return src + (int64_t)J * p.ks + ((int64_t)zs * p.ny + ys) * p.nx + xs;
 }
 
-template <int J, bool SLAB>
+template <int J, bool SLAB, bool COHERENT = false>
 __device__ __forceinline__ void load_all(double (&f)[19], const double* __restrict__ src, int x,
                                          int y, int z, int64_t c, const KParams& p, uint32_t w) {
   if constexpr (J < 19) {
-    f[J] = ldg(pull_addr<J, SLAB>(src, x, y, z, c, p, w));
-    load_all<J + 1, SLAB>(f, src, x, y, z, c, p, w);
+    f[J] = ldstate<COHERENT>(pull_addr<J, SLAB>(src, x, y, z, c, p, w));
+    load_all<J + 1, SLAB, COHERENT>(f, src, x, y, z, c, p, w);
   }
 }
 
 // Second phase for CLI / moving-wall links: f[J] already holds g_k(x).
-template <int J>
+template <int J, bool COHERENT = false>
 __device__ __forceinline__ void links_all(double (&f)[19], const double* __restrict__ src,
                                           int64_t c, const KParams& p, uint32_t w, int32_t base) {
   if constexpr (J < 19) {
@@ -236,7 +244,7 @@ __device__ __forceinline__ void links_all(double (&f)[19], const double* __restr
       constexpr int K = opp(J);
       const int32_t r = base + __popc(w & ((1u << J) - 1u) & kBounceMask);
       const double rec = __ldg(p.links + r);
-      const double gj = ldg(src + (int64_t)J * p.ks + c);  // g_kb(x_f1), boundary.cpp:29-31
+      const double gj = ldstate<COHERENT>(src + (int64_t)J * p.ks + c);  // g_kb(x_f1), boundary.cpp:29-31
       if (rec == rec) {
         if (!isinf(rec)) {  // CLI, boundary.cpp:24-32: ((c*a) - (c*b)) + d
           f[J] = DADD(DSUB(DMUL(rec, f[K]), DMUL(rec, gj)), f[J]);
@@ -245,11 +253,11 @@ __device__ __forceinline__ void links_all(double (&f)[19], const double* __restr
         }
       }  // NaN: simple bounce-back, f[J] = g_k(x) already
     }
-    links_all<J + 1>(f, src, c, p, w, base);
+    links_all<J + 1, COHERENT>(f, src, c, p, w, base);
   }
 }
 
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP, bool COHERENT = false>
 __device__ __forceinline__ void sweep_cell(const KParams& p, const double* __restrict__ src,
                                            double* __restrict__ dst, int x, int y, int z,
                                            CellWord cw) {
@@ -263,8 +271,8 @@ __device__ __forceinline__ void sweep_cell(const KParams& p, const double* __res
     return;
   }
   double f[19];
-  load_all<0, SLAB>(f, src, x, y, z, c, p, w);
-  if (RECORDS && (w & kBounceMask)) links_all<1>(f, src, c, p, w, cw.base);
+  load_all<0, SLAB, COHERENT>(f, src, x, y, z, c, p, w);
+  if (RECORDS && (w & kBounceMask)) links_all<1, COHERENT>(f, src, c, p, w, cw.base);
   if (OP == OP_STREAM_COLLIDE) {
     if (GLBM)
       collide_glbm<RHO1>(f, p, z);
@@ -806,6 +814,33 @@ __global__ void __launch_bounds__(32 * kTileWarps, 4)
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// Persistent sweep for L2-resident domains (e.g. C1, 20 MB of state): ONE
+// cooperative launch runs `nsteps` K1 sweeps, ping-ponging the two buffers,
+// with a grid-wide barrier between steps instead of a kernel boundary.  The
+// evolving state is read with L2-coherent loads (written by other blocks in
+// the same launch); the grid barrier orders the steps.
+// ---------------------------------------------------------------------------
+template <bool RHO1, bool GLBM, bool RECORDS>
+__global__ void __launch_bounds__(128) k_sweep_persistent(const KParams p, double* a, double* b,
+                                                          int64_t nsteps) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t cells = (int64_t)p.nx * p.ny * p.nz;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = 0; s < nsteps; ++s) {
+    const double* src = (s & 1) ? b : a;
+    double* dst = (s & 1) ? a : b;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += stride) {
+      const int x = (int)(c % p.nx);
+      const int64_t r = c / p.nx;
+      const int y = (int)(r % p.ny), z = (int)(r / p.ny);
+      sweep_cell<RHO1, GLBM, RECORDS, false, OP_STREAM_COLLIDE, true>(p, src, dst, x, y, z,
+                                                                      ld_cw(p.cells + c));
+    }
+    grid.sync();
+  }
+}
+
 // Edge columns x = 0 and x = nx-1 only (slab overlap path).
 template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(128) k_sweep_edges(const KParams p,
@@ -1090,6 +1125,43 @@ void launch_sweep(const SweepConfig& cfg, const KParams& p, const double* src, d
     else
       dispatch_rec<false, false>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
   }
+}
+
+template <bool RHO1, bool GLBM, bool RECORDS>
+int64_t persistent_t(const KParams& p, double* a, double* b, int64_t nsteps, cudaStream_t s) {
+  auto kern = k_sweep_persistent<RHO1, GLBM, RECORDS>;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0);
+  const int64_t cells = (int64_t)p.nx * p.ny * p.nz;
+  const int64_t want = (cells + 127) / 128;
+  const int blocks = (int)std::min<int64_t>(want, (int64_t)sms * per_sm);
+  if (blocks < 1) return -1;
+  KParams pp = p;
+  void* args[] = {(void*)&pp, (void*)&a, (void*)&b, (void*)&nsteps};
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks), dim3(128), args, 0, s) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+}
+
+int launch_sweep_persistent(const SweepConfig& cfg, const KParams& p, double* a, double* b,
+                            int64_t nsteps, cudaStream_t s) {
+  const bool rho1 = p.rho0 == 1.0;
+  int64_t r;
+  if (rho1) {
+    if (cfg.glbm) r = cfg.records ? persistent_t<true, true, true>(p, a, b, nsteps, s)
+                                  : persistent_t<true, true, false>(p, a, b, nsteps, s);
+    else r = cfg.records ? persistent_t<true, false, true>(p, a, b, nsteps, s)
+                         : persistent_t<true, false, false>(p, a, b, nsteps, s);
+  } else {
+    if (cfg.glbm) r = cfg.records ? persistent_t<false, true, true>(p, a, b, nsteps, s)
+                                  : persistent_t<false, true, false>(p, a, b, nsteps, s);
+    else r = cfg.records ? persistent_t<false, false, true>(p, a, b, nsteps, s)
+                         : persistent_t<false, false, false>(p, a, b, nsteps, s);
+  }
+  return (int)r;
 }
 
 void launch_collide_inplace(bool glbm, bool slab, const KParams& p, double* buf,

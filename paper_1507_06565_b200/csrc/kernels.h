@@ -17,6 +17,10 @@ struct SweepConfig {
 
 void launch_sweep(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
                   cudaStream_t s);
+// One cooperative launch running nsteps K1 sweeps (a -> b -> a ...); returns 0
+// on success, -1 if the cooperative launch is not possible.
+int launch_sweep_persistent(const SweepConfig& cfg, const KParams& p, double* a, double* b,
+                            int64_t nsteps, cudaStream_t s);
 void launch_collide_inplace(bool glbm, bool slab, const KParams& p, double* buf,
                             cudaStream_t s);
 void launch_macro_fields(bool glbm, const KParams& p, const double* f, double* drho,

@@ -225,17 +225,28 @@ def test_state_machine_interleaving(gpu, orc):
     compare_all(sim, o, geom, "c")
 
 
-def test_graph_path_equals_single_steps(gpu):
+@pytest.mark.parametrize("persistent", ["1", "0"])
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_multistep_paths_equal_single_steps(gpu, orc, monkeypatch, persistent, scheme):
+    """step(n) uses the persistent cooperative kernel (L2-resident domains) or
+    CUDA graphs of K1 launches; both must equal n single steps and the oracle."""
     pg = gpu
+    monkeypatch.setenv("PGPU_PERSISTENT", persistent)
     geom = sphere_geometry(pg, dims=(32, 16, 24), n=5, seed=8)
     p = pg.relaxation_from_magic(0.1, 3.0 / 16.0)
     p.body_force = (1e-6, 0, 0)
-    a = pg.Simulation.from_params(geom, p, pg.WallScheme.CLI)
-    b = pg.Simulation.from_params(geom, p, pg.WallScheme.CLI)
-    a.step(50)
-    for _ in range(50):
+    a = pg.Simulation.from_params(geom, p, pg.WallScheme(scheme))
+    b = pg.Simulation.from_params(geom, p, pg.WallScheme(scheme))
+    a.step(51)
+    for _ in range(51):
         b.step(1)
     assert np.array_equal(a.get_pdfs(), b.get_pdfs())
+    o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, scheme)
+    o.step(51)
+    fl = fluid_mask(geom)
+    assert np.array_equal(a.get_pdfs()[:, fl], o.get_pdfs()[:, fl])
+    if persistent == "1":
+        assert a.launch_count < 10  # one cooperative launch for the 50 K1 steps
 
 
 def test_nonfinite_guard(gpu):
