@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(128, PGPU_SWEEP_MINB) k_sweep(const KParams p,
   }
 }
 
-// Asynchronous-copy pipeline helpers (k_sweep_pipe / k_sweep_tile).
+// Asynchronous-copy pipeline helpers (k_sweep_pipe).
 constexpr int kPipeBX = 128;
 // Pipeline depth per variant (measured on C4, round 1): SBB sweeps keep two
 // shared-memory stages at 4 blocks/SM; sweeps with link records (CLI /
@@ -339,11 +339,14 @@ constexpr int kPipeBX = 128;
 __host__ __device__ constexpr int pipe_stages(bool records) { return records ? 1 : 2; }
 __host__ __device__ constexpr int pipe_minb(bool records) { return records ? 5 : 4; }
 #ifndef PGPU_POOL
-#define PGPU_POOL 96
+#define PGPU_POOL 192
 #endif
 constexpr int kPool = PGPU_POOL;  // per-warp, per-stage slots for CLI / moving-wall extras
+constexpr int kLinkCap = kPool / 2;  // link entries per warp and stage (2 pool slots each)
+// per stage: 19 population slots per thread + per warp (pool + descriptors)
 __host__ __device__ constexpr int pipe_smem(bool records) {
-  return pipe_stages(records) * (19 * kPipeBX + (records ? (kPipeBX / 32) * kPool : 0)) *
+  return pipe_stages(records) *
+         (19 * kPipeBX + (records ? (kPipeBX / 32) * (kPool + kLinkCap) : 0)) *
          (int)sizeof(double);
 }
 
@@ -396,48 +399,53 @@ __device__ __forceinline__ int warp_excl_scan(int n, int lane, int* total) {
   return v - n;
 }
 
-// Extras of the bounce directions of one cell (ascending j): the link record
-// and g_j(x), two pool slots per bounce direction.
-__device__ __forceinline__ void issue_extras(double* pool, const double* __restrict__ src,
-                                             int64_t c, const KParams& p, uint32_t w,
-                                             int32_t base) {
+// Warp-cooperative link handling.  A warp's bounce links of one plane form a
+// list (entry e = owner lane's i-th bounce direction, ordered by a warp
+// prefix sum).  Owners publish a descriptor per entry {record index,
+// owner thread << 8 | j}; then all 32 lanes issue the record / g_j(x) copies
+// and later apply the closures round-robin over the list, so a warp iterates
+// ceil(links / 32) times instead of as often as its busiest lane.
+struct LinkDesc {
+  int32_t rec;  // index into p.links
+  int32_t oj;   // owner thread << 8 | j
+};
+
+__device__ __forceinline__ void publish_links(LinkDesc* desc, uint32_t w, int32_t base, int off,
+                                              int tx) {
   uint32_t m = w & kBounceMask;
   int i = 0;
   while (m) {
     const int j = __ffs(m) - 1;
     m &= m - 1;
-    cp_async8(pool + 2 * i, p.links + base + i);
-    cp_async8(pool + 2 * i + 1, src + (int64_t)j * p.ks + c);
+    const int e = off + i;
+    if (e < kLinkCap) desc[e] = LinkDesc{base + i, (tx << 8) | j};
     ++i;
   }
 }
 
-// CLI / moving-wall closure applied in shared memory before the gather: the
-// stage slot of bounce direction j holds g_k(x) and the slot of k = opp(j)
-// holds the pull value g_k(x - e_k) (boundary.cpp:24-41, same arithmetic as
-// links_all).  Records and g_j(x) come from the pool, or directly from global
-// memory for lanes whose pool allocation overflowed.  A loop over the set
-// bits keeps the code small.
-__device__ __forceinline__ void links_smem(double* slot, const double* pool, bool from_pool,
-                                           const double* __restrict__ src, int64_t c,
-                                           const KParams& p, uint32_t w, int32_t base) {
-  uint32_t m = w & kBounceMask;
-  int i = 0;
-  while (m) {
-    const int j = __ffs(m) - 1;
-    m &= m - 1;
+__device__ __forceinline__ void issue_links(double* pool, const LinkDesc* desc, int n, int lane,
+                                            const double* __restrict__ src, int64_t row_cell0,
+                                            const KParams& p) {
+  for (int e = lane; e < n; e += 32) {
+    const LinkDesc d = desc[e];
+    const int j = d.oj & 31;
+    cp_async8(pool + 2 * e, p.links + d.rec);
+    cp_async8(pool + 2 * e + 1, src + row_cell0 + (d.oj >> 8) + (int64_t)j * p.ks);
+  }
+}
+
+// Closure of one entry (boundary.cpp:24-41 in pull form, same arithmetic as
+// links_all): slot j of the owner holds g_k(x), slot k the pull value.
+__device__ __forceinline__ void close_link(double* stage_base, int owner, int j, double rec,
+                                           double gj, const KParams& p) {
+  if (rec == rec) {
     const int k = (j & 1) ? j + 1 : j - 1;
-    const double rec = from_pool ? pool[2 * i] : __ldg(p.links + base + i);
-    if (rec == rec) {
-      const double gk = slot[j * kPipeBX];
-      if (!isinf(rec)) {
-        const double gj = from_pool ? pool[2 * i + 1] : __ldg(src + (int64_t)j * p.ks + c);
-        slot[j * kPipeBX] = DADD(DSUB(DMUL(rec, slot[k * kPipeBX]), DMUL(rec, gj)), gk);
-      } else {
-        slot[j * kPipeBX] = DSUB(gk, p.mw[k]);
-      }
-    }
-    ++i;
+    double* sj = stage_base + j * kPipeBX + owner;
+    const double gk = *sj;
+    if (!isinf(rec))
+      *sj = DADD(DSUB(DMUL(rec, stage_base[k * kPipeBX + owner]), DMUL(rec, gj)), gk);
+    else
+      *sj = DSUB(gk, p.mw[k]);
   }
 }
 
@@ -468,14 +476,18 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   const bool active = x < p.nx && !(part == PART_INTERIOR && (x == 0 || x == p.nx - 1));
   const int xx = active ? x : 0;
   double* const main0 = smem + tx;
-  double* const pool0 = smem + kStages * 19 * kPipeBX + warp * kPool;
-  constexpr int kMainStride = 19 * kPipeBX, kPoolStride = (kPipeBX / 32) * kPool;
+  constexpr int kMainStride = 19 * kPipeBX;
+  constexpr int kWarpExtra = kPool + kLinkCap;              // doubles per warp per stage
+  constexpr int kExtraStride = (kPipeBX / 32) * kWarpExtra;  // per stage
+  double* const pool0 = smem + kStages * kMainStride + warp * kWarpExtra;
+  LinkDesc* const desc0 = reinterpret_cast<LinkDesc*>(pool0 + kPool);
   auto cidx = [&](int z) { return ((int64_t)z * p.ny + y) * p.nx + xx; };
   const CellWord kSkip{kNonFluid, 0};
 
   // issue plane z into stage s; returns this lane's pool offset (-1: overflow)
   const bool yint = y > 0 && y < p.ny - 1;
   const bool xint = xx > 0 && xx < p.nx - 1;
+  int lane_off = 0;  // this lane's first entry in the warp's link list (last issue)
   auto issue = [&](int z, int s, CellWord cw) -> int {
     const bool fluid = !(cw.w & kNonFluid);
     if (fluid) {
@@ -484,19 +496,20 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
       else
         issue_all<0, SLAB>(main0 + s * kMainStride, src, xx, y, z, cidx(z), p, cw.w);
     }
-    int off = 0;
+    int total = 0;
     if (RECORDS) {
-      const int n = fluid ? 2 * __popc(cw.w & kBounceMask) : 0;
-      int total;
-      off = warp_excl_scan(n, lane, &total);
-      if (n) {
-        if (off + n <= kPool)
-          issue_extras(pool0 + s * kPoolStride + off, src, cidx(z), p, cw.w, cw.base);
-        else
-          off = -1;
+      const int n = fluid ? __popc(cw.w & kBounceMask) : 0;
+      const int off = warp_excl_scan(n, lane, &total);
+      lane_off = off;
+      if (total) {
+        LinkDesc* desc = reinterpret_cast<LinkDesc*>(pool0 + s * kExtraStride + kPool);
+        if (n) publish_links(desc, cw.w, cw.base, off, tx);
+        __syncwarp();
+        issue_links(pool0 + s * kExtraStride, desc, min(total, kLinkCap), lane, src,
+                    cidx(z) - xx + blockIdx.x * kPipeBX, p);
       }
     }
-    return off;
+    return total;
   };
 
   // Peeled pipeline: iteration z issues plane z+1 and computes plane z
@@ -506,13 +519,14 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   // runs at a convergence point (it contains a warp scan).
   CellWord cw_cur = kSkip;
   CellWord cw_next = active ? ld_cw(p.cells + cidx(z0)) : kSkip;
-  int off_cur = 0;
+  int off_cur = 0, lane_off_cur = 0;
   int s = kStages == 2 ? 1 : 0;
   for (int z = z0 - 1; z < z1; ++z) {
-    int off_next = 0;
+    int off_next = 0, lane_off_next = 0;
     CellWord cw_nn = kSkip;
     if (kStages == 2) {
       if (z + 1 < z1) off_next = issue(z + 1, s ^ 1, cw_next);
+      lane_off_next = lane_off;
       cp_async_commit();
       cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
       cp_async_wait<1>();  // this thread's copies for plane z have landed
@@ -523,16 +537,40 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     const bool fluid = !(w & kNonFluid);
     const int64_t c = cidx(z);
     double f[19];
+    if (RECORDS && off_cur) {  // off_cur: this warp's link count for plane z
+      __syncwarp();            // every lane's copies of plane z have landed
+      double* stage_base = smem + s * kMainStride + warp * 32;
+      const double* pool = pool0 + s * kExtraStride;
+      const LinkDesc* desc = reinterpret_cast<const LinkDesc*>(pool + kPool);
+      const int ncoop = min(off_cur, kLinkCap);
+      for (int e = lane; e < ncoop; e += 32) {
+        const LinkDesc d = desc[e];
+        close_link(stage_base - warp * 32, d.oj >> 8, d.oj & 31, pool[2 * e], pool[2 * e + 1], p);
+      }
+      if (off_cur > kLinkCap && fluid && (w & kBounceMask)) {
+        // pool overflow: this lane closes its own entries past the cap directly
+        const int off = lane_off_cur;
+        uint32_t m = w & kBounceMask;
+        int i = 0;
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          if (off + i >= kLinkCap)
+            close_link(smem + s * kMainStride, tx, j, __ldg(p.links + cw_cur.base + i),
+                       ldg(src + (int64_t)j * p.ks + c), p);
+          ++i;
+        }
+      }
+      __syncwarp();  // closures of other lanes' cells are visible
+    }
     if (fluid) {
-      double* st = main0 + s * kMainStride;
-      if (RECORDS && (w & kBounceMask))
-        links_smem(st, pool0 + s * kPoolStride + (off_cur >= 0 ? off_cur : 0), off_cur >= 0,
-                   src, c, p, w, cw_cur.base);
+      const double* st = main0 + s * kMainStride;
 #pragma unroll
       for (int j = 0; j < 19; ++j) f[j] = st[j * kPipeBX];
     }
     if (kStages == 1) {  // stage consumed: refill it with plane z+1
       if (z + 1 < z1) off_next = issue(z + 1, 0, cw_next);
+      lane_off_next = lane_off;
       cp_async_commit();
       cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
     }
@@ -572,244 +610,8 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     cw_cur = cw_next;
     cw_next = cw_nn;
     off_cur = off_next;
+    lane_off_cur = lane_off_next;
     if (kStages == 2) s ^= 1;
-  }
-  cp_async_wait<0>();
-}
-
-// ---------------------------------------------------------------------------
-// K1 main sweep, tile form (default).  Each WARP owns 32 consecutive cells of
-// one x row and marches through `zper` z-planes on its own (no block
-// barriers).  For every direction plane j it copies the 36-cell source span
-// [x0-2, x0+34) of row (y-e_jy, z-e_jz) into shared memory with 16-byte
-// cp.async.cg copies (L2 -> smem, no L1 allocation), predicated per cell pair
-// by a warp ballot of the lanes whose pull needs that pair -- solid stretches
-// are not fetched.  Bounce-closure values (g_k(x), the link record, g_j(x))
-// go through a per-warp pool allocated by a warp prefix sum.  Two stages:
-// plane z+1 is in flight while plane z is collided.
-// ---------------------------------------------------------------------------
-constexpr int kTileW = 36;                  // doubles per plane span per warp
-constexpr int kTilePool = 128;              // pool slots per warp per stage
-constexpr int kTileStage = 19 * kTileW + kTilePool;  // doubles per warp per stage
-constexpr int kTileWarps = 4;               // warps per block
-constexpr int kTileSmem = 2 * kTileStage * kTileWarps * (int)sizeof(double);
-
-__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
-}
-
-// Source row of plane J for row (y, z) (periodic wrap in y/z).
-template <int J>
-__device__ __forceinline__ int64_t src_row(int y, int z, const KParams& p) {
-  constexpr int ey = EY[J], ez = EZ[J];
-  int ys = y - ey, zs = z - ez;
-  if (ey == 1 && y == 0) ys = p.ny - 1;
-  if (ey == -1 && y == p.ny - 1) ys = 0;
-  if (ez == 1 && z == 0) zs = p.nz - 1;
-  if (ez == -1 && z == p.nz - 1) zs = 0;
-  return (int64_t)zs * p.ny + ys;
-}
-
-template <int J, bool SLAB>
-__device__ __forceinline__ void tile_issue_plane(double* tile, const double* __restrict__ src,
-                                                 int x0w, int y, int z, int lane, uint32_t need,
-                                                 const KParams& p) {
-  constexpr int ex = EX[J];
-  // ballot bit l: lane l pulls direction J, source cell x0w + l - ex (tile index l - ex + 2)
-  const unsigned m = __ballot_sync(0xffffffffu, need);
-  if (lane < kTileW / 2 && m) {
-    const int q = lane;  // pair q covers tile indices 2q, 2q+1
-    const int l0 = 2 * q - 2 + ex, l1 = l0 + 1;  // consumer lanes of the pair's cells
-    const bool needed = ((l0 >= 0 && l0 < 32) && ((m >> l0) & 1u)) ||
-                        ((l1 >= 0 && l1 < 32) && ((m >> l1) & 1u));
-    if (needed) {
-      const int64_t row = src_row<J>(y, z, p);
-      int s0 = x0w - 2 + 2 * q;  // global x of the pair's first cell
-      double* dst = tile + J * kTileW + 2 * q;
-      if (s0 >= 0 && s0 + 1 < p.nx) {
-        cp_async16(dst, src + (int64_t)J * p.ks + row * p.nx + s0);
-      } else if (!SLAB) {
-        s0 = s0 < 0 ? s0 + p.nx : s0 - p.nx;  // periodic wrap; nx is even
-        cp_async16(dst, src + (int64_t)J * p.ks + row * p.nx + s0);
-      } else {
-        // slab: the needed out-of-domain cell comes from the ghost column
-        const int64_t g = (int64_t)halo_slot(J) * p.ny * p.nz + row;
-        if (s0 < 0) {
-          if (((m >> 0) & 1u) && ex == 1) cp_async8(dst + 1, p.ghost_lo + g);  // x = -1
-        } else {
-          if (((m >> 31) & 1u) && ex == -1) cp_async8(dst, p.ghost_hi + g);   // x = nx
-        }
-      }
-    }
-  }
-}
-
-template <int J, bool SLAB>
-__device__ __forceinline__ void tile_issue_all(double* tile, const double* __restrict__ src,
-                                               int x0w, int y, int z, int lane, uint32_t w,
-                                               const KParams& p) {
-  if constexpr (J < 19) {
-    const bool need = !(w & kNonFluid) && (J == 0 || !((w >> J) & 1u));
-    tile_issue_plane<J, SLAB>(tile, src, x0w, y, z, lane, need, p);
-    tile_issue_all<J + 1, SLAB>(tile, src, x0w, y, z, lane, w, p);
-  }
-}
-
-// Pool layout per bounce direction (ascending j): g_k(x) [, record, g_j(x)].
-template <bool RECORDS>
-__device__ __forceinline__ void tile_issue_bounce(double* pool, const double* __restrict__ src,
-                                                  int64_t c, const KParams& p, uint32_t w,
-                                                  int32_t base) {
-  uint32_t m = w & kBounceMask;
-  int i = 0;
-  while (m) {
-    const int j = __ffs(m) - 1;
-    m &= m - 1;
-    const int k = (j & 1) ? j + 1 : j - 1;
-    if (RECORDS) {
-      cp_async8(pool + 3 * i, src + (int64_t)k * p.ks + c);
-      cp_async8(pool + 3 * i + 1, p.links + base + i);
-      cp_async8(pool + 3 * i + 2, src + (int64_t)j * p.ks + c);
-    } else {
-      cp_async8(pool + i, src + (int64_t)k * p.ks + c);
-    }
-    ++i;
-  }
-}
-
-template <int J, bool RECORDS>
-__device__ __forceinline__ void tile_gather(double (&f)[19], const double* tile,
-                                            const double* pool, int lane, uint32_t w,
-                                            const KParams& p, int i) {
-  if constexpr (J < 19) {
-    constexpr int ex = EX[J];
-    if (J != 0 && ((w >> J) & 1u)) {
-      constexpr int K = opp(J);
-      if (RECORDS) {
-        const double gk = pool[3 * i], rec = pool[3 * i + 1];
-        double v = gk;  // SBB (NaN record)
-        if (rec == rec) {
-          if (!isinf(rec))
-            v = DADD(DSUB(DMUL(rec, f[K]), DMUL(rec, pool[3 * i + 2])), gk);  // CLI
-          else
-            v = DSUB(gk, p.mw[K]);  // moving wall
-        }
-        f[J] = v;
-      } else {
-        f[J] = pool[i];
-      }
-      ++i;
-    } else {
-      f[J] = tile[J * kTileW + lane - ex + 2];
-    }
-    tile_gather<J + 1, RECORDS>(f, tile, pool, lane, w, p, i);
-  }
-}
-
-template <int J, bool SLAB>
-__device__ __forceinline__ void direct_bounce(double (&f)[19], const double* __restrict__ src,
-                                              int64_t c, const KParams& p, uint32_t w) {
-  if constexpr (J < 19) {
-    if ((w >> J) & 1u) f[J] = ldg(src + (int64_t)opp(J) * p.ks + c);
-    direct_bounce<J + 1, SLAB>(f, src, c, p, w);
-  }
-}
-
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
-__global__ void __launch_bounds__(32 * kTileWarps, 4)
-    k_sweep_tile(const KParams p, const double* __restrict__ src, double* __restrict__ dst,
-                 int part, int zper) {
-  extern __shared__ double smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x0w = (blockIdx.x * kTileWarps + warp) * 32;
-  const int x = x0w + lane;
-  const int y = blockIdx.y;
-  const int z0 = blockIdx.z * zper;
-  const int z1 = min(z0 + zper, p.nz);
-  if (x0w >= p.nx) return;  // whole warp outside (nx is a multiple of 32)
-  const bool active = !(part == PART_INTERIOR && (x == 0 || x == p.nx - 1));
-  double* const st0 = smem + (size_t)warp * 2 * kTileStage;
-  constexpr int kPoolPer = RECORDS ? 3 : 1;
-  auto cidx = [&](int z) { return ((int64_t)z * p.ny + y) * p.nx + x; };
-  const CellWord kSkip{kNonFluid, 0};
-
-  auto issue = [&](int z, int s, CellWord cw) -> int {
-    double* tile = st0 + s * kTileStage;
-    tile_issue_all<0, SLAB>(tile, src, x0w, y, z, lane, cw.w, p);
-    const bool fluid = !(cw.w & kNonFluid);
-    const int n = fluid ? kPoolPer * __popc(cw.w & kBounceMask) : 0;
-    int total;
-    int off = warp_excl_scan(n, lane, &total);
-    if (n) {
-      if (off + n <= kTilePool)
-        tile_issue_bounce<RECORDS>(tile + 19 * kTileW + off, src, cidx(z), p, cw.w, cw.base);
-      else
-        off = -1;
-    }
-    return off;
-  };
-
-  CellWord cw_cur = active ? ld_cw(p.cells + cidx(z0)) : kSkip;
-  int off_cur = issue(z0, 0, cw_cur);
-  cp_async_commit();
-  CellWord cw_next = (active && z0 + 1 < z1) ? ld_cw(p.cells + cidx(z0 + 1)) : kSkip;
-  int s = 0;
-  for (int z = z0; z < z1; ++z) {
-    int off_next = 0;
-    if (z + 1 < z1) off_next = issue(z + 1, s ^ 1, cw_next);
-    cp_async_commit();
-    const CellWord cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
-    cp_async_wait<1>();
-    __syncwarp();  // other lanes' copies of plane z are visible
-    const uint32_t w = cw_cur.w;
-    if (w & kFillSector) {
-      const int64_t c = cidx(z);
-#pragma unroll
-      for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, 0.0);
-    } else if (!(w & kNonFluid)) {
-      const double* tile = st0 + s * kTileStage;
-      const int64_t c = cidx(z);
-      double f[19];
-      if (off_cur >= 0) {
-        tile_gather<0, RECORDS>(f, tile, tile + 19 * kTileW + off_cur, lane, w, p, 0);
-      } else {  // pool overflow: bounce values loaded directly
-        tile_gather<0, false>(f, tile, tile, lane, 0u, p, 0);
-        direct_bounce<1, SLAB>(f, src, c, p, w);
-        if (RECORDS) links_all<1>(f, src, c, p, w, cw_cur.base);
-      }
-      if (OP == OP_STREAM_COLLIDE) {
-        if (GLBM)
-          collide_glbm<RHO1>(f, p, z);
-        else
-          collide_core<RHO1>(f, p);
-      }
-#pragma unroll
-      for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, f[j]);
-      if (SLAB && OP == OP_STREAM_COLLIDE) {
-        const int64_t hp = (int64_t)p.ny * p.nz;
-        const int64_t h = (int64_t)z * p.ny + y;
-        if (x == 0) {
-          p.send_lo[0 * hp + h] = f[2];
-          p.send_lo[1 * hp + h] = f[8];
-          p.send_lo[2 * hp + h] = f[10];
-          p.send_lo[3 * hp + h] = f[12];
-          p.send_lo[4 * hp + h] = f[14];
-        }
-        if (x == p.nx - 1) {
-          p.send_hi[0 * hp + h] = f[1];
-          p.send_hi[1 * hp + h] = f[7];
-          p.send_hi[2 * hp + h] = f[9];
-          p.send_hi[3 * hp + h] = f[11];
-          p.send_hi[4 * hp + h] = f[13];
-        }
-      }
-    }
-    __syncwarp();  // all lanes done reading stage s before it is refilled
-    cw_cur = cw_next;
-    cw_next = cw_nn;
-    off_cur = off_next;
-    s ^= 1;
   }
   cp_async_wait<0>();
 }
@@ -1033,13 +835,11 @@ int pipe_zper(const KParams& p) {
   int zper = (int)std::min<int64_t>(8, std::max<int64_t>(1, cols * p.nz / (148 * 4 * 4)));
   return std::min(zper, p.nz);
 }
-// PGPU_SWEEP=pipe (default) | tile | plain -- kernel variant (experiments)
+// PGPU_SWEEP=pipe (default) | plain: the async-copy pipeline, or the plain
+// one-cell-per-thread sweep kept as the round-1 reference point.
 int g_sweep_mode = [] {
   const char* e = std::getenv("PGPU_SWEEP");
-  if (!e) return 1;
-  if (e[0] == 't') return 0;
-  if (e[0] == 'p' && e[1] == 'l') return 2;
-  return 1;
+  return (e && e[0] == 'p' && e[1] == 'l') ? 2 : 1;
 }();
 dim3 sweep_grid(const KParams& p) {
   const int bx = cell_block(p).x;
@@ -1053,18 +853,6 @@ void launch_sweep_t(const KParams& p, const double* src, double* dst, int part,
     const int64_t n = 2 * (int64_t)p.ny * p.nz;
     k_sweep_edges<RHO1, GLBM, RECORDS, SLAB, OP>
         <<<(unsigned)((n + kBX - 1) / kBX), kBX, 0, s>>>(p, src, dst);
-  } else if (g_sweep_mode == 0 && p.nx % 32 == 0) {
-    const int zper = pipe_zper(p);
-    const int bx = 32 * kTileWarps;
-    const dim3 grid((p.nx + bx - 1) / bx, p.ny, (p.nz + zper - 1) / zper);
-    static bool attr = [] {
-      cudaFuncSetAttribute(k_sweep_tile<RHO1, GLBM, RECORDS, SLAB, OP>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-      return true;
-    }();
-    (void)attr;
-    k_sweep_tile<RHO1, GLBM, RECORDS, SLAB, OP><<<grid, bx, kTileSmem, s>>>(p, src, dst, part,
-                                                                            zper);
   } else if (g_sweep_mode <= 1) {
     const int zper = pipe_zper(p);
     const dim3 grid((p.nx + kPipeBX - 1) / kPipeBX, p.ny, (p.nz + zper - 1) / zper);
