@@ -399,6 +399,29 @@ __device__ __forceinline__ int warp_excl_scan(int n, int lane, int* total) {
   return v - n;
 }
 
+// Special registers read through volatile asm: values recomputed at their use
+// instead of being kept live (and spilled) across the z loop.
+__device__ __forceinline__ int v_tid_x() {
+  int r;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ int v_ctaid_x() {
+  int r;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ int v_ctaid_y() {
+  int r;
+  asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ int v_ctaid_z() {
+  int r;
+  asm volatile("mov.u32 %0, %%ctaid.z;" : "=r"(r));
+  return r;
+}
+
 // Warp-cooperative link handling.  A warp's bounce links of one plane form a
 // list (entry e = owner lane's i-th bounce direction, ordered by a warp
 // prefix sum).  Owners publish a descriptor per entry {record index,
@@ -485,13 +508,16 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   const CellWord kSkip{kNonFluid, 0};
 
   // issue plane z into stage s; returns this lane's pool offset (-1: overflow)
-  const bool yint = y > 0 && y < p.ny - 1;
-  const bool xint = xx > 0 && xx < p.nx - 1;
-  int lane_off = 0;  // this lane's first entry in the warp's link list (last issue)
+  // z-plane range end and the wrap-free predicate are recomputed where used
+  auto z_end = [&]() { return min((v_ctaid_z() + 1) * zper, p.nz); };
+  auto off_wrap = [&](int z) {
+    const int xv = v_ctaid_x() * kPipeBX + v_tid_x(), yv = v_ctaid_y();
+    return xv > 0 && xv < p.nx - 1 && yv > 0 && yv < p.ny - 1 && z > 0 && z < p.nz - 1;
+  };
   auto issue = [&](int z, int s, CellWord cw) -> int {
     const bool fluid = !(cw.w & kNonFluid);
     if (fluid) {
-      if (xint && yint && z > 0 && z < p.nz - 1)
+      if (off_wrap(z))
         issue_fast<0>(main0 + s * kMainStride, src + cidx(z), p, cw.w);
       else
         issue_all<0, SLAB>(main0 + s * kMainStride, src, xx, y, z, cidx(z), p, cw.w);
@@ -500,7 +526,6 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     if (RECORDS) {
       const int n = fluid ? __popc(cw.w & kBounceMask) : 0;
       const int off = warp_excl_scan(n, lane, &total);
-      lane_off = off;
       if (total) {
         LinkDesc* desc = reinterpret_cast<LinkDesc*>(pool0 + s * kExtraStride + kPool);
         if (n) publish_links(desc, cw.w, cw.base, off, tx);
@@ -519,16 +544,15 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   // runs at a convergence point (it contains a warp scan).
   CellWord cw_cur = kSkip;
   CellWord cw_next = active ? ld_cw(p.cells + cidx(z0)) : kSkip;
-  int off_cur = 0, lane_off_cur = 0;
+  int off_cur = 0;
   int s = kStages == 2 ? 1 : 0;
-  for (int z = z0 - 1; z < z1; ++z) {
-    int off_next = 0, lane_off_next = 0;
+  for (int z = z0 - 1; z < z_end(); ++z) {
+    int off_next = 0;
     CellWord cw_nn = kSkip;
     if (kStages == 2) {
-      if (z + 1 < z1) off_next = issue(z + 1, s ^ 1, cw_next);
-      lane_off_next = lane_off;
+      if (z + 1 < z_end()) off_next = issue(z + 1, s ^ 1, cw_next);
       cp_async_commit();
-      cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
+      cw_nn = (active && z + 2 < z_end()) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
       cp_async_wait<1>();  // this thread's copies for plane z have landed
     } else {
       cp_async_wait<0>();  // plane z landed (the only group in flight)
@@ -547,10 +571,11 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
         const LinkDesc d = desc[e];
         close_link(stage_base - warp * 32, d.oj >> 8, d.oj & 31, pool[2 * e], pool[2 * e + 1], p);
       }
-      if (off_cur > kLinkCap && fluid && (w & kBounceMask)) {
-        // pool overflow: this lane closes its own entries past the cap directly
-        const int off = lane_off_cur;
-        uint32_t m = w & kBounceMask;
+      if (off_cur > kLinkCap) {  // warp-uniform: the pool overflowed for plane z
+        // each lane closes its own entries past the cap with direct loads
+        int tot;
+        const int off = warp_excl_scan(fluid ? __popc(w & kBounceMask) : 0, lane, &tot);
+        uint32_t m = fluid ? (w & kBounceMask) : 0u;
         int i = 0;
         while (m) {
           const int j = __ffs(m) - 1;
@@ -569,10 +594,9 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
       for (int j = 0; j < 19; ++j) f[j] = st[j * kPipeBX];
     }
     if (kStages == 1) {  // stage consumed: refill it with plane z+1
-      if (z + 1 < z1) off_next = issue(z + 1, 0, cw_next);
-      lane_off_next = lane_off;
+      if (z + 1 < z_end()) off_next = issue(z + 1, 0, cw_next);
       cp_async_commit();
-      cw_nn = (active && z + 2 < z1) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
+      cw_nn = (active && z + 2 < z_end()) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
     }
     if (w & kFillSector) {
       double* const dc = dst + c;
@@ -610,7 +634,6 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     cw_cur = cw_next;
     cw_next = cw_nn;
     off_cur = off_next;
-    lane_off_cur = lane_off_next;
     if (kStages == 2) s ^= 1;
   }
   cp_async_wait<0>();
