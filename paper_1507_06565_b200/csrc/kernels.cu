@@ -301,9 +301,9 @@ __device__ __forceinline__ void sweep_cell(const KParams& p, const double* __res
   }
 }
 
-__device__ __forceinline__ CellWord ld_cw(const CellWord* p) {
-  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-  return CellWord{v.x, (int32_t)v.y};
+// Cell word and the cell's first link record (per-cell kernels).
+__device__ __forceinline__ CellWord ld_cw(const KParams& p, int64_t c) {
+  return CellWord{__ldg(p.cellw + c), __ldg(p.cellbase + c)};
 }
 
 // Each block sweeps kZPer consecutive z-planes of one (x-segment, y) column;
@@ -322,10 +322,10 @@ __global__ void __launch_bounds__(128, PGPU_SWEEP_MINB) k_sweep(const KParams p,
   if (x >= p.nx) return;
   if (part == PART_INTERIOR && (x == 0 || x == p.nx - 1)) return;
   const int z1 = min(z0 + kZPer, p.nz);
-  CellWord next = ld_cw(p.cells + ((int64_t)z0 * p.ny + y) * p.nx + x);
+  CellWord next = ld_cw(p, ((int64_t)z0 * p.ny + y) * p.nx + x);
   for (int z = z0; z < z1; ++z) {
     const CellWord cw = next;
-    if (z + 1 < z1) next = ld_cw(p.cells + ((int64_t)(z + 1) * p.ny + y) * p.nx + x);
+    if (z + 1 < z1) next = ld_cw(p, ((int64_t)(z + 1) * p.ny + y) * p.nx + x);
     sweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z, cw);
   }
 }
@@ -496,8 +496,11 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   const int y = blockIdx.y;
   const int z0 = blockIdx.z * zper;
   const int z1 = min(z0 + zper, p.nz);
-  const bool active = x < p.nx && !(part == PART_INTERIOR && (x == 0 || x == p.nx - 1));
-  const int xx = active ? x : 0;
+  // valid: a cell of the row (its links stay in the warp's link list so record
+  // indices follow from the chunk base); active: the cell is swept by this part.
+  const bool valid = x < p.nx;
+  const bool active = valid && !(part == PART_INTERIOR && (x == 0 || x == p.nx - 1));
+  const int xx = valid ? x : 0;
   double* const main0 = smem + tx;
   constexpr int kMainStride = 19 * kPipeBX;
   constexpr int kWarpExtra = kPool + kLinkCap;              // doubles per warp per stage
@@ -506,8 +509,15 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   LinkDesc* const desc0 = reinterpret_cast<LinkDesc*>(pool0 + kPool);
   auto cidx = [&](int z) { return ((int64_t)z * p.ny + y) * p.nx + xx; };
   const CellWord kSkip{kNonFluid, 0};
+  // 4-byte cell word + the warp's chunk base (uniform address: one transaction)
+  const int chunk = (blockIdx.x * kPipeBX + warp * 32) >> 5;
+  auto ld_w = [&](int z) {
+    return CellWord{__ldg(p.cellw + cidx(z)),
+                    RECORDS ? __ldg(p.chunkbase + ((int64_t)z * p.ny + y) * p.nchunk + chunk)
+                            : 0};
+  };
 
-  // issue plane z into stage s; returns this lane's pool offset (-1: overflow)
+  // issue plane z into stage s; returns the warp's link count for plane z.
   // z-plane range end and the wrap-free predicate are recomputed where used
   auto z_end = [&]() { return min((v_ctaid_z() + 1) * zper, p.nz); };
   auto off_wrap = [&](int z) {
@@ -516,7 +526,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   };
   auto issue = [&](int z, int s, CellWord cw) -> int {
     const bool fluid = !(cw.w & kNonFluid);
-    if (fluid) {
+    if (fluid && active) {
       if (off_wrap(z))
         issue_fast<0>(main0 + s * kMainStride, src + cidx(z), p, cw.w);
       else
@@ -528,7 +538,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
       const int off = warp_excl_scan(n, lane, &total);
       if (total) {
         LinkDesc* desc = reinterpret_cast<LinkDesc*>(pool0 + s * kExtraStride + kPool);
-        if (n) publish_links(desc, cw.w, cw.base, off, tx);
+        if (n) publish_links(desc, cw.w, cw.base + off, off, tx);
         __syncwarp();
         issue_links(pool0 + s * kExtraStride, desc, min(total, kLinkCap), lane, src,
                     cidx(z) - xx + blockIdx.x * kPipeBX, p);
@@ -543,7 +553,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   // first moved to registers and the stage refilled with plane z+1.  issue()
   // runs at a convergence point (it contains a warp scan).
   CellWord cw_cur = kSkip;
-  CellWord cw_next = active ? ld_cw(p.cells + cidx(z0)) : kSkip;
+  CellWord cw_next = valid ? ld_w(z0) : kSkip;
   int off_cur = 0;
   int s = kStages == 2 ? 1 : 0;
   for (int z = z0 - 1; z < z_end(); ++z) {
@@ -552,12 +562,12 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     if (kStages == 2) {
       if (z + 1 < z_end()) off_next = issue(z + 1, s ^ 1, cw_next);
       cp_async_commit();
-      cw_nn = (active && z + 2 < z_end()) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
+      cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
       cp_async_wait<1>();  // this thread's copies for plane z have landed
     } else {
       cp_async_wait<0>();  // plane z landed (the only group in flight)
     }
-    const uint32_t w = cw_cur.w;
+    const uint32_t w = active ? cw_cur.w : kNonFluid;
     const bool fluid = !(w & kNonFluid);
     const int64_t c = cidx(z);
     double f[19];
@@ -574,14 +584,15 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
       if (off_cur > kLinkCap) {  // warp-uniform: the pool overflowed for plane z
         // each lane closes its own entries past the cap with direct loads
         int tot;
-        const int off = warp_excl_scan(fluid ? __popc(w & kBounceMask) : 0, lane, &tot);
+        const bool lf = !(cw_cur.w & kNonFluid);  // same counting as issue()
+        const int off = warp_excl_scan(lf ? __popc(cw_cur.w & kBounceMask) : 0, lane, &tot);
         uint32_t m = fluid ? (w & kBounceMask) : 0u;
         int i = 0;
         while (m) {
           const int j = __ffs(m) - 1;
           m &= m - 1;
           if (off + i >= kLinkCap)
-            close_link(smem + s * kMainStride, tx, j, __ldg(p.links + cw_cur.base + i),
+            close_link(smem + s * kMainStride, tx, j, __ldg(p.links + cw_cur.base + off + i),
                        ldg(src + (int64_t)j * p.ks + c), p);
           ++i;
         }
@@ -596,7 +607,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     if (kStages == 1) {  // stage consumed: refill it with plane z+1
       if (z + 1 < z_end()) off_next = issue(z + 1, 0, cw_next);
       cp_async_commit();
-      cw_nn = (active && z + 2 < z_end()) ? ld_cw(p.cells + cidx(z + 2)) : kSkip;
+      cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
     }
     if (w & kFillSector) {
       double* const dc = dst + c;
@@ -660,7 +671,7 @@ __global__ void __launch_bounds__(128) k_sweep_persistent(const KParams p, doubl
       const int64_t r = c / p.nx;
       const int y = (int)(r % p.ny), z = (int)(r / p.ny);
       sweep_cell<RHO1, GLBM, RECORDS, false, OP_STREAM_COLLIDE, true>(p, src, dst, x, y, z,
-                                                                      ld_cw(p.cells + c));
+                                                                      ld_cw(p, c));
     }
     grid.sync();
   }
@@ -679,7 +690,7 @@ __global__ void __launch_bounds__(128) k_sweep_edges(const KParams p,
   const int z = (int)(h / p.ny), y = (int)(h - (int64_t)z * p.ny);
   const int x = side ? p.nx - 1 : 0;
   if (side == 1 && p.nx == 1) return;
-  const CellWord cw = ld_cw(p.cells + ((int64_t)z * p.ny + y) * p.nx + x);
+  const CellWord cw = ld_cw(p, ((int64_t)z * p.ny + y) * p.nx + x);
   sweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z, cw);
 }
 
@@ -690,7 +701,7 @@ __global__ void __launch_bounds__(128) k_collide_inplace(const KParams p, double
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= p.nx) return;
   const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
-  if (p.cells[c].w & kNonFluid) return;
+  if (p.cellw[c] & kNonFluid) return;
   double f[19];
 #pragma unroll
   for (int j = 0; j < 19; ++j) f[j] = buf[(int64_t)j * p.ks + c];
@@ -767,7 +778,7 @@ __global__ void k_macro_fields(const KParams p, const double* __restrict__ f, do
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= p.nx) return;
   const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
-  if (p.cells[c].w & kNonFluid) {
+  if (p.cellw[c] & kNonFluid) {
     if (drho) drho[c] = 0.0;
     if (ux) ux[c] = 0.0;
     if (uy) uy[c] = 0.0;
@@ -784,7 +795,7 @@ __global__ void k_macro_fields(const KParams p, const double* __restrict__ f, do
 
 // Sequential per-plane sum in ascending cell order (simulation.cpp:400-407),
 // one thread per plane so the rounding sequence is the reference's.
-__global__ void k_plane_sums(const CellWord* __restrict__ cells,
+__global__ void k_plane_sums(const uint32_t* __restrict__ cellw,
                              const double* __restrict__ u, int64_t plane, int nz,
                              double* sums) {
   const int z = blockIdx.x * blockDim.x + threadIdx.x;
@@ -792,7 +803,7 @@ __global__ void k_plane_sums(const CellWord* __restrict__ cells,
   double s = 0.0;
   const int64_t c0 = plane * z;
   for (int64_t i = 0; i < plane; ++i) {
-    if (cells[c0 + i].w & kNonFluid) continue;
+    if (cellw[c0 + i] & kNonFluid) continue;
     s = DADD(s, __ldg(u + c0 + i));
   }
   sums[z] = s;
@@ -808,7 +819,7 @@ __global__ void k_max_speed2(const KParams p, const double* __restrict__ f,
   bool bad = false;
   if (x < p.nx) {
     const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
-    if (!(p.cells[c].w & kNonFluid)) {
+    if (!(p.cellw[c] & kNonFluid)) {
       double d, u[3];
       if (!macro_cell<GLBM>(p, f, c, z, d, u)) atomicOr(err, 1);
       m2 = DADD(DADD(DMUL(u[0], u[0]), DMUL(u[1], u[1])), DMUL(u[2], u[2]));
@@ -830,11 +841,11 @@ __global__ void k_max_speed2(const KParams p, const double* __restrict__ f,
   }
 }
 
-__global__ void k_fill_equilibrium(const CellWord* __restrict__ cw, int64_t cells,
+__global__ void k_fill_equilibrium(const uint32_t* __restrict__ cw, int64_t cells,
                                    int64_t ks, double* f, const double* feq /*19*/) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cells) return;
-  if (cw[c].w & kNonFluid) return;
+  if (cw[c] & kNonFluid) return;
 #pragma unroll
   for (int k = 0; k < 19; ++k) f[(int64_t)k * ks + c] = feq[k];
 }
@@ -1000,7 +1011,7 @@ void launch_macro_fields(bool glbm, const KParams& p, const double* f, double* d
 
 void launch_plane_sums(const KParams& p, const double* u, double* sums, cudaStream_t s) {
   const int64_t plane = (int64_t)p.nx * p.ny;
-  k_plane_sums<<<(p.nz + 31) / 32, 32, 0, s>>>(p.cells, u, plane, p.nz, sums);
+  k_plane_sums<<<(p.nz + 31) / 32, 32, 0, s>>>(p.cellw, u, plane, p.nz, sums);
 }
 
 void launch_max_speed2(bool glbm, const KParams& p, const double* f,
@@ -1015,7 +1026,7 @@ void launch_max_speed2(bool glbm, const KParams& p, const double* f,
 
 void launch_fill_equilibrium(const KParams& p, int64_t cells, double* f, const double* feq,
                              cudaStream_t s) {
-  k_fill_equilibrium<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(p.cells, cells, p.ks, f,
+  k_fill_equilibrium<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(p.cellw, cells, p.ks, f,
                                                                      feq);
 }
 

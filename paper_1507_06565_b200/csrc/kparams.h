@@ -47,7 +47,10 @@ struct KParams {
   int32_t nx, ny, nz;
   int32_t px, py, pz;  // periodic flags (x ignored in slab mode)
   int64_t ks;          // element stride between the 19 direction planes
-  const CellWord* cells;     // per-cell word + link base
+  const uint32_t* cellw;     // per-cell word (kNonFluid / bounce bits / kFillSector)
+  const int32_t* cellbase;   // per-cell first link record (per-cell kernels)
+  const int32_t* chunkbase;  // first link record of each 32-cell chunk of a row
+  int32_t nchunk;            // chunks per row = ceil(nx / 32)
   const LinkRec* links;
   int32_t fill_sectors;      // write zeros into fill-flagged non-fluid cells
   double wp, wm, rho0, nu, cf;

@@ -81,7 +81,9 @@ struct pgpu_sim {
   bool eps_in_eq = true;
   // device memory
   double* f[2] = {nullptr, nullptr};
-  CellWord* d_cellword = nullptr;
+  uint32_t* d_cellw = nullptr;
+  int32_t* d_cellbase = nullptr;
+  int32_t* d_chunkbase = nullptr;
   LinkRec* d_recs = nullptr;
   PlaneCoef* d_planes = nullptr;
   double* d_feq = nullptr;
@@ -112,7 +114,9 @@ struct pgpu_sim {
       if (g) cudaGraphExecDestroy(g);
     cudaSetDevice(device);
     for (double* p : f) cudaFree(p);
-    cudaFree(d_cellword);
+    cudaFree(d_cellw);
+    cudaFree(d_cellbase);
+    cudaFree(d_chunkbase);
     cudaFree(d_recs);
     cudaFree(d_planes);
     cudaFree(d_feq);
@@ -709,9 +713,30 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
       CK(cudaMalloc(&s->f[b], fbytes));
       CK(cudaMemsetAsync(s->f[b], 0, fbytes, s->stream));
     }
-    CK(cudaMalloc(&s->d_cellword, sizeof(CellWord) * s->cells));
-    CK(cudaMemcpyAsync(s->d_cellword, s->cellword.data(), sizeof(CellWord) * s->cells,
-                       cudaMemcpyHostToDevice, s->stream));
+    {  // split the host words: 4-byte words, per-cell bases, per-chunk bases
+      const int64_t rows = (int64_t)s->ny * s->nz;
+      const int nchunk = (s->nx + 31) / 32;
+      std::vector<uint32_t> w(s->cells);
+      std::vector<int32_t> b(s->cells), cb(rows * nchunk);
+      parallel_for(rows, [&](int64_t ra, int64_t rb, int) {
+        for (int64_t r = ra; r < rb; ++r) {
+          for (int x = 0; x < s->nx; ++x) {
+            const CellWord& cw = s->cellword[r * s->nx + x];
+            w[r * s->nx + x] = cw.w;
+            b[r * s->nx + x] = cw.base;
+            if ((x & 31) == 0) cb[r * nchunk + (x >> 5)] = cw.base;
+          }
+        }
+      });
+      CK(cudaMalloc(&s->d_cellw, sizeof(uint32_t) * s->cells));
+      CK(cudaMalloc(&s->d_cellbase, sizeof(int32_t) * s->cells));
+      CK(cudaMalloc(&s->d_chunkbase, sizeof(int32_t) * cb.size()));
+      CK(cudaMemcpy(s->d_cellw, w.data(), sizeof(uint32_t) * s->cells, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(s->d_cellbase, b.data(), sizeof(int32_t) * s->cells, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(s->d_chunkbase, cb.data(), sizeof(int32_t) * cb.size(),
+                    cudaMemcpyHostToDevice));
+      s->kp.nchunk = nchunk;
+    }
     CK(cudaMalloc(&s->d_feq, sizeof(double) * 19));
     CK(cudaMalloc(&s->d_flags, sizeof(int) * 2));
     CK(cudaMalloc(&s->d_vmax, sizeof(unsigned long long)));
@@ -730,7 +755,9 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
       kp.bounce_delta[j] = (int64_t)opposite(j) * s->ks - kp.pull_off[j];
       kp.plane_off[j] = (int64_t)j * s->ks;
     }
-    kp.cells = s->d_cellword;
+    kp.cellw = s->d_cellw;
+    kp.cellbase = s->d_cellbase;
+    kp.chunkbase = s->d_chunkbase;
     lap("alloc+upload cellword");
     s->refresh_params();
     if (s->records_needed()) s->upload_records();
