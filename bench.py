@@ -183,7 +183,7 @@ def run_ours(args):
     import paper_1507_06565_b200 as pg
     from paper_1507_06565_b200 import configs
 
-    if world > 1:
+    if world > 1 or args.force_slab:
         from paper_1507_06565_b200.dist import SlabSimulation
 
         w = configs.c4(nx_scale=world) if (args.config == "C4" and args.scaling == "weak") \
@@ -202,7 +202,7 @@ def run_ours(args):
         sim = configs.make_simulation(w, geom, device=local)
         fluid_local = geom.fluid_cells
         stepper = sim.step
-    if world > 1:
+    if world > 1 or args.force_slab:
         stream = sim_obj.me.stream
     else:
         stream = torch.cuda.Stream(device=local)
@@ -253,13 +253,13 @@ def run_ours(args):
 
     # e2e through the C ABI with host buffers (N=1; other ranks mirror it)
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if world == 1 and not args.no_e2e and not args.force_slab:
         del sim
         torch.cuda.empty_cache()
         e2e = e2e_run(pg, configs, w, geom, args.steps, local)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.force_slab:
         try:
             cpu_steps = args.cpu_steps
             mlups, threads, dt = reference_cpu_run(w, geom, cpu_steps, 1)
@@ -281,7 +281,8 @@ def run_ours(args):
             "config": {"workload": w.name, "fluid_cells": fluid_total,
                        "cells": int(np.prod(w.dims)), "scheme": w.scheme.name,
                        "l2": "inputs larger than L2 (2 x 19 x cells x 8 B >> 126 MB)",
-                       "parallelism": f"x-slab{world}" if world > 1 else "single", **w.meta},
+                       "parallelism": f"x-slab{world}" if (world > 1 or args.force_slab)
+                       else "single", **w.meta},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -335,6 +336,9 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-slab", action="store_true",
+                    help="diagnostic: run the multi-GPU slab path (edge/interior split, halo "
+                         "exchange) even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
