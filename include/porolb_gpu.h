@@ -4,7 +4,7 @@
  *
  * Reference interfaces replaced (paths relative to the reference's proj/):
  *   pgpu_relaxation_from_magic   lattice.hpp:42-44,   lattice.cpp:58-75
- *   pgpu_voxelize / _slab        geometry.hpp:76-81,  geometry.cpp:491-632
+ *   pgpu_voxelize / _slab / _device  geometry.hpp:76-81, geometry.cpp:491-632
  *   pgpu_make_box_geometry       geometry.hpp:83-84,  geometry.cpp:634-640
  *   pgpu_create                  simulation.hpp:55,   simulation.cpp:80-102
  *   pgpu_set_body_force          simulation.hpp:57
@@ -178,6 +178,11 @@ int pgpu_voxelize_slab(const pgpu_sphere_pack* pack, const int32_t dims[3],
                        pgpu_voxel_geometry** out);
 int pgpu_make_box_geometry(const int32_t dims[3], const pgpu_voxelize_options* opt,
                            pgpu_voxel_geometry** out);
+/* voxelize() on the GPU: byte-identical output, computed
+ * by sm_100a kernels (flags, per-cell link counts, scan, links with q). */
+int pgpu_voxelize_device(const pgpu_sphere_pack* pack, const int32_t dims[3],
+                         const pgpu_voxelize_options* opt, int32_t device,
+                         pgpu_voxel_geometry** out);
 /* Fills a pgpu_geometry view whose arrays point into the handle (valid until
  * pgpu_voxel_geometry_free). */
 int pgpu_voxel_geometry_view(const pgpu_voxel_geometry* g, pgpu_geometry* view,

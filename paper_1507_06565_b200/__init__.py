@@ -33,6 +33,7 @@ from .porolb import (  # noqa: F401
     run_to_steady,
     trt_collide,
     voxelize,
+    voxelize_device,
     voxelize_slab,
 )
 

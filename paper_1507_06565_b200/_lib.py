@@ -76,6 +76,7 @@ SIGNATURES = {
     "pgpu_voxelize_slab": (C.c_int, [P(SpherePackC), P(i32), P(VoxelizeOptionsC), i32, i32,
                                      P(vp)]),
     "pgpu_make_box_geometry": (C.c_int, [P(i32), P(VoxelizeOptionsC), P(vp)]),
+    "pgpu_voxelize_device": (C.c_int, [P(SpherePackC), P(i32), P(VoxelizeOptionsC), i32, P(vp)]),
     "pgpu_voxel_geometry_view": (C.c_int, [vp, P(Geometry), P(i32)]),
     "pgpu_voxel_geometry_free": (None, [vp]),
     "pgpu_generate_spheres": (C.c_int, [i32, u64, P(f64), f64, f64, f64, f64, f64, f64, i64,
@@ -121,7 +122,7 @@ SIGNATURES = {
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_1507_06565_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_1507_06565_b200/build.py` "
             "(there is no CPU fallback for the B200 path)")
     lib = C.CDLL(str(LIB_PATH))
     for name, (res, args) in SIGNATURES.items():

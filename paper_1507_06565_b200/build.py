@@ -1,7 +1,7 @@
 """In-tree build of libporolb_cuda.so (sm_100a) and the oracle libraries.
 
-    python -m paper_1507_06565_b200.build          # product library
-    python -m paper_1507_06565_b200.build --all    # + oracle/ (+ oracle/_ref when
+    python paper_1507_06565_b200/build.py          # product library
+    python paper_1507_06565_b200/build.py --all    # + oracle/ (+ oracle/_ref when
                                                    #   /root/reference is present)
 
 The product is compiled with nvcc for ``-gencode arch=compute_100a,code=sm_100a``
@@ -30,9 +30,9 @@ CUDA_INC = "/usr/local/cuda/include"
 # The image's $CXX (/opt/gcc) lacks libgomp specs; the system g++ is used.
 CXX = shutil.which("g++") or "g++"
 
-CU_SOURCES = ["kernels.cu"]
+CU_SOURCES = ["kernels.cu", "voxelize_device.cu"]
 CPP_SOURCES = ["params.cpp", "voxelize.cpp", "synth.cpp", "sim.cpp"]
-HEADERS = ["kparams.h", "kernels.h", "host_common.h"]
+HEADERS = ["kparams.h", "kernels.h", "host_common.h", "voxel_geometry.h"]
 
 
 def _run(cmd: list[str]) -> None:

@@ -20,23 +20,8 @@
 #include <vector>
 
 #include "host_common.h"
+#include "voxel_geometry.h"
 
-struct pgpu_voxel_geometry {
-  int32_t dims[3];
-  uint8_t periodic[3];
-  std::vector<uint8_t> flags;
-  std::vector<int64_t> lf, ls;
-  std::vector<int32_t> ld;
-  std::vector<float> lq;
-  std::vector<uint8_t> lm;
-  std::vector<double> porosity;
-  int64_t fluid_cells = 0;
-  int32_t q_fallback_count = 0;
-  int32_t has_lo = 0, has_hi = 0;
-  double lo = 0.0, hi = 0.0;
-  int32_t slab = 0, x_offset = 0, global_nx = 0;
-  std::vector<uint8_t> ghost_lo, ghost_hi;
-};
 
 namespace pgpu {
 namespace {
@@ -162,6 +147,28 @@ struct SphereGrid {
     return ((int64_t)z * gy + y) * gx + x;
   }
 };
+
+}  // namespace
+
+VoxHostGrid build_vox_host_grid(const pgpu_sphere_pack& pack, const uint8_t periodic[3],
+                                const int32_t dims[3]) {
+  VoxHostGrid out;
+  const std::vector<Sph> s = effective_spheres(pack, periodic, dims);
+  SphereGrid grid;
+  grid.build(s, dims);
+  out.spheres.resize(s.size());
+  for (size_t i = 0; i < s.size(); ++i)
+    out.spheres[i] = VoxSph{{s[i].c[0], s[i].c[1], s[i].c[2]}, s[i].r};
+  out.h = grid.h;
+  out.gx = grid.gx;
+  out.gy = grid.gy;
+  out.gz = grid.gz;
+  out.start = grid.start;
+  out.items = grid.items;
+  return out;
+}
+
+namespace {
 
 // Core: voxelize the global domain restricted to global columns [x0, x1).
 // When slab, ghost columns x0-1 and x1 (periodic wrap along x) are also

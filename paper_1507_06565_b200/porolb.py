@@ -318,6 +318,18 @@ def voxelize(pack: SpherePack, dims, periodic=(True, True, False), wall_z_lo: bo
     return _geometry_from_handle(h)
 
 
+def voxelize_device(pack: SpherePack, dims, periodic=(True, True, False), wall_z_lo: bool = False,
+                    wall_z_hi: bool = False, q_clamp_min: float = 0.05,
+                    device: int = 0) -> VoxelGeometry:
+    """voxelize() computed by sm_100a kernels; byte-identical output."""
+    pk, _keep = pack.to_c()
+    d = (C.c_int32 * 3)(*dims)
+    o = _opts(periodic, wall_z_lo, wall_z_hi, q_clamp_min)
+    h = C.c_void_p()
+    _check(lib.pgpu_voxelize_device(C.byref(pk), d, C.byref(o), int(device), C.byref(h)))
+    return _geometry_from_handle(h)
+
+
 def voxelize_slab(pack: SpherePack, dims, x0: int, x1: int, periodic=(True, True, False),
                   wall_z_lo: bool = False, wall_z_hi: bool = False,
                   q_clamp_min: float = 0.05) -> VoxelGeometry:

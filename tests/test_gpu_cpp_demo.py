@@ -12,7 +12,7 @@ DEMO = Path(__file__).resolve().parent.parent / "tools" / "porolb_gpu_demo"
 
 
 def test_cpp_demo_acceptance(gpu):
-    assert DEMO.exists(), "build with python -m paper_1507_06565_b200.build"
+    assert DEMO.exists(), "build with python paper_1507_06565_b200/build.py"
     res = subprocess.run([str(DEMO)], capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout + res.stderr
     out = json.loads(res.stdout)

@@ -5,7 +5,7 @@
 //     (proj/tests/acceptance/acceptance_main.cpp:59-75);
 //   * run_bench / time_scheme, SBB vs CLI on the 128^3 sphere-in-box bench
 //     geometry (proj/src/bench.cpp:17-66; acceptance criterion 10).
-// Prints one JSON object.  Build: python -m paper_1507_06565_b200.build --all
+// Prints one JSON object.  Build: python paper_1507_06565_b200/build.py --all
 #include <chrono>
 #include <cmath>
 #include <cstdio>
