@@ -146,7 +146,24 @@ __device__ __forceinline__ void collide_glbm(double (&fk)[19], const KParams& p,
     const double vmag = DSQRT(DADD(DADD(DMUL(vhx, vhx), DMUL(vhy, vhy)), DMUL(vhz, vhz)));
     denom = DADD(pc.c0, DSQRT(DADD(DMUL(pc.c0, pc.c0), DMUL(pc.c1, vmag))));
   }
-  const double ux = DDIV(vhx, denom), uy = DDIV(vhy, denom), uz = DDIV(vhz, denom);
+  double ux, uy, uz;
+  if (p.cf == 0.0 && pc.denom_mode == 0) {  // denom == 1: identity (free planes)
+    ux = vhx;
+    uy = vhy;
+    uz = vhz;
+  } else if (p.cf == 0.0 && pc.denom_mode == 1) {  // power of two: exact reciprocal
+    ux = DMUL(vhx, pc.inv_denom);
+    uy = DMUL(vhy, pc.inv_denom);
+    uz = DMUL(vhz, pc.inv_denom);
+  } else {
+    ux = DDIV(vhx, denom);
+    uy = DDIV(vhy, denom);
+    uz = DDIV(vhz, denom);
+  }
+  // x / eq_eps with the same shortcuts (plane-uniform branch)
+  auto div_eps = [&](double v) {
+    return pc.eq_mode == 0 ? v : (pc.eq_mode == 1 ? DMUL(v, pc.inv_eq_eps) : DDIV(v, eq_eps));
+  };
   double drag;
   if (p.cf != 0.0) {
     const double umag = DSQRT(DADD(DADD(DMUL(ux, ux), DMUL(uy, uy)), DMUL(uz, uz)));
@@ -159,8 +176,8 @@ __device__ __forceinline__ void collide_glbm(double (&fk)[19], const KParams& p,
   const double Fz = DADD(DMUL(-drag, uz), pc.eps_g[2]);
   const double uu = DADD(DADD(DMUL(ux, ux), DMUL(uy, uy)), DMUL(uz, uz));
   const double uu15 = DMUL(1.5, uu);
-  const double feq0 = DMUL(
-      1.0 / 3.0, DSUB(drho, DDIV(RHO1 ? uu15 : DMUL(DMUL(rho0, 1.5), uu), eq_eps)));
+  const double feq0 =
+      DMUL(1.0 / 3.0, DSUB(drho, div_eps(RHO1 ? uu15 : DMUL(DMUL(rho0, 1.5), uu))));
   fk[0] = DSUB(fk[0], DMUL(wp, DSUB(fk[0], feq0)));
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
@@ -171,7 +188,7 @@ __device__ __forceinline__ void collide_glbm(double (&fk)[19], const KParams& p,
                            DMUL((double)EZ[k], Fz));
     double t = DSUB(DMUL(DMUL(4.5, eu), eu), uu15);
     if (!RHO1) t = DMUL(rho0, t);
-    const double feq_p = DMUL(pair_w(q), DADD(drho, DDIV(t, eq_eps)));
+    const double feq_p = DMUL(pair_w(q), DADD(drho, div_eps(t)));
     const double feq_m = DMUL(p.wr3[q], eu);
     const double fp = DMUL(0.5, DADD(fk[k], fk[kb]));
     const double fm = DMUL(0.5, DSUB(fk[k], fk[kb]));

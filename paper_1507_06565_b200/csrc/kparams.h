@@ -40,6 +40,11 @@ struct PlaneCoef {
   double drag_lin0;      // drag_lin + 0.0              (:247 with cf == 0)
   double drag_q;         // eps * cf / sqrt(K)          (:247, second term)
   double force_pref;     // (1.0 - 0.5*wm) * 3.0 * rho0 (:253)
+  // Division shortcuts that are bit-identical to the division: mode 0 divisor
+  // is 1 (identity), mode 1 divisor is a power of two (multiply by its exact
+  // reciprocal), mode 2 general (divide).
+  int32_t eq_mode, denom_mode;
+  double inv_eq_eps, inv_denom;
 };
 
 // Everything a sweep kernel needs, passed by value.

@@ -191,6 +191,20 @@ struct pgpu_sim {
       c.drag_lin0 = c.drag_lin + 0.0;           // :247 with c_F == 0
       c.drag_q = e * cf / std::sqrt(k);         // :247
       c.force_pref = (1.0 - 0.5 * c.wm) * 3.0 * rho0;  // :253
+      // x / d == x * (1/d) exactly when d is a power of two (1/d is exact)
+      auto mode_of = [](double d, double& inv) {
+        inv = 1.0;
+        if (d == 1.0) return 0;
+        int ex = 0;
+        if (std::isfinite(d) && d > 0.0 && std::frexp(d, &ex) == 0.5 &&
+            std::isfinite(1.0 / d) && 1.0 / d != 0.0) {
+          inv = 1.0 / d;
+          return 1;
+        }
+        return 2;
+      };
+      c.eq_mode = mode_of(c.eq_eps, c.inv_eq_eps);
+      c.denom_mode = mode_of(c.denom_lin, c.inv_denom);
     }
     if (!d_planes) CK(cudaMalloc(&d_planes, sizeof(PlaneCoef) * nz));
     CK(cudaMemcpyAsync(d_planes, pc.data(), sizeof(PlaneCoef) * nz, cudaMemcpyHostToDevice,
