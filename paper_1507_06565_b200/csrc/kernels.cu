@@ -892,6 +892,9 @@ int g_sweep_mode = [] {
   const char* e = std::getenv("PGPU_SWEEP");
   return (e && e[0] == 'p' && e[1] == 'l') ? 2 : 1;
 }();
+}  // namespace
+bool g_plain_sweep() { return g_sweep_mode == 2; }
+namespace {
 dim3 sweep_grid(const KParams& p) {
   const int bx = cell_block(p).x;
   return dim3((p.nx + bx - 1) / bx, p.ny, (p.nz + kZPer - 1) / kZPer);

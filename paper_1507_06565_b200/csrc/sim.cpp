@@ -48,6 +48,10 @@ using namespace pgpu;
     }                                                                                 \
   } while (0)
 
+namespace pgpu {
+bool g_plain_sweep();  // kernels.cu: PGPU_SWEEP=plain selected
+}
+
 struct pgpu_sim {
   int device = 0;
   cudaStream_t own_stream = nullptr;
@@ -66,7 +70,14 @@ struct pgpu_sim {
   int64_t fluid_cells = 0;
   int32_t cli_fallbacks = 0;
   // link structures (host mirror)
-  std::vector<CellWord> cellword;  // w + link base (kparams.h)
+  // w + link base per cell (kparams.h); default-initialised (no 0.5 GB memset)
+  struct CellWords {
+    std::unique_ptr<CellWord[]> buf;
+    CellWord& operator[](int64_t i) { return buf[i]; }
+    const CellWord& operator[](int64_t i) const { return buf[i]; }
+    void resize(int64_t n) { buf.reset(new CellWord[n]); }
+  } cellword;
+  bool cellbase_uploaded = false;
   std::vector<LinkRec> recs;       // host-computed CLI coefficient / NaN / +inf
   std::vector<uint8_t> rec_kind;   // LinkKind per record
   std::vector<float> rec_q;
@@ -232,7 +243,21 @@ struct pgpu_sim {
     });
   }
 
+  // Per-cell link bases are read only by the per-cell kernels (slab edge
+  // columns, the persistent small-domain sweep, the plain sweep), so they are
+  // uploaded on first need.
+  void upload_cellbase() {
+    if (cellbase_uploaded) return;
+    std::vector<int32_t> b(cells);
+    parallel_for(cells, [&](int64_t a, int64_t e, int) {
+      for (int64_t c = a; c < e; ++c) b[c] = cellword[c].base;
+    });
+    CK(cudaMemcpy(d_cellbase, b.data(), sizeof(int32_t) * cells, cudaMemcpyHostToDevice));
+    cellbase_uploaded = true;
+  }
+
   void upload_records() {
+    if (slab || persistent || g_plain_sweep()) upload_cellbase();
     if (n_links == 0) {
       records_uploaded = true;
       return;
@@ -476,23 +501,46 @@ inline int wrap(int v, int n, bool periodic) {
 
 void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
   const int nx = s->nx, ny = s->ny, nz = s->nz;
+  const bool trace = std::getenv("PGPU_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pgpu]   build_links %-18s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   const uint8_t* flags = g->flags;
   // bit0 non-fluid; bit j: upstream x - e_j is non-fluid or outside the domain.
   // Row-wise: the 18 source rows of row (y, z) are resolved once, then a
   // tight loop over x; only x = 0 and x = nx-1 need the wrap / ghost rules.
   s->cellword.resize(s->cells);
   parallel_for((int64_t)nz * ny, [&](int64_t ra, int64_t rb, int) {
+    std::vector<uint32_t> wrow(nx);
     const uint8_t* srow[19];
     bool srow_ok[19];
     for (int64_t r = ra; r < rb; ++r) {
       const int z = (int)(r / ny), y = (int)(r % ny);
       const int64_t row = r * nx;
+      const uint8_t* own = flags + row;
       for (int j = 1; j < 19; ++j) {
         const int ys = wrap(y - kE[j][1], ny, s->per[1]);
         const int zs = wrap(z - kE[j][2], nz, s->per[2]);
         srow_ok[j] = ys >= 0 && zs >= 0;
         srow[j] = srow_ok[j] ? flags + ((int64_t)zs * ny + ys) * nx : nullptr;
       }
+      // interior columns: one contiguous (vectorisable) pass per direction
+      for (int x = 0; x < nx; ++x) wrow[x] = own[x] != 0 ? kNonFluid : 0u;
+      for (int j = 1; j < 19; ++j) {
+        const uint32_t bit = 1u << j;
+        if (!srow_ok[j]) {
+          for (int x = 1; x < nx - 1; ++x) wrow[x] |= bit;
+          continue;
+        }
+        const uint8_t* src = srow[j] - kE[j][0];
+        for (int x = 1; x < nx - 1; ++x) wrow[x] |= (src[x] != 0) ? bit : 0u;
+      }
+      // x = 0 and x = nx-1: wrap / ghost rules
       auto edge_word = [&](int x) -> uint32_t {
         uint32_t w = 0;
         for (int j = 1; j < 19; ++j) {
@@ -516,24 +564,16 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
         }
         return w;
       };
+      wrow[0] = own[0] != 0 ? kNonFluid : edge_word(0);
+      if (nx > 1) wrow[nx - 1] = own[nx - 1] != 0 ? kNonFluid : edge_word(nx - 1);
       for (int x = 0; x < nx; ++x) {
         CellWord& cw = s->cellword[row + x];
+        cw.w = (wrow[x] & kNonFluid) ? kNonFluid : wrow[x];
         cw.base = 0;
-        if (flags[row + x] != 0) {
-          cw.w = kNonFluid;
-          continue;
-        }
-        if (x == 0 || x == nx - 1) {
-          cw.w = edge_word(x);
-          continue;
-        }
-        uint32_t w = 0;
-        for (int j = 1; j < 19; ++j)
-          w |= (uint32_t)(!srow_ok[j] || srow[j][x - kE[j][0]] != 0) << j;
-        cw.w = w;
       }
     }
   });
+  lap("cell words");
   // non-fluid cells sharing an aligned 4-cell (32-byte) group with fluid
   // cells are zero-filled by the sweep, so no DRAM sector is partly written
   const int64_t ngroups = (s->cells + 3) / 4;
@@ -549,6 +589,7 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
       }
     });
   }
+  lap("fill bits");
   // per-cell record base: exclusive prefix of bounce counts (two-pass parallel scan)
   const int nt = hw_threads();
   std::vector<int64_t> part(nt + 1, 0);
@@ -577,6 +618,7 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
        << "directions of the flag field (" << total << "); links must close exactly those directions";
     throw ConfigError(os.str());
   }
+  lap("prefix");
   s->n_links = total;
   s->rec_kind.assign(total, kLinkSBB);
   s->rec_q.assign(total, 0.5f);
@@ -627,6 +669,7 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
       errs[t] = e.what();
     }
   }, nt);
+  lap("link records");
   for (const std::string& e : errs)
     if (!e.empty()) throw ConfigError(e);
   s->any_moving = false;
@@ -731,13 +774,12 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
       const int64_t rows = (int64_t)s->ny * s->nz;
       const int nchunk = (s->nx + 31) / 32;
       std::vector<uint32_t> w(s->cells);
-      std::vector<int32_t> b(s->cells), cb(rows * nchunk);
+      std::vector<int32_t> cb(rows * nchunk);
       parallel_for(rows, [&](int64_t ra, int64_t rb, int) {
         for (int64_t r = ra; r < rb; ++r) {
           for (int x = 0; x < s->nx; ++x) {
             const CellWord& cw = s->cellword[r * s->nx + x];
             w[r * s->nx + x] = cw.w;
-            b[r * s->nx + x] = cw.base;
             if ((x & 31) == 0) cb[r * nchunk + (x >> 5)] = cw.base;
           }
         }
@@ -746,7 +788,6 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
       CK(cudaMalloc(&s->d_cellbase, sizeof(int32_t) * s->cells));
       CK(cudaMalloc(&s->d_chunkbase, sizeof(int32_t) * cb.size()));
       CK(cudaMemcpy(s->d_cellw, w.data(), sizeof(uint32_t) * s->cells, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(s->d_cellbase, b.data(), sizeof(int32_t) * s->cells, cudaMemcpyHostToDevice));
       CK(cudaMemcpy(s->d_chunkbase, cb.data(), sizeof(int32_t) * cb.size(),
                     cudaMemcpyHostToDevice));
       s->kp.nchunk = nchunk;
@@ -773,15 +814,15 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     kp.cellbase = s->d_cellbase;
     kp.chunkbase = s->d_chunkbase;
     lap("alloc+upload cellword");
-    s->refresh_params();
-    if (s->records_needed()) s->upload_records();
-    CK(cudaStreamSynchronize(s->stream));
-    lap("records");
     {  // two PDF grids well inside the 126 MB L2 -> persistent multi-step sweeps
       const char* e = std::getenv("PGPU_PERSISTENT");
       const double state_bytes = 2.0 * 19.0 * 8.0 * (double)s->ks;
       s->persistent = !s->slab && (e ? e[0] == '1' : state_bytes <= 48e6);
     }
+    s->refresh_params();
+    if (s->records_needed()) s->upload_records();
+    CK(cudaStreamSynchronize(s->stream));
+    lap("records");
     *out = s.release();
   });
 }
