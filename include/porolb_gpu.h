@@ -26,6 +26,14 @@
  *   pgpu_make_glbm_params        simulation.hpp:31-36, simulation.cpp:23-50
  *   pgpu_glbm_force_and_velocity simulation.hpp:38-43, simulation.cpp:52-66
  *   pgpu_equilibrium / trt_collide lattice.hpp:46-61, lattice.cpp:77-128
+ *   pgpu_get_flags               field.hpp:45 (flags())
+ *   pgpu_format_double           io.hpp:43,  io.cpp:11-15
+ *   pgpu_write/read_profile_csv  io.hpp:14-18, io.cpp:41-97
+ *   pgpu_write_comparison_csv    io.hpp:20-24, io.cpp:99-110 (interp_linear profile.cpp:21-29)
+ *   pgpu_write_report            io.hpp:26-28, io.cpp:112-116
+ *   pgpu_write_vtk               io.hpp:30-32, io.cpp:117-149
+ *   pgpu_write/read_sphere_csv   io.hpp:34-36, io.cpp:151-199
+ *   pgpu_write/read_voxel_file   io.hpp:38-41, io.cpp:201-278
  *
  * Conventions
  *  - Plain pointers and sizes only; every input array is COPIED by the callee,
@@ -228,6 +236,8 @@ int pgpu_steps_done(pgpu_sim* sim, int64_t* out);
 int pgpu_cli_fallback_count(pgpu_sim* sim, int32_t* out);
 int pgpu_fluid_cells(pgpu_sim* sim, int64_t* out);
 int pgpu_dims(pgpu_sim* sim, int32_t dims[3]);
+/* The geometry's flag bytes (field.hpp:45 flags(); 0 fluid, 1 solid, 2 wall). */
+int pgpu_get_flags(pgpu_sim* sim, uint8_t* out);
 
 /* Pre-collision populations f(steps_done) in the reference layout
  * (19*cells doubles).  Only fluid-cell slots are defined on output. */
@@ -277,6 +287,37 @@ int pgpu_halo_parity(pgpu_sim* sim, int32_t* parity);
  * part 1 = interior; pgpu_step_finish advances the step counter. */
 int pgpu_step_part(pgpu_sim* sim, int32_t part);
 int pgpu_step_finish(pgpu_sim* sim);
+
+/* ---- file formats (io.hpp; byte-identical to the reference's writers) ------ */
+/* "%.17g" of v, NUL-terminated (cap >= 25 always suffices). */
+int pgpu_format_double(double v, char* buf, int32_t cap);
+/* Profile CSV: meta->n_planes rows; u_normalized may be shorter (n_norm
+ * entries, missing ones print as 0 like io.cpp:58). */
+int pgpu_write_profile_csv(const char* path, const pgpu_profile_meta* meta, const double* z,
+                           const double* u_superficial, const double* u_intrinsic,
+                           const double* epsilon, const double* u_normalized, int32_t n_norm);
+/* Parses like io.cpp:64-97.  meta->n_planes = rows found, *n_norm = rows with
+ * a fifth column; arrays are filled only when rows <= capacity (call with
+ * capacity 0 to size them). */
+int pgpu_read_profile_csv(const char* path, int32_t capacity, pgpu_profile_meta* meta, double* z,
+                          double* u_superficial, double* u_intrinsic, double* epsilon,
+                          double* u_normalized, int32_t* n_norm);
+int pgpu_write_comparison_csv(const char* path, int32_t n_a, const double* z_a,
+                              const double* u_a, const char* name_a, int32_t n_b,
+                              const double* z_b, const double* u_b, const char* name_b);
+int pgpu_write_report(const char* path, int32_t n, const char* const* keys,
+                      const char* const* values);
+/* Legacy VTK of the current state (flags, delta_rho, velocity); moments are
+ * computed on the device, text is formatted on all host threads. */
+int pgpu_write_vtk(const char* path, pgpu_sim* sim);
+int pgpu_write_sphere_csv(const char* path, const pgpu_sphere_pack* pack, uint64_t seed);
+/* Parses like io.cpp:164-199; same capacity convention as profiles. */
+int pgpu_read_sphere_csv(const char* path, int64_t capacity, int64_t* n_spheres, double* cx,
+                         double* cy, double* cz, double* radius, double box[3],
+                         double* bottom_plate_z, uint64_t* seed, double* achieved_height);
+int pgpu_write_voxel_file(const char* path, const pgpu_geometry* geom);
+/* Flags from the file, links rebuilt with q = 1/2 (io.cpp:210-278). */
+int pgpu_read_voxel_file(const char* path, pgpu_voxel_geometry** out);
 
 #ifdef __cplusplus
 }

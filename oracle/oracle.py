@@ -128,6 +128,18 @@ class RefLib:
         L.ref_make_glbm_params.argtypes = [C.c_int, P(f64), P(f64), f64, f64, f64, C.c_int, f64,
                                            P(f64), P(f64)]
         L.ref_set_threads.argtypes = [C.c_int]
+        cs = C.c_char_p
+        L.ref_format_double.argtypes = [f64, cs, C.c_int]
+        L.ref_write_profile_csv.argtypes = [cs, C.c_int] + [P(f64)] * 4 + [C.c_int, P(f64), P(f64)]
+        L.ref_read_profile_csv.argtypes = [cs, C.c_int, P(C.c_int)] + [P(f64)] * 6
+        L.ref_write_comparison_csv.argtypes = [cs, C.c_int, P(f64), P(f64), cs, C.c_int, P(f64),
+                                               P(f64), cs]
+        L.ref_write_report.argtypes = [cs, C.c_int, P(cs), P(cs)]
+        L.ref_write_vtk.argtypes = [cs, vp]
+        L.ref_write_sphere_csv.argtypes = [cs, i64] + [P(f64)] * 5 + [f64, C.c_uint64]
+        L.ref_read_sphere_csv.argtypes = [cs, i64, P(i64)] + [P(f64)] * 5 + [P(C.c_uint64)]
+        L.ref_write_voxel_file.argtypes = [cs, vp]
+        L.ref_read_voxel_file.argtypes = [cs, P(vp)]
 
     def _check(self, st):
         if st != 0:
@@ -242,6 +254,85 @@ class RefLib:
     def simulation(self, geom, nu, wp, wm, lam, g, scheme, rho0=1.0) -> "RefSim":
         return RefSim(self, geom, nu, wp, wm, lam, g, scheme, rho0)
 
+    # -- file formats (io.cpp) ---------------------------------------------------
+    def format_double(self, v) -> str:
+        buf = C.create_string_buffer(64)
+        self._check(self.lib.ref_format_double(float(v), buf, 64))
+        return buf.value.decode()
+
+    def write_profile_csv(self, path, z, us, ui, eps, un, meta):
+        cols = [np.ascontiguousarray(c, dtype=np.float64) for c in (z, us, ui, eps, un)]
+        m = np.asarray(meta, dtype=np.float64)
+        self._check(self.lib.ref_write_profile_csv(
+            str(path).encode(), cols[0].size, *[_p(c, f64) for c in cols[:4]], cols[4].size,
+            _p(cols[4], f64), _p(m, f64)))
+
+    def read_profile_csv(self, path):
+        counts = (C.c_int * 2)()
+        meta = np.zeros(8)
+        null = P(f64)()
+        self._check(self.lib.ref_read_profile_csv(str(path).encode(), 0, counts, null, null, null,
+                                                  null, null, _p(meta, f64)))
+        n = counts[0]
+        b = [np.zeros(max(n, 1)) for _ in range(5)]
+        self._check(self.lib.ref_read_profile_csv(str(path).encode(), n, counts,
+                                                  *[_p(x, f64) for x in b], _p(meta, f64)))
+        return dict(z=b[0][:n], u_superficial=b[1][:n], u_intrinsic=b[2][:n], epsilon=b[3][:n],
+                    u_normalized=b[4][:counts[1]], meta=meta)
+
+    def write_comparison_csv(self, path, za, ua, name_a, zb, ub, name_b):
+        a = [np.ascontiguousarray(c, dtype=np.float64) for c in (za, ua, zb, ub)]
+        self._check(self.lib.ref_write_comparison_csv(
+            str(path).encode(), a[0].size, _p(a[0], f64), _p(a[1], f64), name_a.encode(),
+            a[2].size, _p(a[2], f64), _p(a[3], f64), name_b.encode()))
+
+    def write_report(self, path, entries):
+        n = len(entries)
+        keys = (C.c_char_p * max(n, 1))(*[str(k).encode() for k, _ in entries])
+        vals = (C.c_char_p * max(n, 1))(*[str(v).encode() for _, v in entries])
+        self._check(self.lib.ref_write_report(str(path).encode(), n, keys, vals))
+
+    def write_sphere_csv(self, path, centers, radii, box, plate_z=0.0, seed=0):
+        cols, r = _pack_arrays(centers, radii)
+        self._check(self.lib.ref_write_sphere_csv(
+            str(path).encode(), r.size, _p(cols[0], f64), _p(cols[1], f64), _p(cols[2], f64),
+            _p(r, f64), _v3(box), float(plate_z), int(seed)))
+
+    def read_sphere_csv(self, path):
+        n = C.c_int64()
+        extra = np.zeros(5)
+        seed = C.c_uint64()
+        null = P(f64)()
+        self._check(self.lib.ref_read_sphere_csv(str(path).encode(), 0, C.byref(n), null, null,
+                                                 null, null, _p(extra, f64), C.byref(seed)))
+        k = n.value
+        b = [np.zeros(max(k, 1)) for _ in range(4)]
+        self._check(self.lib.ref_read_sphere_csv(str(path).encode(), k, C.byref(n),
+                                                 *[_p(x, f64) for x in b], _p(extra, f64),
+                                                 C.byref(seed)))
+        return dict(centers=np.stack([x[:k] for x in b[:3]], axis=1), radii=b[3][:k],
+                    box=tuple(extra[:3]), bottom_plate_z=extra[3], achieved_height=extra[4],
+                    seed=int(seed.value))
+
+    def write_voxel_file(self, path, geom):
+        h = self.geometry_handle(geom)
+        try:
+            self._check(self.lib.ref_write_voxel_file(str(path).encode(), h))
+        finally:
+            self.lib.ref_geometry_free(h)
+
+    def read_voxel_file(self, path) -> OGeom:
+        h = vp()
+        self._check(self.lib.ref_read_voxel_file(str(path).encode(), C.byref(h)))
+        try:
+            with open(path, "rb") as f:  # dims/periodic from the header
+                head = f.readline().split()
+            dims = tuple(int(x) for x in head[2:5])
+            periodic = tuple(int(x) != 0 for x in head[5:8])
+            return self._geom_from_handle(h, dims, periodic)
+        finally:
+            self.lib.ref_geometry_free(h)
+
 
 class RefSim:
     """porolb::Simulation from the reference sources (simulation.cpp:80-434)."""
@@ -329,6 +420,9 @@ class RefSim:
 
     def max_speed(self):
         return float(self.ref.lib.ref_sim_max_speed(self.h))
+
+    def write_vtk(self, path):
+        self.ref._check(self.ref.lib.ref_write_vtk(str(path).encode(), self.h))
 
     def run_to_steady_state(self, tol=1e-8, check_interval=1000, max_steps=2000000,
                             max_speed=0.3 / 1.7320508075688772):

@@ -15,6 +15,7 @@
 //   make_glbm_params           proj/src/simulation.cpp:23-50
 //   kozeny_carman              proj/src/glbm.cpp:90-111
 //   apply_sbb/cli/moving_wall  proj/src/boundary.cpp:19-41
+//   file formats               proj/src/io.cpp:11-278
 // Status codes: 0 ok, 1 ConfigError, 2 NumericalInstability, 3 GeometryError,
 // 5 other std::exception.
 #include <cstdint>
@@ -33,6 +34,7 @@
 #include "porolb/field.hpp"
 #include "porolb/geometry.hpp"
 #include "porolb/glbm.hpp"
+#include "porolb/io.hpp"
 #include "porolb/lattice.hpp"
 #include "porolb/simulation.hpp"
 
@@ -385,6 +387,133 @@ int ref_make_glbm_params(int n, const double* eps, const double* K, double cf, d
     std::memcpy(wp, p.omega_plus.data(), sizeof(double) * n);
     std::memcpy(wm, p.omega_minus.data(), sizeof(double) * n);
   });
+}
+
+// ---- file formats (io.cpp) ------------------------------------------------------
+int ref_format_double(double v, char* buf, int cap) {
+  return guard([&] {
+    const std::string t = format_double(v);
+    if (static_cast<int>(t.size()) + 1 > cap) throw std::runtime_error("buffer too small");
+    std::memcpy(buf, t.c_str(), t.size() + 1);
+  });
+}
+
+namespace {
+// meta: [u_max, height, z0, nu, g0, g1, g2, stream_axis]
+ProfileData make_profile(int n, const double* z, const double* us, const double* ui,
+                         const double* eps, int n_norm, const double* un, const double meta[8]) {
+  ProfileData p;
+  p.z.assign(z, z + n);
+  p.u_superficial.assign(us, us + n);
+  p.u_intrinsic.assign(ui, ui + n);
+  p.epsilon.assign(eps, eps + n);
+  if (n_norm > 0) p.u_normalized.assign(un, un + n_norm);
+  p.u_max = meta[0];
+  p.height = meta[1];
+  p.z0 = meta[2];
+  p.nu = meta[3];
+  p.body_force = {meta[4], meta[5], meta[6]};
+  p.stream_axis = static_cast<int>(meta[7]);
+  return p;
+}
+}  // namespace
+
+int ref_write_profile_csv(const char* path, int n, const double* z, const double* us,
+                          const double* ui, const double* eps, int n_norm, const double* un,
+                          const double meta[8]) {
+  return guard([&] { write_profile_csv(path, make_profile(n, z, us, ui, eps, n_norm, un, meta)); });
+}
+
+// counts: [rows, n_norm]; arrays filled when rows <= cap
+int ref_read_profile_csv(const char* path, int cap, int counts[2], double* z, double* us,
+                         double* ui, double* eps, double* un, double meta[8]) {
+  return guard([&] {
+    const ProfileData p = read_profile_csv(path);
+    counts[0] = static_cast<int>(p.z.size());
+    counts[1] = static_cast<int>(p.u_normalized.size());
+    meta[0] = p.u_max;
+    meta[1] = p.height;
+    meta[2] = p.z0;
+    meta[3] = p.nu;
+    meta[4] = p.body_force[0];
+    meta[5] = p.body_force[1];
+    meta[6] = p.body_force[2];
+    meta[7] = p.stream_axis;
+    if (counts[0] > cap) return;
+    for (size_t i = 0; i < p.z.size(); ++i) {
+      z[i] = p.z[i];
+      us[i] = p.u_superficial[i];
+      ui[i] = p.u_intrinsic[i];
+      eps[i] = p.epsilon[i];
+    }
+    for (size_t i = 0; i < p.u_normalized.size(); ++i) un[i] = p.u_normalized[i];
+  });
+}
+
+int ref_write_comparison_csv(const char* path, int na, const double* za, const double* ua,
+                             const char* name_a, int nb, const double* zb, const double* ub,
+                             const char* name_b) {
+  return guard([&] {
+    ProfileData a, b;
+    a.z.assign(za, za + na);
+    a.u_superficial.assign(ua, ua + na);
+    b.z.assign(zb, zb + nb);
+    b.u_superficial.assign(ub, ub + nb);
+    write_comparison_csv(path, a, name_a, b, name_b);
+  });
+}
+
+int ref_write_report(const char* path, int n, const char* const* keys,
+                     const char* const* values) {
+  return guard([&] {
+    std::vector<std::pair<std::string, std::string>> e;
+    for (int i = 0; i < n; ++i) e.emplace_back(keys[i], values[i]);
+    write_report(path, e);
+  });
+}
+
+int ref_write_vtk(const char* path, void* s) {
+  return guard([&] { write_vtk(path, *static_cast<Simulation*>(s)); });
+}
+
+int ref_write_sphere_csv(const char* path, int64_t n, const double* cx, const double* cy,
+                         const double* cz, const double* r, const double box[3], double plate_z,
+                         uint64_t seed) {
+  return guard([&] {
+    SpherePack pack = make_pack(n, cx, cy, cz, r, box, plate_z);
+    pack.seed = seed;
+    write_sphere_csv(path, pack);
+  });
+}
+
+// extra: [box0, box1, box2, plate_z, achieved_height]; arrays filled when n <= cap
+int ref_read_sphere_csv(const char* path, int64_t cap, int64_t* n, double* cx, double* cy,
+                        double* cz, double* r, double extra[5], uint64_t* seed) {
+  return guard([&] {
+    const SpherePack p = read_sphere_csv(path);
+    *n = static_cast<int64_t>(p.spheres.size());
+    extra[0] = p.box.lx;
+    extra[1] = p.box.ly;
+    extra[2] = p.box.lz;
+    extra[3] = p.bottom_plate_z;
+    extra[4] = p.achieved_height;
+    *seed = p.seed;
+    if (*n > cap) return;
+    for (int64_t i = 0; i < *n; ++i) {
+      cx[i] = p.spheres[i].center[0];
+      cy[i] = p.spheres[i].center[1];
+      cz[i] = p.spheres[i].center[2];
+      r[i] = p.spheres[i].radius;
+    }
+  });
+}
+
+int ref_write_voxel_file(const char* path, void* g) {
+  return guard([&] { write_voxel_file(path, *static_cast<VoxelGeometry*>(g)); });
+}
+
+int ref_read_voxel_file(const char* path, void** out) {
+  return guard([&] { *out = new VoxelGeometry(read_voxel_file(path)); });
 }
 
 }  // extern "C"

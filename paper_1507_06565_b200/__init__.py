@@ -37,4 +37,17 @@ from .porolb import (  # noqa: F401
     voxelize_slab,
 )
 
+from .fileio import (  # noqa: F401,E402
+    format_double,
+    read_profile_csv,
+    read_sphere_csv,
+    read_voxel_file,
+    write_comparison_csv,
+    write_profile_csv,
+    write_report,
+    write_sphere_csv,
+    write_voxel_file,
+    write_vtk,
+)
+
 __version__ = "0.1.0"

@@ -116,6 +116,22 @@ SIGNATURES = {
     "pgpu_halo_parity": (C.c_int, [vp, P(i32)]),
     "pgpu_step_part": (C.c_int, [vp, i32]),
     "pgpu_step_finish": (C.c_int, [vp]),
+    "pgpu_get_flags": (C.c_int, [vp, P(u8)]),
+    # file formats (io.hpp)
+    "pgpu_format_double": (C.c_int, [f64, C.c_char_p, i32]),
+    "pgpu_write_profile_csv": (C.c_int, [C.c_char_p, P(ProfileMeta), P(f64), P(f64), P(f64),
+                                         P(f64), P(f64), i32]),
+    "pgpu_read_profile_csv": (C.c_int, [C.c_char_p, i32, P(ProfileMeta), P(f64), P(f64), P(f64),
+                                        P(f64), P(f64), P(i32)]),
+    "pgpu_write_comparison_csv": (C.c_int, [C.c_char_p, i32, P(f64), P(f64), C.c_char_p, i32,
+                                            P(f64), P(f64), C.c_char_p]),
+    "pgpu_write_report": (C.c_int, [C.c_char_p, i32, P(C.c_char_p), P(C.c_char_p)]),
+    "pgpu_write_vtk": (C.c_int, [C.c_char_p, vp]),
+    "pgpu_write_sphere_csv": (C.c_int, [C.c_char_p, P(SpherePackC), u64]),
+    "pgpu_read_sphere_csv": (C.c_int, [C.c_char_p, i64, P(i64), P(f64), P(f64), P(f64), P(f64),
+                                       P(f64), P(f64), P(u64), P(f64)]),
+    "pgpu_write_voxel_file": (C.c_int, [C.c_char_p, P(Geometry)]),
+    "pgpu_read_voxel_file": (C.c_int, [C.c_char_p, P(vp)]),
 }
 
 

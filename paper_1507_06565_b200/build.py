@@ -31,7 +31,7 @@ CUDA_INC = "/usr/local/cuda/include"
 CXX = shutil.which("g++") or "g++"
 
 CU_SOURCES = ["kernels.cu", "voxelize_device.cu"]
-CPP_SOURCES = ["params.cpp", "voxelize.cpp", "synth.cpp", "sim.cpp"]
+CPP_SOURCES = ["params.cpp", "voxelize.cpp", "synth.cpp", "sim.cpp", "io.cpp"]
 HEADERS = ["kparams.h", "kernels.h", "host_common.h", "voxel_geometry.h"]
 
 

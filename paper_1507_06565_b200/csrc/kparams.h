@@ -18,10 +18,12 @@ typedef double LinkRec;
 
 // Per-cell word: bit 0 = not fluid; bits 1..18 = f_j comes from a link;
 // bit 19 = non-fluid cell that shares a 32-byte sector with a fluid cell
-// (written with zeros so no sector is ever partially written).
+// (written with zeros so no sector is ever partially written); bits 24..31 =
+// the reference flag byte of a non-fluid cell (write_vtk, pgpu_get_flags).
 constexpr uint32_t kNonFluid = 1u;
 constexpr uint32_t kBounceMask = 0x7FFFEu;
 constexpr uint32_t kFillSector = 1u << 19;
+constexpr int kFlagShift = 24;
 struct alignas(8) CellWord {
   uint32_t w;
   int32_t base;  // first link record of the cell

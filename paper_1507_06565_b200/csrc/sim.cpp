@@ -568,7 +568,7 @@ void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
       if (nx > 1) wrow[nx - 1] = own[nx - 1] != 0 ? kNonFluid : edge_word(nx - 1);
       for (int x = 0; x < nx; ++x) {
         CellWord& cw = s->cellword[row + x];
-        cw.w = (wrow[x] & kNonFluid) ? kNonFluid : wrow[x];
+        cw.w = (wrow[x] & kNonFluid) ? (kNonFluid | (uint32_t)own[x] << kFlagShift) : wrow[x];
         cw.base = 0;
       }
     }
@@ -971,6 +971,16 @@ int pgpu_fluid_cells(pgpu_sim* sim, int64_t* out) {
   return guard([&] {
     SIM_CHECK();
     *out = sim->fluid_cells;
+  });
+}
+
+int pgpu_get_flags(pgpu_sim* sim, uint8_t* out) {
+  return guard([&] {
+    SIM_CHECK();
+    if (!out) throw std::invalid_argument("null output");
+    parallel_for(sim->cells, [&](int64_t a, int64_t b, int) {
+      for (int64_t c = a; c < b; ++c) out[c] = (uint8_t)(sim->cellword[c].w >> kFlagShift);
+    });
   });
 }
 

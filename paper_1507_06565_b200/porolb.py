@@ -180,6 +180,7 @@ class SpherePack:
     box: tuple
     bottom_plate_z: float = 0.0
     seed: int = 0
+    achieved_height: float = 0.0  # max over spheres of z + r (read_sphere_csv)
 
     def to_c(self):
         c = np.ascontiguousarray(self.centers, dtype=np.float64).reshape(-1, 3)
@@ -571,6 +572,13 @@ class Simulation:
         u = np.zeros(3)
         _check(lib.pgpu_macroscopic(self._h, int(cell), C.byref(d), _p(u, C.c_double)))
         return d.value, u
+
+    def flags(self) -> np.ndarray:
+        """The geometry's flag bytes (field.hpp:45), shaped (nz, ny, nx)."""
+        nx, ny, nz = self.geometry_dims
+        out = np.empty((nz, ny, nx), dtype=np.uint8)
+        _check(lib.pgpu_get_flags(self._h, _p(out, C.c_uint8)))
+        return out
 
     def macroscopic_fields(self):
         """(delta_rho, ux, uy, uz), each shaped (nz, ny, nx); 0 on non-fluid cells."""
