@@ -13,6 +13,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../porolb_gpu.h"
@@ -87,6 +88,8 @@ struct SpherePack {  // geometry.hpp:25-32
   std::vector<Sphere> spheres;
   Box3 box;
   double bottom_plate_z = 0.0;
+  std::uint64_t seed = 0;
+  double achieved_height = 0.0;
 };
 struct Dims {
   int nx = 0, ny = 0, nz = 0;
@@ -360,6 +363,94 @@ inline RunStats run_to_steady_state(Simulation& sim, const SteadyConfig& cfg,
   r.residual = s.residual;
   r.cli_fallbacks = s.cli_fallbacks;
   return r;
+}
+
+// ---- file formats (io.hpp:11-44), native writers in libporolb_cuda.so ----------
+inline std::string format_double(double v) {  // io.cpp:11-15
+  char buf[32];
+  check(pgpu_format_double(v, buf, sizeof buf));
+  return buf;
+}
+
+inline void write_profile_csv(const std::string& path, const ProfileData& p) {
+  pgpu_profile_meta m{};
+  m.n_planes = static_cast<int32_t>(p.z.size());
+  m.u_max = p.u_max;
+  m.height = p.height;
+  m.z0 = p.z0;
+  m.nu = p.nu;
+  for (int a = 0; a < 3; ++a) m.body_force[a] = p.body_force[a];
+  m.stream_axis = p.stream_axis;
+  check(pgpu_write_profile_csv(path.c_str(), &m, p.z.data(), p.u_superficial.data(),
+                               p.u_intrinsic.data(), p.epsilon.data(), p.u_normalized.data(),
+                               static_cast<int32_t>(p.u_normalized.size())));
+}
+
+inline ProfileData read_profile_csv(const std::string& path) {
+  pgpu_profile_meta m{};
+  int32_t nn = 0;
+  check(pgpu_read_profile_csv(path.c_str(), 0, &m, nullptr, nullptr, nullptr, nullptr, nullptr,
+                              &nn));
+  std::vector<double> b[5];
+  for (auto& v : b) v.resize(static_cast<std::size_t>(m.n_planes));
+  check(pgpu_read_profile_csv(path.c_str(), m.n_planes, &m, b[0].data(), b[1].data(),
+                              b[2].data(), b[3].data(), b[4].data(), &nn));
+  ProfileData p = detail::profile_from(b, m);
+  p.u_normalized.resize(static_cast<std::size_t>(nn));
+  return p;
+}
+
+inline void write_comparison_csv(const std::string& path, const ProfileData& a,
+                                 const std::string& name_a, const ProfileData& b,
+                                 const std::string& name_b) {
+  check(pgpu_write_comparison_csv(path.c_str(), static_cast<int32_t>(a.z.size()), a.z.data(),
+                                  a.u_superficial.data(), name_a.c_str(),
+                                  static_cast<int32_t>(b.z.size()), b.z.data(),
+                                  b.u_superficial.data(), name_b.c_str()));
+}
+
+inline void write_report(const std::string& path,
+                         const std::vector<std::pair<std::string, std::string>>& entries) {
+  std::vector<const char*> k, v;
+  for (const auto& e : entries) {
+    k.push_back(e.first.c_str());
+    v.push_back(e.second.c_str());
+  }
+  check(pgpu_write_report(path.c_str(), static_cast<int32_t>(k.size()), k.data(), v.data()));
+}
+
+inline void write_vtk(const std::string& path, const Simulation& sim) {
+  check(pgpu_write_vtk(path.c_str(), sim.handle()));
+}
+
+inline void write_sphere_csv(const std::string& path, const SpherePack& pack) {
+  detail::PackArrays pa(pack);
+  check(pgpu_write_sphere_csv(path.c_str(), &pa.c, pack.seed));
+}
+
+inline SpherePack read_sphere_csv(const std::string& path) {
+  int64_t n = 0;
+  SpherePack p;
+  double box[3];
+  check(pgpu_read_sphere_csv(path.c_str(), 0, &n, nullptr, nullptr, nullptr, nullptr, box,
+                             &p.bottom_plate_z, &p.seed, &p.achieved_height));
+  std::vector<double> c[4];
+  for (auto& v : c) v.resize(static_cast<std::size_t>(n));
+  check(pgpu_read_sphere_csv(path.c_str(), n, &n, c[0].data(), c[1].data(), c[2].data(),
+                             c[3].data(), box, &p.bottom_plate_z, &p.seed, &p.achieved_height));
+  p.box = {box[0], box[1], box[2]};
+  for (int64_t i = 0; i < n; ++i) p.spheres.push_back({{c[0][i], c[1][i], c[2][i]}, c[3][i]});
+  return p;
+}
+
+inline void write_voxel_file(const std::string& path, const VoxelGeometry& g) {
+  check(pgpu_write_voxel_file(path.c_str(), &g.c()));
+}
+
+inline VoxelGeometry read_voxel_file(const std::string& path) {
+  pgpu_voxel_geometry* h = nullptr;
+  check(pgpu_read_voxel_file(path.c_str(), &h));
+  return VoxelGeometry(h);
 }
 
 }  // namespace porolb_gpu

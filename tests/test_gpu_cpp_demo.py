@@ -1,6 +1,7 @@
 """The C++ drop-in (tools/porolb_gpu_demo.cpp over include/porolb_gpu/porolb_gpu.hpp):
 reference acceptance criteria 1 (Poiseuille exactness) and 10 (bench sanity,
-CLI >= 0.75 x SBB MLUPS on the 128^3 sphere-in-box) run through the C++ API."""
+CLI >= 0.75 x SBB MLUPS on the 128^3 sphere-in-box) run through the C++ API,
+plus the scenario files (profile / sphere CSV, voxel file) written and read back."""
 import json
 import subprocess
 from pathlib import Path
@@ -19,3 +20,4 @@ def test_cpp_demo_acceptance(gpu):
     assert out["poiseuille_converged"] and out["poiseuille_max_rel_err"] <= 1e-8
     assert out["cli_over_sbb"] >= 0.75
     assert out["bench_cells"] == 128 ** 3
+    assert out["io_round_trip"]  # profile/sphere CSV + voxel file through the io.hpp mirror
