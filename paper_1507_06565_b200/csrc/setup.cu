@@ -1,0 +1,284 @@
+// Device-side construction of the sweep's link structures (pgpu_create,
+// simulation.cpp:80-102): from the caller's flag field and link list, uploaded
+// once, sm_100a kernels build
+//   * the per-cell words (bit0 non-fluid + flag byte, bits 1..18 "f_j comes
+//     from a link", bit19 sector fill) -- the fluid->non-fluid test of
+//     geometry.cpp:574-591 in pull form, with the periodic / open / ghost-column
+//     rules of the host voxelizer;
+//   * the per-cell and per-32-cell-chunk record bases (exclusive scan);
+//   * one record per link (CLI coefficient c = (1-2q)/(1+2q) from the fp32 q,
+//     boundary.cpp:27-28, NaN = SBB, +inf = moving wall) after validating that
+//     the links close exactly the fluid->non-fluid directions.
+// Replaces a multi-threaded host pass plus the upload of its results: the
+// host only moves the caller's arrays (flags 1 B/cell, links 25 B/link).
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "kparams.h"
+#include "setup.h"
+
+namespace pgpu {
+namespace {
+
+__constant__ int8_t cE[19][3] = {{0, 0, 0},  {1, 0, 0},   {-1, 0, 0}, {0, 1, 0},   {0, -1, 0},
+                                 {0, 0, 1},  {0, 0, -1},  {1, 1, 0},  {-1, -1, 0}, {1, -1, 0},
+                                 {-1, 1, 0}, {1, 0, 1},   {-1, 0, -1}, {1, 0, -1}, {-1, 0, 1},
+                                 {0, 1, 1},  {0, -1, -1}, {0, 1, -1}, {0, -1, 1}};
+
+__device__ __forceinline__ int dopp(int k) { return k == 0 ? 0 : ((k & 1) ? k + 1 : k - 1); }
+
+__device__ __forceinline__ int dwrap(int v, int n, bool periodic) {
+  if (v >= 0 && v < n) return v;
+  if (!periodic) return -1;
+  return (v % n + n) % n;
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " +
+                                                 cudaGetErrorString(e));
+}
+
+// One thread per cell; grid (x blocks, y, z).
+__global__ void k_cellwords(const uint8_t* __restrict__ flags, const uint8_t* __restrict__ glo,
+                            const uint8_t* __restrict__ ghi, int nx, int ny, int nz, bool px,
+                            bool py, bool pz, bool slab, uint32_t* __restrict__ cellw,
+                            int32_t* __restrict__ count) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= nx) return;
+  const int64_t c = ((int64_t)z * ny + y) * nx + x;
+  const uint8_t own = flags[c];
+  if (own != 0) {
+    cellw[c] = kNonFluid | ((uint32_t)own << kFlagShift);
+    count[c] = 0;
+    return;
+  }
+  uint32_t w = 0;
+#pragma unroll
+  for (int j = 1; j < 19; ++j) {
+    const int ys = dwrap(y - cE[j][1], ny, py);
+    const int zs = dwrap(z - cE[j][2], nz, pz);
+    bool nonfluid;
+    if (ys < 0 || zs < 0) {
+      nonfluid = true;
+    } else {
+      const int xr = x - cE[j][0];
+      if (slab && xr < 0) {
+        nonfluid = glo[(int64_t)zs * ny + ys] != 0;
+      } else if (slab && xr >= nx) {
+        nonfluid = ghi[(int64_t)zs * ny + ys] != 0;
+      } else {
+        const int xs = slab ? xr : dwrap(xr, nx, px);
+        nonfluid = xs < 0 || flags[((int64_t)zs * ny + ys) * nx + xs] != 0;
+      }
+    }
+    if (nonfluid) w |= 1u << j;
+  }
+  cellw[c] = w;
+  count[c] = __popc(w & kBounceMask);
+}
+
+// Non-fluid cells sharing an aligned 4-cell (32-byte) group with a fluid cell.
+__global__ void k_fill_sectors(uint32_t* __restrict__ cellw, int64_t cells) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c0 = g * 4;
+  if (c0 >= cells) return;
+  const int64_t c1 = c0 + 4 < cells ? c0 + 4 : cells;
+  bool anyfluid = false;
+  for (int64_t c = c0; c < c1; ++c) anyfluid |= !(cellw[c] & kNonFluid);
+  if (!anyfluid) return;
+  for (int64_t c = c0; c < c1; ++c)
+    if (cellw[c] & kNonFluid) cellw[c] |= kFillSector;
+}
+
+__global__ void k_chunkbase(const int32_t* __restrict__ base, int32_t* __restrict__ chunkbase,
+                            int nx, int64_t rows, int nchunk) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * nchunk) return;
+  const int64_t r = i / nchunk;
+  const int ch = (int)(i - r * nchunk);
+  chunkbase[i] = base[r * nx + ch * 32];
+}
+
+struct ToI64 {
+  __host__ __device__ int64_t operator()(int32_t v) const { return v; }
+};
+
+// One thread per input link (validation as pgpu_create's contract, records).
+__global__ void k_links(LinkSetupArgs a, uint32_t* __restrict__ seen,
+                        unsigned long long* __restrict__ err,
+                        unsigned long long* __restrict__ fallbacks, int* __restrict__ moving_any) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool fb = false, mv = false;
+  int code = 0;
+  if (i < a.n_links) {
+    const int64_t c = a.link_cell[i];
+    const int k = a.link_dir[i];
+    if (c < 0 || c >= a.cells || (a.cellw[c] & kNonFluid)) {
+      code = kSetupErrCell;
+    } else if (k < 1 || k > 18) {
+      code = kSetupErrDir;
+    } else {
+      const int j = dopp(k);
+      const uint32_t w = a.cellw[c];
+      if (!((w >> j) & 1u)) {
+        code = kSetupErrFluidNeighbour;
+      } else {
+        const int64_t r = (int64_t)a.cellbase[c] + __popc(w & ((1u << j) - 1u) & kBounceMask);
+        const uint32_t bit = 1u << (r & 31);
+        if (atomicOr(&seen[r >> 5], bit) & bit) {
+          code = kSetupErrDuplicate;
+        } else {
+          const int64_t sf = a.link_second[i];
+          mv = a.link_moving && a.link_moving[i];
+          fb = a.cli && sf == -1;  // simulation.cpp:97-101
+          double rec = __longlong_as_double(0x7FF8000000000000ll);  // SBB
+          if (mv) {
+            rec = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+          } else if (a.cli && sf != -1) {
+            if ((w >> k) & 1u) {
+              code = kSetupErrSecondNotFluid;
+            } else {
+              const int nx = a.nx, ny = a.ny, nz = a.nz;
+              const int x = (int)(c % nx), y = (int)((c / nx) % ny),
+                        z = (int)(c / ((int64_t)nx * ny));
+              const int xr = x - cE[k][0];
+              const int ys = dwrap(y - cE[k][1], ny, a.py);
+              const int zs = dwrap(z - cE[k][2], nz, a.pz);
+              bool ok;
+              if (a.slab && (xr < 0 || xr >= nx)) {
+                ok = sf == -2;
+              } else {
+                const int xs = a.slab ? xr : dwrap(xr, nx, a.px);
+                ok = sf == ((int64_t)zs * ny + ys) * nx + xs;
+              }
+              if (!ok) code = kSetupErrSecondCell;
+              // boundary.cpp:27-28 from the fp32 q, round-to-nearest each op
+              const double q = (double)a.link_q[i];
+              rec = __ddiv_rn(__dsub_rn(1.0, __dmul_rn(2.0, q)), __dadd_rn(1.0, __dmul_rn(2.0, q)));
+            }
+          }
+          if (a.recs) a.recs[r] = rec;
+        }
+      }
+    }
+  }
+  if (code) atomicMin(err, ((unsigned long long)i << 8) | (unsigned long long)code);
+  const unsigned m = __activemask();
+  const unsigned bf = __ballot_sync(m, fb), bm = __ballot_sync(m, mv);
+  if ((threadIdx.x & 31) == (__ffs(m) - 1)) {
+    if (bf) atomicAdd(fallbacks, (unsigned long long)__popc(bf));
+    if (bm) atomicOr(moving_any, 1);
+  }
+}
+
+__global__ void k_fill_nan(double* __restrict__ recs, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) recs[i] = __longlong_as_double(0x7FF8000000000000ll);
+}
+
+// simulation.cpp:104-112: links whose wall neighbour lies in plane nz-1 move.
+__global__ void k_mark_lid(const uint32_t* __restrict__ cellw, const int32_t* __restrict__ base,
+                           double* __restrict__ recs, int nx, int ny, int nz,
+                           int* __restrict__ any) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= nx) return;
+  const int64_t c = ((int64_t)z * ny + y) * nx + x;
+  const uint32_t w = cellw[c];
+  if ((w & kNonFluid) || !(w & kBounceMask)) return;
+  int64_t r = base[c];
+  bool hit = false;
+  for (int j = 1; j < 19; ++j) {
+    if (!((w >> j) & 1u)) continue;
+    if (z + cE[dopp(j)][2] == nz - 1) {
+      recs[r] = __longlong_as_double(0x7FF0000000000000ll);
+      hit = true;
+    }
+    ++r;
+  }
+  if (hit) atomicOr(any, 1);
+}
+
+__global__ void k_unpack_flags(const uint32_t* __restrict__ cellw, uint8_t* __restrict__ out,
+                               int64_t cells) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < cells) out[c] = (uint8_t)(cellw[c] >> kFlagShift);
+}
+
+inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void setup_cellwords(const CellSetupArgs& a, cudaStream_t s) {
+  const dim3 blk(128), grid((a.nx + 127) / 128, a.ny, a.nz);
+  k_cellwords<<<grid, blk, 0, s>>>(a.flags, a.ghost_lo, a.ghost_hi, a.nx, a.ny, a.nz, a.px, a.py,
+                                   a.pz, a.slab, a.cellw, a.count);
+  ck(cudaGetLastError(), "k_cellwords");
+  const int64_t cells = (int64_t)a.nx * a.ny * a.nz;
+  if (a.fill_sectors) {
+    k_fill_sectors<<<blocks((cells + 3) / 4, 256), 256, 0, s>>>(a.cellw, cells);
+    ck(cudaGetLastError(), "k_fill_sectors");
+  }
+}
+
+int64_t setup_bases(const int32_t* count, int32_t* base, int32_t* chunkbase, int nx, int64_t rows,
+                    int nchunk, void* scratch, size_t scratch_bytes, int64_t* d_total,
+                    cudaStream_t s) {
+  const int64_t cells = (int64_t)nx * rows;
+  cub::TransformInputIterator<int64_t, ToI64, const int32_t*> wide(count, ToI64());
+  size_t need_r = 0, need_s = 0;
+  ck(cub::DeviceReduce::Sum(nullptr, need_r, wide, d_total, cells, s), "reduce size");
+  ck(cub::DeviceScan::ExclusiveSum(nullptr, need_s, count, base, cells, s), "scan size");
+  if (need_r > scratch_bytes || need_s > scratch_bytes) return -1;
+  ck(cub::DeviceReduce::Sum(scratch, scratch_bytes, wide, d_total, cells, s), "reduce");
+  int64_t total = 0;
+  ck(cudaMemcpyAsync(&total, d_total, sizeof(total), cudaMemcpyDeviceToHost, s), "total");
+  ck(cudaStreamSynchronize(s), "total sync");
+  if (total > INT32_MAX) return total;  // caller rejects; the scan would overflow
+  ck(cub::DeviceScan::ExclusiveSum(scratch, scratch_bytes, count, base, cells, s), "scan");
+  k_chunkbase<<<blocks(rows * nchunk, 256), 256, 0, s>>>(base, chunkbase, nx, rows, nchunk);
+  ck(cudaGetLastError(), "k_chunkbase");
+  return total;
+}
+
+size_t setup_scratch_bytes(int64_t cells) {
+  cub::TransformInputIterator<int64_t, ToI64, const int32_t*> wide(nullptr, ToI64());
+  size_t need_r = 0, need_s = 0;
+  cub::DeviceReduce::Sum(nullptr, need_r, wide, (int64_t*)nullptr, cells);
+  cub::DeviceScan::ExclusiveSum(nullptr, need_s, (const int32_t*)nullptr, (int32_t*)nullptr, cells);
+  return need_r > need_s ? need_r : need_s;
+}
+
+void setup_links(const LinkSetupArgs& a, uint32_t* seen_bits, unsigned long long* d_err,
+                 unsigned long long* d_fallbacks, int* d_moving, cudaStream_t s) {
+  if (a.n_links == 0) return;
+  k_links<<<blocks(a.n_links, 256), 256, 0, s>>>(a, seen_bits, d_err, d_fallbacks, d_moving);
+  ck(cudaGetLastError(), "k_links");
+}
+
+void fill_records_nan(double* recs, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  k_fill_nan<<<blocks(n, 256), 256, 0, s>>>(recs, n);
+  ck(cudaGetLastError(), "k_fill_nan");
+}
+
+void mark_lid_links(const uint32_t* cellw, const int32_t* base, double* recs, int nx, int ny,
+                    int nz, int* d_any, cudaStream_t s) {
+  const dim3 blk(128), grid((nx + 127) / 128, ny, nz);
+  k_mark_lid<<<grid, blk, 0, s>>>(cellw, base, recs, nx, ny, nz, d_any);
+  ck(cudaGetLastError(), "k_mark_lid");
+}
+
+void unpack_flags(const uint32_t* cellw, uint8_t* out, int64_t cells, cudaStream_t s) {
+  k_unpack_flags<<<blocks(cells, 256), 256, 0, s>>>(cellw, out, cells);
+  ck(cudaGetLastError(), "k_unpack_flags");
+}
+
+}  // namespace pgpu

@@ -27,6 +27,7 @@
 #include "host_common.h"
 #include "kernels.h"
 #include "kparams.h"
+#include "setup.h"
 
 namespace pgpu {
 void moments(const double f[19], double rho0, double& drho, double u[3]);
@@ -69,21 +70,9 @@ struct pgpu_sim {
   double lo = 0.0, hi = 0.0;
   int64_t fluid_cells = 0;
   int32_t cli_fallbacks = 0;
-  // link structures (host mirror)
-  // w + link base per cell (kparams.h); default-initialised (no 0.5 GB memset)
-  struct CellWords {
-    std::unique_ptr<CellWord[]> buf;
-    CellWord& operator[](int64_t i) { return buf[i]; }
-    const CellWord& operator[](int64_t i) const { return buf[i]; }
-    void resize(int64_t n) { buf.reset(new CellWord[n]); }
-  } cellword;
-  bool cellbase_uploaded = false;
-  std::vector<LinkRec> recs;       // host-computed CLI coefficient / NaN / +inf
-  std::vector<uint8_t> rec_kind;   // LinkKind per record
-  std::vector<float> rec_q;
+  // link structures live on the device only (setup.cu builds them)
   int64_t n_links = 0;
   bool any_moving = false;
-  bool records_uploaded = false;
   double lid[3] = {0.0, 0.0, 0.0};
   // GLBM (set_porous)
   bool porous = false, glbm_active = false;
@@ -226,49 +215,13 @@ struct pgpu_sim {
 
   bool records_needed() const { return scheme == PGPU_CLI || any_moving; }
 
-  // boundary.cpp:27-28 on the host: c = (1 - 2q)/(1 + 2q) from the fp32 q.
-  void encode_records() {
-    recs.resize(n_links);
-    parallel_for(n_links, [&](int64_t a, int64_t b, int) {
-      for (int64_t r = a; r < b; ++r) {
-        if (rec_kind[r] == kLinkCLI) {
-          const double q = rec_q[r];
-          recs[r] = (1.0 - 2.0 * q) / (1.0 + 2.0 * q);
-        } else if (rec_kind[r] == kLinkMoving) {
-          recs[r] = std::numeric_limits<double>::infinity();
-        } else {
-          recs[r] = std::numeric_limits<double>::quiet_NaN();
-        }
-      }
-    });
-  }
-
-  // Per-cell link bases are read only by the per-cell kernels (slab edge
-  // columns, the persistent small-domain sweep, the plain sweep), so they are
-  // uploaded on first need.
-  void upload_cellbase() {
-    if (cellbase_uploaded) return;
-    std::vector<int32_t> b(cells);
-    parallel_for(cells, [&](int64_t a, int64_t e, int) {
-      for (int64_t c = a; c < e; ++c) b[c] = cellword[c].base;
-    });
-    CK(cudaMemcpy(d_cellbase, b.data(), sizeof(int32_t) * cells, cudaMemcpyHostToDevice));
-    cellbase_uploaded = true;
-  }
-
-  void upload_records() {
-    if (slab || persistent || g_plain_sweep()) upload_cellbase();
-    if (n_links == 0) {
-      records_uploaded = true;
-      return;
-    }
-    encode_records();
-    if (!d_recs) CK(cudaMalloc(&d_recs, sizeof(LinkRec) * n_links));
-    CK(cudaMemcpyAsync(d_recs, recs.data(), sizeof(LinkRec) * n_links, cudaMemcpyHostToDevice,
-                       stream));
-    CK(cudaStreamSynchronize(stream));
+  // Records are built by pgpu_create when the scheme is CLI or a link moves;
+  // a later set_lid_velocity on an SBB simulation starts from all-SBB (NaN).
+  void ensure_records() {
+    if (d_recs || n_links == 0) return;
+    CK(cudaMalloc(&d_recs, sizeof(LinkRec) * n_links));
+    fill_records_nan(d_recs, n_links, stream);
     kp.links = d_recs;
-    records_uploaded = true;
     drop_graphs();
   }
 
@@ -335,7 +288,6 @@ struct pgpu_sim {
 
   void step(int64_t n) {
     if (slab) throw ConfigError("slab simulations step through pgpu_step_part + halo exchange");
-    if (records_needed() && !records_uploaded) upload_records();
     for (int64_t i = 0; i < n;) {
       if (!post) {
         k0();
@@ -493,191 +445,144 @@ struct pgpu_sim {
 
 namespace {
 
-inline int wrap(int v, int n, bool periodic) {
-  if (v >= 0 && v < n) return v;
-  if (!periodic) return -1;
-  return (v % n + n) % n;
+// Device temporary freed at scope exit.
+struct DevBuf {
+  void* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+template <class T>
+void upload(DevBuf& b, const T* host, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  CK(cudaMalloc(&b.p, sizeof(T) * n));
+  CK(cudaMemcpyAsync(b.p, host, sizeof(T) * n, cudaMemcpyHostToDevice, st));
 }
 
-void build_links(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors) {
-  const int nx = s->nx, ny = s->ny, nz = s->nz;
-  const bool trace = std::getenv("PGPU_TRACE") != nullptr;
-  auto t0 = std::chrono::steady_clock::now();
-  auto lap = [&](const char* what) {
-    if (!trace) return;
-    const auto t1 = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[pgpu]   build_links %-18s %8.1f ms\n", what,
-                 std::chrono::duration<double, std::milli>(t1 - t0).count());
-    t0 = t1;
-  };
-  const uint8_t* flags = g->flags;
-  // bit0 non-fluid; bit j: upstream x - e_j is non-fluid or outside the domain.
-  // Row-wise: the 18 source rows of row (y, z) are resolved once, then a
-  // tight loop over x; only x = 0 and x = nx-1 need the wrap / ghost rules.
-  s->cellword.resize(s->cells);
-  parallel_for((int64_t)nz * ny, [&](int64_t ra, int64_t rb, int) {
-    std::vector<uint32_t> wrow(nx);
-    const uint8_t* srow[19];
-    bool srow_ok[19];
-    for (int64_t r = ra; r < rb; ++r) {
-      const int z = (int)(r / ny), y = (int)(r % ny);
-      const int64_t row = r * nx;
-      const uint8_t* own = flags + row;
-      for (int j = 1; j < 19; ++j) {
-        const int ys = wrap(y - kE[j][1], ny, s->per[1]);
-        const int zs = wrap(z - kE[j][2], nz, s->per[2]);
-        srow_ok[j] = ys >= 0 && zs >= 0;
-        srow[j] = srow_ok[j] ? flags + ((int64_t)zs * ny + ys) * nx : nullptr;
-      }
-      // interior columns: one contiguous (vectorisable) pass per direction
-      for (int x = 0; x < nx; ++x) wrow[x] = own[x] != 0 ? kNonFluid : 0u;
-      for (int j = 1; j < 19; ++j) {
-        const uint32_t bit = 1u << j;
-        if (!srow_ok[j]) {
-          for (int x = 1; x < nx - 1; ++x) wrow[x] |= bit;
-          continue;
-        }
-        const uint8_t* src = srow[j] - kE[j][0];
-        for (int x = 1; x < nx - 1; ++x) wrow[x] |= (src[x] != 0) ? bit : 0u;
-      }
-      // x = 0 and x = nx-1: wrap / ghost rules
-      auto edge_word = [&](int x) -> uint32_t {
-        uint32_t w = 0;
-        for (int j = 1; j < 19; ++j) {
-          bool nonfluid;
-          if (!srow_ok[j]) {
-            nonfluid = true;
-          } else {
-            const int xr = x - kE[j][0];
-            const int ys = wrap(y - kE[j][1], ny, s->per[1]);
-            const int zs = wrap(z - kE[j][2], nz, s->per[2]);
-            if (s->slab && xr < 0) {
-              nonfluid = g->ghost_flags_lo[(int64_t)zs * ny + ys] != 0;
-            } else if (s->slab && xr >= nx) {
-              nonfluid = g->ghost_flags_hi[(int64_t)zs * ny + ys] != 0;
-            } else {
-              const int xs = s->slab ? xr : wrap(xr, nx, s->per[0]);
-              nonfluid = xs < 0 || srow[j][xs] != 0;
-            }
-          }
-          if (nonfluid) w |= 1u << j;
-        }
-        return w;
-      };
-      wrow[0] = own[0] != 0 ? kNonFluid : edge_word(0);
-      if (nx > 1) wrow[nx - 1] = own[nx - 1] != 0 ? kNonFluid : edge_word(nx - 1);
-      for (int x = 0; x < nx; ++x) {
-        CellWord& cw = s->cellword[row + x];
-        cw.w = (wrow[x] & kNonFluid) ? (kNonFluid | (uint32_t)own[x] << kFlagShift) : wrow[x];
-        cw.base = 0;
-      }
-    }
-  });
-  lap("cell words");
-  // non-fluid cells sharing an aligned 4-cell (32-byte) group with fluid
-  // cells are zero-filled by the sweep, so no DRAM sector is partly written
-  const int64_t ngroups = (s->cells + 3) / 4;
-  if (fill_sectors) {
-    parallel_for(ngroups, [&](int64_t a, int64_t b, int) {
-      for (int64_t gi = a; gi < b; ++gi) {
-        const int64_t c0 = gi * 4, c1 = std::min<int64_t>(c0 + 4, s->cells);
-        bool anyfluid = false;
-        for (int64_t c = c0; c < c1; ++c) anyfluid |= !(s->cellword[c].w & kNonFluid);
-        if (!anyfluid) continue;
-        for (int64_t c = c0; c < c1; ++c)
-          if (s->cellword[c].w & kNonFluid) s->cellword[c].w |= kFillSector;
-      }
-    });
+const char* setup_error_text(int code) {
+  switch (code) {
+    case kSetupErrCell: return "boundary link on a non-fluid or out-of-range cell";
+    case kSetupErrDir: return "boundary link direction must be in 1..18";
+    case kSetupErrFluidNeighbour: return "boundary link points to a fluid neighbour";
+    case kSetupErrDuplicate: return "duplicate boundary link";
+    case kSetupErrSecondNotFluid: return "CLI second_fluid is not a fluid cell";
+    case kSetupErrSecondCell: return "CLI second_fluid must be the cell x_f1 - e_k";
+    default: return "invalid boundary link";
   }
-  lap("fill bits");
-  // per-cell record base: exclusive prefix of bounce counts (two-pass parallel scan)
-  const int nt = hw_threads();
-  std::vector<int64_t> part(nt + 1, 0);
-  auto count_of = [&](int64_t c) -> int64_t {
-    const uint32_t w = s->cellword[c].w;
-    return (w & kNonFluid) ? 0 : __builtin_popcount(w & kBounceMask);
-  };
-  parallel_for(s->cells, [&](int64_t a, int64_t b, int t) {
-    int64_t acc = 0;
-    for (int64_t c = a; c < b; ++c) acc += count_of(c);
-    part[t + 1] = acc;
-  }, nt);
-  for (int t = 0; t < nt; ++t) part[t + 1] += part[t];
-  const int64_t total = part[nt];
-  if (total > std::numeric_limits<int32_t>::max()) throw ConfigError("too many boundary links");
-  parallel_for(s->cells, [&](int64_t a, int64_t b, int t) {
-    int64_t acc = part[t];
-    for (int64_t c = a; c < b; ++c) {
-      s->cellword[c].base = (int32_t)acc;
-      acc += count_of(c);
-    }
-  }, nt);
-  if (g->n_links != total) {
+}
+
+// Builds cell words, record bases and link records on the device from the
+// caller's flags and link list (setup.cu).  Only the caller's arrays cross
+// PCIe: flags 1 B/cell (+ ghost columns), links 25 B/link.
+template <class Lap>
+void device_setup(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors, Lap&& lap) {
+  const cudaStream_t st = s->stream;
+  const int64_t cells = s->cells, rows = (int64_t)s->ny * s->nz;
+  const int nchunk = (s->nx + 31) / 32;
+  const int64_t L = g->n_links;
+  DevBuf flags, glo, ghi, count, scratch, total, lf, ls, ld, lq, lm, seen, res;
+  upload(flags, g->flags, cells, st);
+  if (s->slab) {
+    upload(glo, g->ghost_flags_lo, rows, st);
+    upload(ghi, g->ghost_flags_hi, rows, st);
+  }
+  upload(lf, g->link_fluid_cell, L, st);
+  upload(ls, g->link_second_fluid, L, st);
+  upload(ld, g->link_direction, L, st);
+  upload(lq, g->link_q, L, st);
+  if (g->link_moving) upload(lm, g->link_moving, L, st);
+  lap("upload flags+links");
+
+  CK(cudaMalloc(&s->d_cellw, sizeof(uint32_t) * cells));
+  CK(cudaMalloc(&s->d_cellbase, sizeof(int32_t) * cells));
+  CK(cudaMalloc(&s->d_chunkbase, sizeof(int32_t) * rows * nchunk));
+  CK(cudaMalloc(&count.p, sizeof(int32_t) * cells));
+  CellSetupArgs ca;
+  ca.flags = flags.as<uint8_t>();
+  ca.ghost_lo = glo.as<uint8_t>();
+  ca.ghost_hi = ghi.as<uint8_t>();
+  ca.nx = s->nx;
+  ca.ny = s->ny;
+  ca.nz = s->nz;
+  ca.px = s->per[0];
+  ca.py = s->per[1];
+  ca.pz = s->per[2];
+  ca.slab = s->slab;
+  ca.fill_sectors = fill_sectors;
+  ca.cellw = s->d_cellw;
+  ca.count = count.as<int32_t>();
+  setup_cellwords(ca, st);
+  const size_t sb = setup_scratch_bytes(cells);
+  CK(cudaMalloc(&scratch.p, sb));
+  CK(cudaMalloc(&total.p, sizeof(int64_t)));
+  const int64_t tot = setup_bases(count.as<int32_t>(), s->d_cellbase, s->d_chunkbase, s->nx, rows,
+                                  nchunk, scratch.p, sb, total.as<int64_t>(), st);
+  if (tot < 0) throw CudaError("setup: scan scratch too small");
+  if (tot > std::numeric_limits<int32_t>::max()) throw ConfigError("too many boundary links");
+  if (L != tot) {
     std::ostringstream os;
-    os << "boundary links (" << g->n_links << ") do not match the fluid->non-fluid lattice "
-       << "directions of the flag field (" << total << "); links must close exactly those directions";
+    os << "boundary links (" << L << ") do not match the fluid->non-fluid lattice "
+       << "directions of the flag field (" << tot << "); links must close exactly those directions";
     throw ConfigError(os.str());
   }
-  lap("prefix");
-  s->n_links = total;
-  s->rec_kind.assign(total, kLinkSBB);
-  s->rec_q.assign(total, 0.5f);
-  std::vector<uint8_t> seen(total, 0);
-  std::vector<int64_t> fallbacks(nt, 0);
-  std::vector<uint8_t> moving_any(nt, 0);
-  std::vector<std::string> errs(nt);
-  parallel_for(g->n_links, [&](int64_t a, int64_t b, int t) {
-    try {
-      for (int64_t i = a; i < b; ++i) {
-        const int64_t c = g->link_fluid_cell[i];
-        const int k = g->link_direction[i];
-        if (c < 0 || c >= s->cells || flags[c] != 0)
-          throw ConfigError("boundary link on a non-fluid or out-of-range cell");
-        if (k < 1 || k > 18) throw ConfigError("boundary link direction must be in 1..18");
-        const int j = opposite(k);
-        const uint32_t w = s->cellword[c].w;
-        if (!((w >> j) & 1u)) throw ConfigError("boundary link points to a fluid neighbour");
-        const int64_t r = s->cellword[c].base + __builtin_popcount(w & ((1u << j) - 1u) & kBounceMask);
-        if (__atomic_exchange_n(&seen[r], (uint8_t)1, __ATOMIC_RELAXED))
-          throw ConfigError("duplicate boundary link");
-        s->rec_q[r] = g->link_q[i];
-        const int64_t sf = g->link_second_fluid[i];
-        const bool moving = g->link_moving && g->link_moving[i];
-        if (s->scheme == PGPU_CLI && sf == -1) ++fallbacks[t];  // simulation.cpp:97-101
-        if (moving) {
-          s->rec_kind[r] = kLinkMoving;
-          moving_any[t] = 1;
-        } else if (s->scheme == PGPU_CLI && sf != -1) {
-          // second_fluid must be the upstream cell x - e_k, which is then fluid
-          if ((w >> k) & 1u) throw ConfigError("CLI second_fluid is not a fluid cell");
-          const int x = (int)(c % nx), y = (int)((c / nx) % ny), z = (int)(c / ((int64_t)nx * ny));
-          const int xr = x - kE[k][0];
-          const int ys = wrap(y - kE[k][1], ny, s->per[1]);
-          const int zs = wrap(z - kE[k][2], nz, s->per[2]);
-          bool ok;
-          if (s->slab && (xr < 0 || xr >= nx)) {
-            ok = sf == -2;
-          } else {
-            const int xs = s->slab ? xr : wrap(xr, nx, s->per[0]);
-            ok = sf == ((int64_t)zs * ny + ys) * nx + xs;
-          }
-          if (!ok) throw ConfigError("CLI second_fluid must be the cell x_f1 - e_k");
-          s->rec_kind[r] = kLinkCLI;
-        }
-      }
-    } catch (const std::exception& e) {
-      errs[t] = e.what();
-    }
-  }, nt);
-  lap("link records");
-  for (const std::string& e : errs)
-    if (!e.empty()) throw ConfigError(e);
-  s->any_moving = false;
-  s->cli_fallbacks = 0;
-  for (int t = 0; t < nt; ++t) {
-    s->cli_fallbacks += (int32_t)fallbacks[t];
-    s->any_moving = s->any_moving || moving_any[t];
+  s->n_links = tot;
+  s->kp.nchunk = nchunk;
+  lap("cell words+bases");
+
+  // records: CLI coefficients / SBB / moving wall; validation in the same pass
+  const bool cli = s->scheme == PGPU_CLI;
+  if (L > 0 && (cli || g->link_moving)) CK(cudaMalloc(&s->d_recs, sizeof(LinkRec) * L));
+  const int64_t words = (L + 31) / 32;
+  if (words) {
+    CK(cudaMalloc(&seen.p, sizeof(uint32_t) * words));
+    CK(cudaMemsetAsync(seen.p, 0, sizeof(uint32_t) * words, st));
   }
+  struct Res {
+    unsigned long long err, fallbacks;
+    int moving;
+  } host_res{~0ull, 0ull, 0};
+  CK(cudaMalloc(&res.p, sizeof(Res)));
+  CK(cudaMemcpyAsync(res.p, &host_res, sizeof(Res), cudaMemcpyHostToDevice, st));
+  LinkSetupArgs la;
+  la.n_links = L;
+  la.cells = cells;
+  la.nx = s->nx;
+  la.ny = s->ny;
+  la.nz = s->nz;
+  la.px = s->per[0];
+  la.py = s->per[1];
+  la.pz = s->per[2];
+  la.slab = s->slab;
+  la.cli = cli;
+  la.link_cell = lf.as<int64_t>();
+  la.link_second = ls.as<int64_t>();
+  la.link_dir = ld.as<int32_t>();
+  la.link_q = lq.as<float>();
+  la.link_moving = lm.as<uint8_t>();
+  la.cellw = s->d_cellw;
+  la.cellbase = s->d_cellbase;
+  la.recs = s->d_recs;
+  Res* dr = res.as<Res>();
+  setup_links(la, seen.as<uint32_t>(), &dr->err, &dr->fallbacks, &dr->moving, st);
+  CK(cudaMemcpyAsync(&host_res, res.p, sizeof(Res), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (host_res.err != ~0ull) throw ConfigError(setup_error_text((int)(host_res.err & 0xFF)));
+  s->cli_fallbacks = cli ? (int32_t)host_res.fallbacks : 0;
+  s->any_moving = host_res.moving != 0;
+  if (s->d_recs && !s->records_needed()) {
+    CK(cudaFree(s->d_recs));
+    s->d_recs = nullptr;
+  }
+  s->kp.links = s->d_recs;
+  lap("link records");
 }
 
 }  // namespace
@@ -761,36 +666,13 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
       t0 = t1;
     };
     const char* fill_env = std::getenv("PGPU_FILL_SECTORS");
-    build_links(s.get(), g, !(fill_env && fill_env[0] == '0'));
-    lap("build_links");
+    device_setup(s.get(), g, !(fill_env && fill_env[0] == '0'), lap);
 
     // device buffers: two full PDF grids, zero-filled like the reference
     const size_t fbytes = sizeof(double) * 19 * (size_t)s->ks;
     for (int b = 0; b < 2; ++b) {
       CK(cudaMalloc(&s->f[b], fbytes));
       CK(cudaMemsetAsync(s->f[b], 0, fbytes, s->stream));
-    }
-    {  // split the host words: 4-byte words, per-cell bases, per-chunk bases
-      const int64_t rows = (int64_t)s->ny * s->nz;
-      const int nchunk = (s->nx + 31) / 32;
-      std::vector<uint32_t> w(s->cells);
-      std::vector<int32_t> cb(rows * nchunk);
-      parallel_for(rows, [&](int64_t ra, int64_t rb, int) {
-        for (int64_t r = ra; r < rb; ++r) {
-          for (int x = 0; x < s->nx; ++x) {
-            const CellWord& cw = s->cellword[r * s->nx + x];
-            w[r * s->nx + x] = cw.w;
-            if ((x & 31) == 0) cb[r * nchunk + (x >> 5)] = cw.base;
-          }
-        }
-      });
-      CK(cudaMalloc(&s->d_cellw, sizeof(uint32_t) * s->cells));
-      CK(cudaMalloc(&s->d_cellbase, sizeof(int32_t) * s->cells));
-      CK(cudaMalloc(&s->d_chunkbase, sizeof(int32_t) * cb.size()));
-      CK(cudaMemcpy(s->d_cellw, w.data(), sizeof(uint32_t) * s->cells, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(s->d_chunkbase, cb.data(), sizeof(int32_t) * cb.size(),
-                    cudaMemcpyHostToDevice));
-      s->kp.nchunk = nchunk;
     }
     CK(cudaMalloc(&s->d_feq, sizeof(double) * 19));
     CK(cudaMalloc(&s->d_flags, sizeof(int) * 2));
@@ -813,16 +695,15 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     kp.cellw = s->d_cellw;
     kp.cellbase = s->d_cellbase;
     kp.chunkbase = s->d_chunkbase;
-    lap("alloc+upload cellword");
+    lap("alloc pdfs");
     {  // two PDF grids well inside the 126 MB L2 -> persistent multi-step sweeps
       const char* e = std::getenv("PGPU_PERSISTENT");
       const double state_bytes = 2.0 * 19.0 * 8.0 * (double)s->ks;
       s->persistent = !s->slab && (e ? e[0] == '1' : state_bytes <= 48e6);
     }
     s->refresh_params();
-    if (s->records_needed()) s->upload_records();
     CK(cudaStreamSynchronize(s->stream));
-    lap("records");
+    lap("params+sync");
     *out = s.release();
   });
 }
@@ -880,24 +761,19 @@ int pgpu_set_lid_velocity(pgpu_sim* sim, const double u[3]) {
     SIM_CHECK();
     sim->sync();
     for (int i = 0; i < 3; ++i) sim->lid[i] = u[i];
-    const int nx = sim->nx, ny = sim->ny, nz = sim->nz;
-    for (int64_t c = 0; c < sim->cells; ++c) {
-      const uint32_t w = sim->cellword[c].w;
-      if ((w & kNonFluid) || !(w & kBounceMask)) continue;
-      int64_t r = sim->cellword[c].base;
-      const int z = (int)(c / ((int64_t)nx * ny));
-      for (int j = 1; j < 19; ++j) {
-        if (!((w >> j) & 1u)) continue;
-        const int k = opposite(j);
-        if (z + kE[k][2] == nz - 1) {
-          sim->rec_kind[r] = kLinkMoving;
-          sim->any_moving = true;
-        }
-        ++r;
-      }
+    sim->ensure_records();  // SBB scheme: all-SBB records first
+    if (sim->d_recs) {
+      DevBuf any;
+      CK(cudaMalloc(&any.p, sizeof(int)));
+      CK(cudaMemsetAsync(any.p, 0, sizeof(int), sim->stream));
+      mark_lid_links(sim->d_cellw, sim->d_cellbase, sim->d_recs, sim->nx, sim->ny, sim->nz,
+                     any.as<int>(), sim->stream);
+      int hit = 0;
+      CK(cudaMemcpyAsync(&hit, any.p, sizeof(int), cudaMemcpyDeviceToHost, sim->stream));
+      CK(cudaStreamSynchronize(sim->stream));
+      if (hit) sim->any_moving = true;
     }
     sim->refresh_params();
-    if (sim->records_needed()) sim->upload_records();
   });
 }
 
@@ -978,9 +854,11 @@ int pgpu_get_flags(pgpu_sim* sim, uint8_t* out) {
   return guard([&] {
     SIM_CHECK();
     if (!out) throw std::invalid_argument("null output");
-    parallel_for(sim->cells, [&](int64_t a, int64_t b, int) {
-      for (int64_t c = a; c < b; ++c) out[c] = (uint8_t)(sim->cellword[c].w >> kFlagShift);
-    });
+    DevBuf tmp;
+    CK(cudaMalloc(&tmp.p, sim->cells));
+    unpack_flags(sim->d_cellw, tmp.as<uint8_t>(), sim->cells, sim->stream);
+    CK(cudaMemcpyAsync(out, tmp.p, sim->cells, cudaMemcpyDeviceToHost, sim->stream));
+    CK(cudaStreamSynchronize(sim->stream));
   });
 }
 
@@ -1213,7 +1091,6 @@ int pgpu_step_part(pgpu_sim* sim, int32_t part) {
     SIM_CHECK();
     if (!sim->slab) throw ConfigError("split steps need a slab geometry");
     if (!sim->send_lo) throw ConfigError("halo buffers not set");
-    if (sim->records_needed() && !sim->records_uploaded) sim->upload_records();
     if (part == 0) {
       if (sim->pending) throw ConfigError("previous split step not finished");
       if (!sim->post) {
