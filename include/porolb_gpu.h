@@ -286,6 +286,10 @@ int pgpu_halo_parity(pgpu_sim* sim, int32_t* parity);
 /* Split step for overlap: part 0 = edge columns (fills send buffers),
  * part 1 = interior; pgpu_step_finish advances the step counter. */
 int pgpu_step_part(pgpu_sim* sim, int32_t part);
+/* Same, with the part's kernels on `stream` (a cudaStream_t; NULL = the
+ * simulation's stream) so edge columns + exchange and the interior can run
+ * on two streams; the caller orders them (dist.py DistTransport). */
+int pgpu_step_part_on(pgpu_sim* sim, int32_t part, void* stream);
 int pgpu_step_finish(pgpu_sim* sim);
 
 /* ---- file formats (io.hpp; byte-identical to the reference's writers) ------ */

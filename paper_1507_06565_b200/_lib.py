@@ -115,6 +115,7 @@ SIGNATURES = {
     "pgpu_set_halo_buffers": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "pgpu_halo_parity": (C.c_int, [vp, P(i32)]),
     "pgpu_step_part": (C.c_int, [vp, i32]),
+    "pgpu_step_part_on": (C.c_int, [vp, i32, vp]),
     "pgpu_step_finish": (C.c_int, [vp]),
     "pgpu_get_flags": (C.c_int, [vp, P(u8)]),
     # file formats (io.hpp)

@@ -1086,11 +1086,19 @@ int pgpu_halo_parity(pgpu_sim* sim, int32_t* parity) {
   });
 }
 
-int pgpu_step_part(pgpu_sim* sim, int32_t part) {
+int pgpu_step_part_on(pgpu_sim* sim, int32_t part, void* stream) {
   return guard([&] {
     SIM_CHECK();
     if (!sim->slab) throw ConfigError("split steps need a slab geometry");
     if (!sim->send_lo) throw ConfigError("halo buffers not set");
+    // the part's kernels go to `stream` (null: the simulation's stream)
+    const cudaStream_t keep = sim->stream;
+    if (stream) sim->stream = static_cast<cudaStream_t>(stream);
+    struct Restore {
+      pgpu_sim* s;
+      cudaStream_t st;
+      ~Restore() { s->stream = st; }
+    } restore{sim, keep};
     if (part == 0) {
       if (sim->pending) throw ConfigError("previous split step not finished");
       if (!sim->post) {
@@ -1108,6 +1116,8 @@ int pgpu_step_part(pgpu_sim* sim, int32_t part) {
     }
   });
 }
+
+int pgpu_step_part(pgpu_sim* sim, int32_t part) { return pgpu_step_part_on(sim, part, nullptr); }
 
 int pgpu_step_finish(pgpu_sim* sim) {
   return guard([&] {

@@ -9,14 +9,17 @@ link's second fluid cell x_f1 - e_k lies in the ghost column only for those
 same directions.  So each face carries exactly 5 PDFs per (y, z): the
 paper's communication-reducing ghost-layer exchange.
 
-Per step and rank (DistTransport):
-  1. step_part(0): edge columns x=0 and x=nx-1 are pulled/collided first and
-     their 5 outgoing PDFs written to the send buffers;
-  2. the exchange is enqueued (NCCL send/recv through torch.distributed on the
-     same stream order) into the neighbours' ghost buffers of the next parity;
-  3. step_part(1): the interior columns run on the compute stream while the
-     exchange is in flight;
-  4. step_finish(): buffer swap, parity flip.
+Per step and rank (DistTransport), on two CUDA streams:
+  1. edge stream: step_part(0) pulls/collides the edge columns x=0 and
+     x=nx-1 and writes their 5 outgoing PDFs to the send buffers, then the
+     exchange (NCCL send/recv through torch.distributed) fills the
+     neighbours' ghost buffers of the next parity;
+  2. compute stream: step_part(1), the interior columns, concurrently;
+  3. step_finish(): buffer swap, parity flip.
+Interior cells never read ghosts, so the only cross-stream orderings are the
+column dependencies between consecutive steps: the edge part of step n+1
+waits for the interior of step n (and for the exchange of step n, in stream
+order), the interior of step n+1 waits for the edge part of step n.
 The exchange is the only data-path collective; observables combine per-rank
 partial sums with all_reduce.  LocalTransport runs all slabs in one process on
 one device (sequentially, no kernel ever waits on another), which is how the
@@ -103,28 +106,60 @@ class DistTransport:
         self.right = (rank.rank + 1) % rank.world
 
     def step(self, n: int = 1) -> None:
-        with _on(self.me.stream):
-            self._step(n)
+        if self.me.stream is None:  # CPU engine: one ordered sequence
+            self._step_serial(n)
+            return
+        self._step_two_streams(n)
 
-    def _step(self, n: int) -> None:
+    def _exchange(self):
         me, dist = self.me, self.dist
+        p = me.sim.halo_parity
+        if me.world == 1:
+            me.recv_hi[p].copy_(me.send_lo)
+            me.recv_lo[p].copy_(me.send_hi)
+            return []
+        ops = [dist.P2POp(dist.isend, me.send_lo, self.left, self.group, tag=0),
+               dist.P2POp(dist.isend, me.send_hi, self.right, self.group, tag=1),
+               dist.P2POp(dist.irecv, me.recv_hi[p], self.right, self.group, tag=0),
+               dist.P2POp(dist.irecv, me.recv_lo[p], self.left, self.group, tag=1)]
+        return dist.batch_isend_irecv(ops)
+
+    def _step_serial(self, n: int) -> None:
+        me = self.me
         for _ in range(int(n)):
             me.sim.step_part(0)  # edge columns -> send buffers
-            p = me.sim.halo_parity
-            reqs = []
-            if me.world == 1:
-                me.recv_hi[p].copy_(me.send_lo)
-                me.recv_lo[p].copy_(me.send_hi)
-            else:
-                ops = [dist.P2POp(dist.isend, me.send_lo, self.left, self.group, tag=0),
-                       dist.P2POp(dist.isend, me.send_hi, self.right, self.group, tag=1),
-                       dist.P2POp(dist.irecv, me.recv_hi[p], self.right, self.group, tag=0),
-                       dist.P2POp(dist.irecv, me.recv_lo[p], self.left, self.group, tag=1)]
-                reqs = dist.batch_isend_irecv(ops)
-            me.sim.step_part(1)  # interior columns overlap the exchange
+            reqs = self._exchange()
+            me.sim.step_part(1)  # interior columns
             me.sim.step_finish()
             for req in reqs:  # the next step's edge part reads the new ghosts
                 req.wait()
+
+    def _step_two_streams(self, n: int) -> None:
+        import torch
+
+        me = self.me
+        main = me.stream
+        if getattr(self, "_edge_stream", None) is None:
+            self._edge_stream = torch.cuda.Stream(device=main.device)
+        edge = self._edge_stream
+        edge.wait_stream(main)  # everything issued before step() on the main stream
+        prev_edge = None
+        for _ in range(int(n)):
+            ev_main = torch.cuda.Event()
+            ev_main.record(main)  # interior of the previous step
+            with torch.cuda.stream(edge):
+                edge.wait_event(ev_main)
+                me.sim.step_part(0, edge.cuda_stream)  # edge columns -> send buffers
+                ev_edge = torch.cuda.Event()
+                ev_edge.record(edge)
+                for req in self._exchange():  # in edge-stream order
+                    req.wait()
+            if prev_edge is not None:  # the interior reads/overwrites the previous
+                main.wait_event(prev_edge)  # step's edge columns
+            me.sim.step_part(1, main.cuda_stream)  # interior, concurrent with edge + exchange
+            me.sim.step_finish()
+            prev_edge = ev_edge
+        main.wait_stream(edge)  # step() returns with all work ordered on the main stream
 
     # -- collective observables ---------------------------------------------
     def _allreduce(self, values, op="sum"):

@@ -631,8 +631,13 @@ class Simulation:
         _check(lib.pgpu_halo_parity(self._h, C.byref(v)))
         return v.value
 
-    def step_part(self, part: int) -> None:
-        _check(lib.pgpu_step_part(self._h, int(part)))
+    def step_part(self, part: int, stream_handle: Optional[int] = None) -> None:
+        """Split step (slab mode); `stream_handle` (cudaStream_t as int) puts
+        this part's kernels on another stream without re-binding the sim."""
+        if stream_handle is None:
+            _check(lib.pgpu_step_part(self._h, int(part)))
+        else:
+            _check(lib.pgpu_step_part_on(self._h, int(part), C.c_void_p(int(stream_handle))))
 
     def step_finish(self) -> None:
         _check(lib.pgpu_step_finish(self._h))

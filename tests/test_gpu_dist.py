@@ -63,3 +63,25 @@ def test_slabs_glbm(gpu):
     sim.step(17)
     fl = g.flags.reshape(w.dims[::-1]) == 0
     assert np.array_equal(lt.gather_pdfs()[:, fl], sim.get_pdfs()[:, fl])
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_dist_transport_two_streams_single_rank(gpu, scheme):
+    """DistTransport's two-stream schedule (edge part + exchange on one stream,
+    interior on another, cross-step events only) at world size 1, where the
+    exchange is the periodic self-copy: bit-identical to the single domain,
+    also when observables and more steps interleave."""
+    pg = gpu
+    from paper_1507_06565_b200 import configs
+    from paper_1507_06565_b200.dist import SlabSimulation
+    w = bed_workload(pg, scheme)
+    ss = SlabSimulation(w, 0, 1, device=0)
+    g = w.geometry()
+    sim = configs.make_simulation(w, g)
+    fl = g.flags.reshape(w.dims[::-1]) == 0
+    for n in (1, 9, 13):
+        ss.step(n)
+        sim.step(n)
+        got = ss.sim.get_pdfs()
+        assert np.array_equal(got[:, fl], sim.get_pdfs()[:, fl]), n
+    assert ss.max_speed() == sim.max_speed()
