@@ -45,6 +45,17 @@ __device__ __forceinline__ constexpr double pair_w(int p) { return p < 3 ? 1.0 /
 enum SweepOp { OP_STREAM_COLLIDE = 0, OP_STREAM_ONLY = 1 };
 enum SweepPart { PART_ALL = 0, PART_EDGES = 1, PART_INTERIOR = 2 };
 
+// x-slab split: the edge part sweeps one warp-aligned band of columns at each
+// x face (x < w or x >= nx - w; it alone reads ghosts and fills the send
+// buffers), the interior part the rest.  Bands of 32 keep the edge rows
+// coalesced, so the edge part streams like the interior instead of touching
+// one 8-byte slot per DRAM line.
+__host__ __device__ __forceinline__ int edge_band(int nx) { return nx < 64 ? (nx + 1) / 2 : 32; }
+__device__ __forceinline__ bool in_edge_band(int x, int nx) {
+  const int w = edge_band(nx);
+  return x < w || x >= nx - w;
+}
+
 // ---------------------------------------------------------------------------
 // Collision: simulation.cpp:150-196 (core) and :198-274 (GLBM), literal order.
 // ---------------------------------------------------------------------------
@@ -337,7 +348,7 @@ __global__ void __launch_bounds__(128, PGPU_SWEEP_MINB) k_sweep(const KParams p,
   const int y = blockIdx.y;
   const int z0 = blockIdx.z * kZPer;
   if (x >= p.nx) return;
-  if (part == PART_INTERIOR && (x == 0 || x == p.nx - 1)) return;
+  if (part == PART_INTERIOR && in_edge_band(x, p.nx)) return;
   const int z1 = min(z0 + kZPer, p.nz);
   CellWord next = ld_cw(p, ((int64_t)z0 * p.ny + y) * p.nx + x);
   for (int z = z0; z < z1; ++z) {
@@ -516,7 +527,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   // valid: a cell of the row (its links stay in the warp's link list so record
   // indices follow from the chunk base); active: the cell is swept by this part.
   const bool valid = x < p.nx;
-  const bool active = valid && !(part == PART_INTERIOR && (x == 0 || x == p.nx - 1));
+  const bool active = valid && !(part == PART_INTERIOR && in_edge_band(x, p.nx));
   const int xx = valid ? x : 0;
   double* const main0 = smem + tx;
   constexpr int kMainStride = 19 * kPipeBX;
@@ -699,14 +710,14 @@ template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(128) k_sweep_edges(const KParams p,
                                                      const double* __restrict__ src,
                                                      double* __restrict__ dst) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t hp = (int64_t)p.ny * p.nz;
-  if (t >= 2 * hp) return;
-  const int side = (int)(t / hp);
-  const int64_t h = t - side * hp;
-  const int z = (int)(h / p.ny), y = (int)(h - (int64_t)z * p.ny);
-  const int x = side ? p.nx - 1 : 0;
-  if (side == 1 && p.nx == 1) return;
+  // grid (2 faces, ceil(ny/4), nz); each warp one row's band
+  const int w = edge_band(p.nx);
+  const int xx = threadIdx.x & 31;
+  const int y = blockIdx.y * 4 + (threadIdx.x >> 5);
+  const int z = blockIdx.z;
+  if (xx >= w || y >= p.ny) return;
+  const int x = blockIdx.x ? p.nx - w + xx : xx;
+  if (blockIdx.x && x < w) return;  // the bands overlap when nx < 2w
   const CellWord cw = ld_cw(p, ((int64_t)z * p.ny + y) * p.nx + x);
   sweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z, cw);
 }
@@ -904,9 +915,8 @@ template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
 void launch_sweep_t(const KParams& p, const double* src, double* dst, int part,
                     cudaStream_t s) {
   if (part == PART_EDGES) {
-    const int64_t n = 2 * (int64_t)p.ny * p.nz;
     k_sweep_edges<RHO1, GLBM, RECORDS, SLAB, OP>
-        <<<(unsigned)((n + kBX - 1) / kBX), kBX, 0, s>>>(p, src, dst);
+        <<<dim3(2, (p.ny + 3) / 4, p.nz), 128, 0, s>>>(p, src, dst);
   } else if (g_sweep_mode <= 1) {
     const int zper = pipe_zper(p);
     const dim3 grid((p.nx + kPipeBX - 1) / kPipeBX, p.ny, (p.nz + zper - 1) / zper);
