@@ -369,6 +369,9 @@ __host__ __device__ constexpr int pipe_minb(bool records) { return records ? 5 :
 #ifndef PGPU_POOL
 #define PGPU_POOL 192
 #endif
+#ifndef PGPU_CW_EARLY
+#define PGPU_CW_EARLY 0
+#endif
 constexpr int kPool = PGPU_POOL;  // per-warp, per-stage slots for CLI / moving-wall extras
 constexpr int kLinkCap = kPool / 2;  // link entries per warp and stage (2 pool slots each)
 // per stage: 19 population slots per thread + per warp (pool + descriptors)
@@ -635,8 +638,12 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     if (kStages == 1) {  // stage consumed: refill it with plane z+1
       if (z + 1 < z_end()) off_next = issue(z + 1, 0, cw_next);
       cp_async_commit();
-      cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
+      // plane z+2's word: loaded after the collision so it does not occupy
+      // registers across it (at 96 registers it would be spilled right after
+      // its load, which exposes the load latency)
+      if (PGPU_CW_EARLY) cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
     }
+    bool got_nn = false;
     if (w & kFillSector) {
       double* const dc = dst + c;
 #pragma unroll
@@ -647,6 +654,10 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
           collide_glbm<RHO1>(f, p, z);
         else
           collide_core<RHO1>(f, p);
+      }
+      if (kStages == 1 && !PGPU_CW_EARLY) {
+        cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
+        got_nn = true;
       }
       double* const dc = dst + c;
 #pragma unroll
@@ -670,6 +681,8 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
         }
       }
     }
+    if (kStages == 1 && !PGPU_CW_EARLY && !got_nn)
+      cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
     cw_cur = cw_next;
     cw_next = cw_nn;
     off_cur = off_next;
