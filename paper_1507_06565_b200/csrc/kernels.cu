@@ -372,6 +372,9 @@ __host__ __device__ constexpr int pipe_minb(bool records) { return records ? 5 :
 #ifndef PGPU_CW_EARLY
 #define PGPU_CW_EARLY 0
 #endif
+#ifndef PGPU_CW_LATE2
+#define PGPU_CW_LATE2 0
+#endif
 constexpr int kPool = PGPU_POOL;  // per-warp, per-stage slots for CLI / moving-wall extras
 constexpr int kLinkCap = kPool / 2;  // link entries per warp and stage (2 pool slots each)
 // per stage: 19 population slots per thread + per warp (pool + descriptors)
@@ -583,6 +586,10 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   // plane z+1 is issued before waiting for plane z; with one stage plane z is
   // first moved to registers and the stage refilled with plane z+1.  issue()
   // runs at a convergence point (it contains a warp scan).
+  // The word of plane z+2 is loaded after plane z's collision where the
+  // collision's register demand would otherwise spill it right after its load
+  // (one-stage sweeps at 96 registers, GLBM sweeps); measured per variant.
+  constexpr bool kLateW = kStages == 1 ? !PGPU_CW_EARLY : (GLBM || PGPU_CW_LATE2);
   CellWord cw_cur = kSkip;
   CellWord cw_next = valid ? ld_w(z0) : kSkip;
   int off_cur = 0;
@@ -593,7 +600,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     if (kStages == 2) {
       if (z + 1 < z_end()) off_next = issue(z + 1, s ^ 1, cw_next);
       cp_async_commit();
-      cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
+      if (!kLateW) cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
       cp_async_wait<1>();  // this thread's copies for plane z have landed
     } else {
       cp_async_wait<0>();  // plane z landed (the only group in flight)
@@ -655,7 +662,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
         else
           collide_core<RHO1>(f, p);
       }
-      if (kStages == 1 && !PGPU_CW_EARLY) {
+      if (kLateW) {
         cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
         got_nn = true;
       }
@@ -681,7 +688,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
         }
       }
     }
-    if (kStages == 1 && !PGPU_CW_EARLY && !got_nn)
+    if (kLateW && !got_nn)
       cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
     cw_cur = cw_next;
     cw_next = cw_nn;

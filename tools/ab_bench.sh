@@ -5,8 +5,9 @@ cfgs=$1; shift
 for cfg in $cfgs; do
   for v in product "$@"; do
     if [ $v = product ]; then unset PGPU_LIB; else export PGPU_LIB=paper_1507_06565_b200/_variants/$v/libporolb_cuda.so; fi
-    for rep in 1 2; do
-      r=$(python bench.py --config $cfg --steps 200 --warmup 10 --no-cpu-baseline --no-e2e 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"]), round(d["roofline"]["frac"],3))')
+    for rep in 1 2 3; do
+      st=200; [ $cfg != C4 ] && st=2000
+      r=$(python bench.py --config $cfg --steps $st --warmup 20 --no-cpu-baseline --no-e2e 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"]), round(d["roofline"]["frac"],3))')
       echo "$cfg $v $r"
     done
   done
