@@ -550,6 +550,12 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
                     RECORDS ? __ldg(p.chunkbase + ((int64_t)z * p.ny + y) * p.nchunk + chunk)
                             : 0};
   };
+  // word of plane z+2: two-stage sweeps load it unconditionally (clamped
+  // plane; masked where used), one-stage sweeps select (measured per variant)
+  auto next_w = [&](int z2) {
+    if (pipe_stages(RECORDS) == 2) return ld_w(min(z2, p.nz - 1));
+    return (valid && z2 < min((v_ctaid_z() + 1) * zper, p.nz)) ? ld_w(z2) : CellWord{kNonFluid, 0};
+  };
 
   // issue plane z into stage s; returns the warp's link count for plane z.
   // z-plane range end and the wrap-free predicate are recomputed where used
@@ -590,17 +596,19 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   // collision's register demand would otherwise spill it right after its load
   // (one-stage sweeps at 96 registers, GLBM sweeps); measured per variant.
   constexpr bool kLateW = kStages == 1 ? !PGPU_CW_EARLY : (GLBM || PGPU_CW_LATE2);
+  // Words are loaded unconditionally (clamped plane, x = 0 for lanes past the
+  // row) and masked where used, so no select waits on a load in flight.
   CellWord cw_cur = kSkip;
-  CellWord cw_next = valid ? ld_w(z0) : kSkip;
+  CellWord cw_next = ld_w(z0);
   int off_cur = 0;
   int s = kStages == 2 ? 1 : 0;
   for (int z = z0 - 1; z < z_end(); ++z) {
     int off_next = 0;
     CellWord cw_nn = kSkip;
     if (kStages == 2) {
-      if (z + 1 < z_end()) off_next = issue(z + 1, s ^ 1, cw_next);
+      if (z + 1 < z_end()) off_next = issue(z + 1, s ^ 1, valid ? cw_next : kSkip);
       cp_async_commit();
-      if (!kLateW) cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
+      if (!kLateW) cw_nn = next_w(z + 2);
       cp_async_wait<1>();  // this thread's copies for plane z have landed
     } else {
       cp_async_wait<0>();  // plane z landed (the only group in flight)
@@ -622,7 +630,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
       if (off_cur > kLinkCap) {  // warp-uniform: the pool overflowed for plane z
         // each lane closes its own entries past the cap with direct loads
         int tot;
-        const bool lf = !(cw_cur.w & kNonFluid);  // same counting as issue()
+        const bool lf = valid && !(cw_cur.w & kNonFluid);  // same counting as issue()
         const int off = warp_excl_scan(lf ? __popc(cw_cur.w & kBounceMask) : 0, lane, &tot);
         uint32_t m = fluid ? (w & kBounceMask) : 0u;
         int i = 0;
@@ -643,12 +651,12 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
       for (int j = 0; j < 19; ++j) f[j] = st[j * kPipeBX];
     }
     if (kStages == 1) {  // stage consumed: refill it with plane z+1
-      if (z + 1 < z_end()) off_next = issue(z + 1, 0, cw_next);
+      if (z + 1 < z_end()) off_next = issue(z + 1, 0, valid ? cw_next : kSkip);
       cp_async_commit();
       // plane z+2's word: loaded after the collision so it does not occupy
       // registers across it (at 96 registers it would be spilled right after
       // its load, which exposes the load latency)
-      if (PGPU_CW_EARLY) cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
+      if (PGPU_CW_EARLY) cw_nn = next_w(z + 2);
     }
     bool got_nn = false;
     if (w & kFillSector) {
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
           collide_core<RHO1>(f, p);
       }
       if (kLateW) {
-        cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
+        cw_nn = next_w(z + 2);
         got_nn = true;
       }
       double* const dc = dst + c;
@@ -689,7 +697,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
       }
     }
     if (kLateW && !got_nn)
-      cw_nn = (valid && z + 2 < z_end()) ? ld_w(z + 2) : kSkip;
+      cw_nn = next_w(z + 2);
     cw_cur = cw_next;
     cw_next = cw_nn;
     off_cur = off_next;
