@@ -70,7 +70,7 @@ def build_product(force: bool = False, defines: tuple = (), lib: Path = LIB,
         objs.append(o)
         if force or _stale(o, [CSRC / src] + hdrs):
             jobs.append([CXX, "-std=c++17", "-O3", "-fPIC", "-pthread", "-ffp-contract=off",
-                         "-Wall", "-Wno-unused-function", f"-I{CUDA_INC}", "-c",
+                         "-Wall", "-Wno-unused-function", f"-I{CUDA_INC}", *dflags, "-c",
                          str(CSRC / src), "-o", str(o)])
     if jobs:
         with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
