@@ -251,12 +251,17 @@ def run_ours(args):
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_per_launch}
 
-    # e2e through the C ABI with host buffers (N=1; other ranks mirror it)
+    # e2e through the public API with host buffers
     e2e = None
     if world == 1 and not args.no_e2e and not args.force_slab:
         del sim
         torch.cuda.empty_cache()
         e2e = e2e_run(pg, configs, w, geom, args.steps, local)
+    elif (world > 1 or args.force_slab) and not args.no_e2e:
+        slab_geom = sim_obj.me.geometry
+        del sim, sim_obj, stepper
+        torch.cuda.empty_cache()
+        e2e = e2e_run_dist(w, slab_geom, args.steps, rank, world, local, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.force_slab:
@@ -321,6 +326,45 @@ def e2e_run(pg, configs, w, geom, steps, device):
             "profile_s": t1 - td,
             "what": "pgpu_create from host geometry + K steps + pgpu_get_pdfs (pinned) + "
                     "pgpu_planar_profile"}
+
+
+def e2e_run_dist(w, geom, steps, rank, world, device, dist):
+    """N > 1: every rank creates its slab from its host slab geometry, steps
+    through DistTransport (NCCL halo), downloads its f(N) into pinned memory
+    and joins the global profile; time = max over ranks."""
+    import torch
+
+    from paper_1507_06565_b200.dist import SlabSimulation
+
+    cells = geom.cells
+    pdf_host = torch.empty(19 * cells, dtype=torch.float64, pin_memory=True).numpy()
+    h2d = (geom.flags.nbytes + geom.n_links * (8 + 8 + 4 + 4 + 1) + geom.porosity.nbytes
+           + 2 * geom.ghost_flags_lo.nbytes)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    ss = SlabSimulation(w, rank, world, device=device, geometry=geom)
+    tc = time.perf_counter()
+    ss.step(steps)
+    ss.sim.get_pdfs(pdf_host.reshape(19, *geom.dims[::-1]))
+    td = time.perf_counter()
+    prof = ss.planar_profile()
+    t1 = time.perf_counter()
+    loc = torch.tensor([t1 - t0, tc - t0, td - tc, t1 - td], dtype=torch.float64, device="cuda")
+    fl = torch.tensor([float(ss.sim.fluid_cells)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(loc, op=dist.ReduceOp.MAX)
+        dist.all_reduce(fl)
+    tt, tcr, tst, tpr = (float(v) for v in loc.cpu())
+    d2h = pdf_host.nbytes + 5 * prof.z.nbytes
+    del ss
+    torch.cuda.empty_cache()
+    return {"value": float(fl.item()) * steps / tt / 1e6, "unit": "MLUPS",
+            "h2d_bytes_per_step": world * h2d / steps, "d2h_bytes_per_step": world * d2h / steps,
+            "seconds": tt, "create_s": tcr, "steps_and_pdf_download_s": tst, "profile_s": tpr,
+            "what": "per rank: pgpu_create from its host slab geometry + K steps with the NCCL "
+                    "halo + pgpu_get_pdfs (pinned) + global planar profile; max over ranks"}
 
 
 def main():

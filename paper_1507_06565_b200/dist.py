@@ -63,14 +63,14 @@ class SlabRank:
     send/receive halo buffers (torch tensors on the engine's device)."""
 
     def __init__(self, workload, rank: int, world: int, device=0, engine: Optional[Callable] = None,
-                 stream=None):
+                 stream=None, geometry=None):
         import torch
 
         self.rank, self.world = rank, world
         self.stream = None
         self.workload = workload
         self.x0, self.x1 = slab_ranges(workload.dims[0], world)[rank]
-        self.geometry = workload.geometry_slab(self.x0, self.x1)
+        self.geometry = geometry if geometry is not None else workload.geometry_slab(self.x0, self.x1)
         if engine is None:
             self.sim = P.Simulation.from_params(self.geometry, workload.params(), workload.scheme,
                                                 int(device))
@@ -211,8 +211,9 @@ class DistTransport:
 class SlabSimulation(DistTransport):
     """The rank-local handle bench.py uses: SlabSimulation(workload, rank, world)."""
 
-    def __init__(self, workload, rank: int, world: int, device=0, group=None, engine=None):
-        super().__init__(SlabRank(workload, rank, world, device, engine), group)
+    def __init__(self, workload, rank: int, world: int, device=0, group=None, engine=None,
+                 geometry=None):
+        super().__init__(SlabRank(workload, rank, world, device, engine, geometry=geometry), group)
         self.sim = self.me.sim
 
     def set_stream(self, stream) -> None:
