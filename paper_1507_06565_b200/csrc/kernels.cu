@@ -849,20 +849,39 @@ __global__ void k_macro_fields(const KParams p, const double* __restrict__ f, do
   if (uz) uz[c] = u[2];
 }
 
-// Sequential per-plane sum in ascending cell order (simulation.cpp:400-407),
-// one thread per plane so the rounding sequence is the reference's.
-__global__ void k_plane_sums(const uint32_t* __restrict__ cellw,
-                             const double* __restrict__ u, int64_t plane, int nz,
-                             double* sums) {
-  const int z = blockIdx.x * blockDim.x + threadIdx.x;
-  if (z >= nz) return;
+// Sequential per-plane sum in ascending cell order (simulation.cpp:400-407):
+// one block per plane; thread 0 adds the plane's values in cell order (the
+// reference's rounding sequence) from shared-memory tiles that the other
+// warps stream in ahead of it.  Non-fluid cells hold +0.0 (k_macro_fields),
+// and s + (+0.0) == s exactly because a round-to-nearest sum that starts at
+// +0.0 is never -0.0, so adding every cell equals adding the fluid cells.
+constexpr int kSumTile = 2048;
+__global__ void __launch_bounds__(256) k_plane_sums(const double* __restrict__ u, int64_t plane,
+                                                    double* sums) {
+  __shared__ double buf[2][kSumTile];
+  const int z = blockIdx.x;
+  const double* src = u + plane * z;
+  const int64_t ntiles = (plane + kSumTile - 1) / kSumTile;
+  auto load = [&](int64_t t, int first, int stride) {
+    const int64_t base = t * kSumTile;
+    double* b = buf[t & 1];
+    for (int i = first; i < kSumTile; i += stride)
+      b[i] = base + i < plane ? __ldg(src + base + i) : 0.0;
+  };
+  load(0, threadIdx.x, blockDim.x);
+  __syncthreads();
   double s = 0.0;
-  const int64_t c0 = plane * z;
-  for (int64_t i = 0; i < plane; ++i) {
-    if (cellw[c0 + i] & kNonFluid) continue;
-    s = DADD(s, __ldg(u + c0 + i));
+  for (int64_t t = 0; t < ntiles; ++t) {
+    if (threadIdx.x >= 32) {
+      if (t + 1 < ntiles) load(t + 1, threadIdx.x - 32, blockDim.x - 32);
+    } else if (threadIdx.x == 0) {
+      const double* b = buf[t & 1];
+      const int n = (int)min((int64_t)kSumTile, plane - t * kSumTile);
+      for (int i = 0; i < n; ++i) s = DADD(s, b[i]);
+    }
+    __syncthreads();
   }
-  sums[z] = s;
+  if (threadIdx.x == 0) sums[z] = s;
 }
 
 // max |u|^2 and finiteness over fluid cells (simulation.cpp:419-434).
@@ -1069,7 +1088,7 @@ void launch_macro_fields(bool glbm, const KParams& p, const double* f, double* d
 
 void launch_plane_sums(const KParams& p, const double* u, double* sums, cudaStream_t s) {
   const int64_t plane = (int64_t)p.nx * p.ny;
-  k_plane_sums<<<(p.nz + 31) / 32, 32, 0, s>>>(p.cellw, u, plane, p.nz, sums);
+  k_plane_sums<<<p.nz, 256, 0, s>>>(u, plane, sums);
 }
 
 void launch_max_speed2(bool glbm, const KParams& p, const double* f,
