@@ -74,6 +74,12 @@ class ClockSampler:
     def stop(self):
         if not self.proc:
             return None
+        late = False
+        if not self.lines:  # timed region shorter than nvidia-smi's first sample
+            late = True
+            t_end = time.time() + 3.0
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.02)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -96,8 +102,11 @@ class ClockSampler:
                     reasons.add(n)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if late:
+            out["note"] = "timed region shorter than the 100 ms sampling period; sampled after it"
+        return out
 
 
 def dist_env():
