@@ -30,9 +30,9 @@ CUDA_INC = "/usr/local/cuda/include"
 # The image's $CXX (/opt/gcc) lacks libgomp specs; the system g++ is used.
 CXX = shutil.which("g++") or "g++"
 
-CU_SOURCES = ["kernels.cu", "voxelize_device.cu", "setup.cu"]
+CU_SOURCES = ["kernels.cu", "sweep_compact.cu", "voxelize_device.cu", "setup.cu"]
 CPP_SOURCES = ["params.cpp", "voxelize.cpp", "synth.cpp", "sim.cpp", "io.cpp"]
-HEADERS = ["kparams.h", "kernels.h", "host_common.h", "voxel_geometry.h", "setup.h"]
+HEADERS = ["kparams.h", "kernels.h", "lattice.cuh", "host_common.h", "voxel_geometry.h", "setup.h"]
 
 
 def _run(cmd: list[str]) -> None:

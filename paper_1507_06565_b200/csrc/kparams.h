@@ -24,6 +24,15 @@ constexpr uint32_t kNonFluid = 1u;
 constexpr uint32_t kBounceMask = 0x7FFFEu;
 constexpr uint32_t kFillSector = 1u << 19;
 constexpr int kFlagShift = 24;
+// Fluid-only ("compact") PDF layout: the fluid cells are numbered in the
+// reference's linear cell order (z, y, x).  Per 32-cell chunk of a row
+// (row = z*ny + y, chunk = x >> 5): the slot of its first fluid cell and the
+// fluid mask, so slot(x) = rank + popc(mask & ((1 << (x & 31)) - 1)).
+struct alignas(8) ChunkEnt {
+  uint32_t rank;
+  uint32_t mask;
+};
+
 struct alignas(8) CellWord {
   uint32_t w;
   int32_t base;  // first link record of the cell
@@ -53,7 +62,10 @@ struct PlaneCoef {
 struct KParams {
   int32_t nx, ny, nz;
   int32_t px, py, pz;  // periodic flags (x ignored in slab mode)
-  int64_t ks;          // element stride between the 19 direction planes
+  int64_t ks;          // element stride between the 19 direction planes of the sweep buffers
+  int64_t ksd;         // plane stride of the dense (observable) layout, cells rounded to 32
+  const ChunkEnt* ctab;  // compact layout: [rows][nchunk] chunk entries (null: dense layout)
+  int32_t poff[19];      // compact layout: j * ks (19 * ks < 2^31 is checked at creation)
   const uint32_t* cellw;     // per-cell word (kNonFluid / bounce bits / kFillSector)
   const int32_t* cellbase;   // per-cell first link record (per-cell kernels)
   const int32_t* chunkbase;  // first link record of each 32-cell chunk of a row

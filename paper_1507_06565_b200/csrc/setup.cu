@@ -206,6 +206,28 @@ __global__ void k_mark_lid(const uint32_t* __restrict__ cellw, const int32_t* __
   if (hit) atomicOr(any, 1);
 }
 
+// Fluid-only layout: per 32-cell chunk of a row its fluid mask and count (one
+// warp per chunk), then {rank, mask} after an exclusive scan of the counts.
+__global__ void k_chunk_fluid(const uint32_t* __restrict__ cellw, int nx, int64_t nchunks,
+                              int nchunk, uint32_t* __restrict__ mask, int32_t* __restrict__ cnt) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= nchunks) return;  // warp-uniform
+  const int64_t row = gw / nchunk;
+  const int x = (int)(gw - row * nchunk) * 32 + lane;
+  const bool fluid = x < nx && !(cellw[row * nx + x] & kNonFluid);
+  const unsigned m = __ballot_sync(0xffffffffu, fluid);
+  if (lane == 0) {
+    mask[gw] = m;
+    cnt[gw] = __popc(m);
+  }
+}
+__global__ void k_pack_ctab(const uint32_t* __restrict__ mask, const int32_t* __restrict__ rank,
+                            ChunkEnt* __restrict__ out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = ChunkEnt{(uint32_t)rank[i], mask[i]};
+}
+
 __global__ void k_unpack_flags(const uint32_t* __restrict__ cellw, uint8_t* __restrict__ out,
                                int64_t cells) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -274,6 +296,34 @@ void mark_lid_links(const uint32_t* cellw, const int32_t* base, double* recs, in
   const dim3 blk(128), grid((nx + 127) / 128, ny, nz);
   k_mark_lid<<<grid, blk, 0, s>>>(cellw, base, recs, nx, ny, nz, d_any);
   ck(cudaGetLastError(), "k_mark_lid");
+}
+
+int64_t build_ctab(const uint32_t* cellw, int nx, int64_t rows, int nchunk, ChunkEnt* ctab,
+                   cudaStream_t s) {
+  const int64_t n = rows * nchunk;
+  uint32_t* mask = nullptr;
+  int32_t *cnt = nullptr, *rank = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  ck(cudaMalloc(&mask, sizeof(uint32_t) * n), "ctab alloc");
+  ck(cudaMalloc(&cnt, sizeof(int32_t) * n), "ctab alloc");
+  ck(cudaMalloc(&rank, sizeof(int32_t) * n), "ctab alloc");
+  k_chunk_fluid<<<blocks(n * 32, 256), 256, 0, s>>>(cellw, nx, n, nchunk, mask, cnt);
+  ck(cudaGetLastError(), "k_chunk_fluid");
+  ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, rank, n, s), "ctab scan size");
+  ck(cudaMalloc(&tmp, tb), "ctab alloc");
+  ck(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, rank, n, s), "ctab scan");
+  k_pack_ctab<<<blocks(n, 256), 256, 0, s>>>(mask, rank, ctab, n);
+  ck(cudaGetLastError(), "k_pack_ctab");
+  int32_t last[2] = {0, 0};
+  ck(cudaMemcpyAsync(&last[0], rank + n - 1, 4, cudaMemcpyDeviceToHost, s), "ctab total");
+  ck(cudaMemcpyAsync(&last[1], cnt + n - 1, 4, cudaMemcpyDeviceToHost, s), "ctab total");
+  ck(cudaStreamSynchronize(s), "ctab sync");
+  cudaFree(mask);
+  cudaFree(cnt);
+  cudaFree(rank);
+  cudaFree(tmp);
+  return (int64_t)last[0] + last[1];
 }
 
 void unpack_flags(const uint32_t* cellw, uint8_t* out, int64_t cells, cudaStream_t s) {

@@ -5,6 +5,8 @@
 #include <cstddef>
 #include <cstdint>
 
+#include "kparams.h"
+
 namespace pgpu {
 
 // Validation failures of the caller's link list (pgpu_create contract).
@@ -54,6 +56,9 @@ void setup_links(const LinkSetupArgs& a, uint32_t* seen_bits, unsigned long long
 void fill_records_nan(double* recs, int64_t n, cudaStream_t s);
 void mark_lid_links(const uint32_t* cellw, const int32_t* base, double* recs, int nx, int ny,
                     int nz, int* d_any, cudaStream_t s);
+// Fluid-only layout chunk table [rows][nchunk] {rank, mask}; returns the fluid count.
+int64_t build_ctab(const uint32_t* cellw, int nx, int64_t rows, int nchunk, ChunkEnt* ctab,
+                   cudaStream_t s);
 void unpack_flags(const uint32_t* cellw, uint8_t* out, int64_t cells, cudaStream_t s);
 
 }  // namespace pgpu

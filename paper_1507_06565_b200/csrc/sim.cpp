@@ -79,8 +79,16 @@ struct pgpu_sim {
   std::vector<double> eps, K, gwp, gwm;
   double cf = 0.0;
   bool eps_in_eq = true;
-  // device memory
+  // device memory.  Dense layout: f[0]/f[1] hold both the pre-collision and
+  // the post-collision states.  Fluid-only ("compact") layout: f[0]/f[1] are
+  // the post-collision sweep buffers (plane stride kp.ks) and `pre` holds the
+  // pre-collision state in the reference's dense layout (plane stride ks).
   double* f[2] = {nullptr, nullptr};
+  bool compact = false;
+  double* pre = nullptr;
+  ChunkEnt* d_ctab = nullptr;
+  double* d_scratch = nullptr;  // compact layout: observable scratch when f[1-cur] is too small
+  int64_t scratch_n = 0;
   uint32_t* d_cellw = nullptr;
   int32_t* d_cellbase = nullptr;
   int32_t* d_chunkbase = nullptr;
@@ -114,6 +122,9 @@ struct pgpu_sim {
       if (g) cudaGraphExecDestroy(g);
     cudaSetDevice(device);
     for (double* p : f) cudaFree(p);
+    cudaFree(pre);
+    cudaFree(d_ctab);
+    cudaFree(d_scratch);
     cudaFree(d_cellw);
     cudaFree(d_cellbase);
     cudaFree(d_chunkbase);
@@ -245,10 +256,28 @@ struct pgpu_sim {
 
   void check_launch() { CK(cudaGetLastError()); }
 
+  // buffer holding the pre-collision state (valid when !post)
+  double* pre_buf() const { return compact ? pre : f[cur]; }
+  // n doubles of device scratch that do not alias the pre-collision state
+  double* scratch(int64_t n) {
+    if (19 * kp.ks >= n) return f[1 - cur];  // dead in the pre state
+    if (scratch_n < n) {
+      cudaFree(d_scratch);
+      d_scratch = nullptr;
+      scratch_n = 0;
+      CK(cudaMalloc(&d_scratch, sizeof(double) * n));
+      scratch_n = n;
+    }
+    return d_scratch;
+  }
+
   // ---- state transitions -----------------------------------------------------
   void k0() {
     set_ghost_ptrs();
-    launch_collide_inplace(glbm_active, slab, kp, f[cur], stream);
+    if (compact)
+      launch_collide_to_compact(glbm_active, slab, kp, pre, f[cur], stream);
+    else
+      launch_collide_inplace(glbm_active, slab, kp, f[cur], stream);
     check_launch();
     ++launches;
   }
@@ -262,10 +291,10 @@ struct pgpu_sim {
     if (!post) return;
     if (slab && pending) throw ConfigError("observable requested in the middle of a split step");
     set_ghost_ptrs();
-    launch_sweep(sweep_cfg(1, 0), kp, f[cur], f[1 - cur], stream);
+    launch_sweep(sweep_cfg(1, 0), kp, f[cur], compact ? pre : f[1 - cur], stream);
     check_launch();
     ++launches;
-    cur = 1 - cur;
+    if (!compact) cur = 1 - cur;
     post = false;
   }
 
@@ -342,8 +371,8 @@ struct pgpu_sim {
     if (axis < 0 || axis > 2) throw ConfigError("stream axis must be 0, 1 or 2");
     ensure_pre();
     reset_flags();
-    double* u = f[1 - cur];  // dead buffer in the pre state
-    launch_macro_fields(glbm_active, kp, f[cur], nullptr, axis == 0 ? u : nullptr,
+    double* u = scratch(ks);  // dead in the pre state
+    launch_macro_fields(glbm_active, kp, pre_buf(), nullptr, axis == 0 ? u : nullptr,
                         axis == 1 ? u : nullptr, axis == 2 ? u : nullptr, d_flags, stream);
     check_launch();
     launch_plane_sums(kp, u, d_sums, stream);
@@ -399,7 +428,7 @@ struct pgpu_sim {
     ensure_pre();
     reset_flags();
     CK(cudaMemsetAsync(d_vmax, 0, sizeof(unsigned long long), stream));
-    launch_max_speed2(glbm_active, kp, f[cur], d_vmax, d_flags + 1, d_flags, stream);
+    launch_max_speed2(glbm_active, kp, pre_buf(), d_vmax, d_flags + 1, d_flags, stream);
     check_launch();
     ++launches;
     unsigned long long bits = 0;
@@ -423,7 +452,7 @@ struct pgpu_sim {
   void get_cell(int64_t cell, double out[19]) {
     if (cell < 0 || cell >= cells) throw ConfigError("cell index out of range");
     ensure_pre();
-    CK(cudaMemcpy2DAsync(out, sizeof(double), f[cur] + cell, ks * sizeof(double), sizeof(double),
+    CK(cudaMemcpy2DAsync(out, sizeof(double), pre_buf() + cell, ks * sizeof(double), sizeof(double),
                          19, cudaMemcpyDeviceToHost, stream));
     sync();
   }
@@ -668,8 +697,38 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     const char* fill_env = std::getenv("PGPU_FILL_SECTORS");
     device_setup(s.get(), g, !(fill_env && fill_env[0] == '0'), lap);
 
-    // device buffers: two full PDF grids, zero-filled like the reference
-    const size_t fbytes = sizeof(double) * 19 * (size_t)s->ks;
+    {  // two PDF grids well inside the 126 MB L2 -> persistent multi-step sweeps
+      const char* e = std::getenv("PGPU_PERSISTENT");
+      const double state_bytes = 2.0 * 19.0 * 8.0 * (double)s->ks;
+      s->persistent = !s->slab && (e ? e[0] == '1' : state_bytes <= 48e6);
+    }
+    {  // layout: fluid-only unless the domain is L2-resident (persistent sweep);
+       // PGPU_LAYOUT=dense|compact overrides
+      const char* e = std::getenv("PGPU_LAYOUT");
+      s->compact = e ? e[0] == 'c' : !s->persistent;
+      if (s->compact) s->persistent = false;
+    }
+    int64_t sweep_ks = s->ks;
+    if (s->compact) {
+      const int64_t rows = (int64_t)s->ny * s->nz;
+      CK(cudaMalloc(&s->d_ctab, sizeof(ChunkEnt) * rows * s->kp.nchunk));
+      const int64_t nf = build_ctab(s->d_cellw, s->nx, rows, s->kp.nchunk, s->d_ctab, s->stream);
+      sweep_ks = std::max<int64_t>(32, (nf + 31) / 32 * 32);
+      if (19 * sweep_ks >= (int64_t)std::numeric_limits<int32_t>::max()) {
+        // 32-bit slot offsets do not reach: keep the dense layout
+        s->compact = false;
+        CK(cudaFree(s->d_ctab));
+        s->d_ctab = nullptr;
+        sweep_ks = s->ks;
+      }
+    }
+    if (s->compact) {
+      const size_t pbytes = sizeof(double) * 19 * (size_t)s->ks;
+      CK(cudaMalloc(&s->pre, pbytes));
+      CK(cudaMemsetAsync(s->pre, 0, pbytes, s->stream));
+    }
+    // device buffers: two PDF grids, zero-filled like the reference
+    const size_t fbytes = sizeof(double) * 19 * (size_t)sweep_ks;
     for (int b = 0; b < 2; ++b) {
       CK(cudaMalloc(&s->f[b], fbytes));
       CK(cudaMemsetAsync(s->f[b], 0, fbytes, s->stream));
@@ -685,7 +744,10 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     kp.px = s->per[0];
     kp.py = s->per[1];
     kp.pz = s->per[2];
-    kp.ks = s->ks;
+    kp.ks = sweep_ks;
+    kp.ksd = s->ks;
+    kp.ctab = s->d_ctab;
+    for (int j = 0; j < 19; ++j) kp.poff[j] = s->compact ? (int32_t)(j * sweep_ks) : 0;
     for (int j = 0; j < 19; ++j) {
       const int64_t d = kE[j][0] + (int64_t)kE[j][1] * s->nx + (int64_t)kE[j][2] * s->nx * s->ny;
       kp.pull_off[j] = (int64_t)j * s->ks - d;
@@ -696,11 +758,6 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     kp.cellbase = s->d_cellbase;
     kp.chunkbase = s->d_chunkbase;
     lap("alloc pdfs");
-    {  // two PDF grids well inside the 126 MB L2 -> persistent multi-step sweeps
-      const char* e = std::getenv("PGPU_PERSISTENT");
-      const double state_bytes = 2.0 * 19.0 * 8.0 * (double)s->ks;
-      s->persistent = !s->slab && (e ? e[0] == '1' : state_bytes <= 48e6);
-    }
     s->refresh_params();
     CK(cudaStreamSynchronize(s->stream));
     lap("params+sync");
@@ -810,11 +867,11 @@ int pgpu_initialize_equilibrium(pgpu_sim* sim, double delta_rho, const double u[
     double feq[19];
     equilibrium(delta_rho, u, sim->params.rho0, feq);
     if (sim->post) {  // the dead buffer becomes the pre-collision state
-      sim->cur = 1 - sim->cur;
+      if (!sim->compact) sim->cur = 1 - sim->cur;
       sim->post = false;
     }
     CK(cudaMemcpyAsync(sim->d_feq, feq, sizeof(feq), cudaMemcpyHostToDevice, sim->stream));
-    launch_fill_equilibrium(sim->kp, sim->cells, sim->f[sim->cur], sim->d_feq, sim->stream);
+    launch_fill_equilibrium(sim->kp, sim->cells, sim->pre_buf(), sim->d_feq, sim->stream);
     sim->check_launch();
     ++sim->launches;
     sim->sync();
@@ -876,7 +933,7 @@ int pgpu_get_pdfs(pgpu_sim* sim, double* out) {
     SIM_CHECK();
     if (!out) throw std::invalid_argument("null output");
     sim->ensure_pre();
-    CK(cudaMemcpy2DAsync(out, sim->cells * sizeof(double), sim->f[sim->cur],
+    CK(cudaMemcpy2DAsync(out, sim->cells * sizeof(double), sim->pre_buf(),
                          sim->ks * sizeof(double), sim->cells * sizeof(double), 19,
                          cudaMemcpyDeviceToHost, sim->stream));
     sim->sync();
@@ -889,9 +946,9 @@ int pgpu_set_pdfs(pgpu_sim* sim, const double* in) {
     if (!in) throw std::invalid_argument("null input");
     if (sim->slab && sim->pending) throw ConfigError("split step in progress");
     sim->sync();
-    if (sim->post) sim->cur = 1 - sim->cur;
+    if (sim->post && !sim->compact) sim->cur = 1 - sim->cur;
     sim->post = false;
-    CK(cudaMemcpy2DAsync(sim->f[sim->cur], sim->ks * sizeof(double), in,
+    CK(cudaMemcpy2DAsync(sim->pre_buf(), sim->ks * sizeof(double), in,
                          sim->cells * sizeof(double), sim->cells * sizeof(double), 19,
                          cudaMemcpyHostToDevice, sim->stream));
     sim->sync();
@@ -910,7 +967,7 @@ int pgpu_set_cell_populations(pgpu_sim* sim, int64_t cell, const double in[19]) 
     SIM_CHECK();
     if (cell < 0 || cell >= sim->cells) throw ConfigError("cell index out of range");
     sim->ensure_pre();
-    CK(cudaMemcpy2DAsync(sim->f[sim->cur] + cell, sim->ks * sizeof(double), in, sizeof(double),
+    CK(cudaMemcpy2DAsync(sim->pre_buf() + cell, sim->ks * sizeof(double), in, sizeof(double),
                          sizeof(double), 19, cudaMemcpyHostToDevice, sim->stream));
     sim->sync();
   });
@@ -928,11 +985,11 @@ int pgpu_macroscopic_fields(pgpu_sim* sim, double* drho, double* ux, double* uy,
     SIM_CHECK();
     sim->ensure_pre();
     sim->reset_flags();
-    double* scratch = sim->f[1 - sim->cur];
+    double* scratch = sim->scratch(4 * sim->ks);
     double* outs[4] = {drho, ux, uy, uz};
     double* dev[4];
     for (int i = 0; i < 4; ++i) dev[i] = outs[i] ? scratch + (int64_t)i * sim->ks : nullptr;
-    launch_macro_fields(sim->glbm_active, sim->kp, sim->f[sim->cur], dev[0], dev[1], dev[2],
+    launch_macro_fields(sim->glbm_active, sim->kp, sim->pre_buf(), dev[0], dev[1], dev[2],
                         dev[3], sim->d_flags, sim->stream);
     sim->check_launch();
     ++sim->launches;

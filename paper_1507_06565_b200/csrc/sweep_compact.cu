@@ -1,0 +1,687 @@
+// sm_100a sweeps over the fluid-only ("compact") PDF layout.
+//
+// Layout: the fluid cells are numbered in the reference's linear cell order
+// (z, y, x) (field.hpp:19-21 restricted to fluid cells); direction plane j of
+// a sweep buffer holds g_j of fluid cell n at element j*ks + n.  Per 32-cell
+// chunk of a row a ChunkEnt {rank, mask} gives
+//     slot(x) = rank + popc(mask & ((1 << (x & 31)) - 1)).
+// Solid and wall cells occupy no storage, so a sweep moves exactly the 304 B
+// per fluid cell of the algorithm (no 32-byte sectors shared with solid cells,
+// no sector-completion writes).  The observable ("pre-collision") state stays
+// in the reference's dense layout in a separate buffer (plane stride ksd):
+//   K0  k_collide_to_compact : g = C(f)   dense f -> compact g (first step)
+//   K1  k_sweep_cpipe        : g' = C(P(g))  compact -> compact (the hot kernel)
+//   KP  k_sweep_cpipe<KP>    : f = P(g)   compact -> dense (observables)
+// with P the pull form of the reference's push streaming + link bounce-back
+// (simulation.cpp:278-342, boundary.cpp:19-41), exactly as in
+// kernels.cu.
+//
+// K1 keeps the structure of kernels.cu's k_sweep_pipe (per-thread cp.async
+// pipeline, pooled link closures) with fluid-only addressing: one chunk entry
+// per source row and plane gives every pull slot with a popcount (see
+// k_sweep_cpipe).  A TMA variant (one cp.async.bulk per direction run and
+// warp) moved the same bytes but was instruction-bound (3.35 G instructions
+// per C4 launch vs 2.16 G, 7.1 ms); it is kept in tools/experiments/.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+
+#include "kernels.h"
+#include "kparams.h"
+#include "lattice.cuh"
+
+namespace pgpu {
+bool g_plain_sweep();  // kernels.cu: PGPU_SWEEP=plain
+namespace {
+
+// ---------------------------------------------------------------------------
+// Small PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cpa8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cpa4(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// Compact index helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t fidx(const KParams& p, int x, int y, int z) {
+  const ChunkEnt e = p.ctab[((int64_t)z * p.ny + y) * p.nchunk + (x >> 5)];
+  return (int64_t)e.rank + __popc(e.mask & ((1u << (x & 31)) - 1u));
+}
+
+// Directions with e_x = +1 / -1 (their x = 0 / x = nx-1 pulls wrap).
+constexpr uint32_t kExPlus = (1u << 1) | (1u << 7) | (1u << 9) | (1u << 11) | (1u << 13);
+constexpr uint32_t kExMinus = (1u << 2) | (1u << 8) | (1u << 10) | (1u << 12) | (1u << 14);
+
+// Source rows: row r holds the directions with (e_y, e_z) = kRowE[r]; their
+// pull sources lie in row (y - e_y, z - e_z).
+//   r0 (0,0): 0 1 2   r1 (1,0): 3 7 10   r2 (-1,0): 4 8 9   r3 (0,1): 5 11 14
+//   r4 (0,-1): 6 12 13   r5 (1,1): 15   r6 (-1,-1): 16   r7 (1,-1): 17   r8 (-1,1): 18
+__host__ __device__ constexpr int row_ey(int r) {
+  return (r == 1 || r == 5 || r == 7) ? 1 : ((r == 2 || r == 6 || r == 8) ? -1 : 0);
+}
+__host__ __device__ constexpr int row_ez(int r) {
+  return (r == 3 || r == 5 || r == 8) ? 1 : ((r == 4 || r == 6 || r == 7) ? -1 : 0);
+}
+__host__ __device__ constexpr int row_of(int j) {
+  return j <= 2 ? 0
+         : (j == 3 || j == 7 || j == 10) ? 1
+         : (j == 4 || j == 8 || j == 9)  ? 2
+         : (j == 5 || j == 11 || j == 14) ? 3
+         : (j == 6 || j == 12 || j == 13) ? 4
+                                          : j - 10;  // 15..18 -> 5..8
+}
+__host__ __device__ constexpr int row_ndirs(int r) { return r < 5 ? 3 : 1; }
+__host__ __device__ constexpr int row_dir(int r, int i) {
+  return r == 0 ? i
+         : r == 1 ? (i == 0 ? 3 : (i == 1 ? 7 : 10))
+         : r == 2 ? (i == 0 ? 4 : (i == 1 ? 8 : 9))
+         : r == 3 ? (i == 0 ? 5 : (i == 1 ? 11 : 14))
+         : r == 4 ? (i == 0 ? 6 : (i == 1 ? 12 : 13))
+                  : r + 10;
+}
+
+// Periodic wrap of a row coordinate; false if it leaves a non-periodic axis.
+__device__ __forceinline__ bool wrap_coord(int& v, int n, int periodic) {
+  if (v >= 0 && v < n) return true;
+  if (!periodic) return false;
+  v = v < 0 ? v + n : v - n;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Per-cell compact sweep (edge bands of the slab split, PGPU_SWEEP=plain, and
+// the reference point for the pipelined kernel): same arithmetic as kernels.cu's
+// sweep_cell, addresses through the chunk table.
+// ---------------------------------------------------------------------------
+template <int J, bool SLAB>
+__device__ __forceinline__ const double* cpull_addr(const double* __restrict__ src, int x, int y,
+                                                    int z, int64_t fc, const KParams& p,
+                                                    uint32_t w) {
+  constexpr int ex = EX[J], ey = EY[J], ez = EZ[J];
+  if (J == 0) return src + fc;
+  if ((w >> J) & 1u) return src + (int64_t)opp(J) * p.ks + fc;  // bounce: g_k(x)
+  int ys = y - ey, zs = z - ez;
+  if (ey == 1 && y == 0) ys = p.ny - 1;
+  if (ey == -1 && y == p.ny - 1) ys = 0;
+  if (ez == 1 && z == 0) zs = p.nz - 1;
+  if (ez == -1 && z == p.nz - 1) zs = 0;
+  int xs = x - ex;
+  if (ex == 1 && x == 0) {
+    if (SLAB) return p.ghost_lo + (int64_t)halo_slot(J) * p.ny * p.nz + zs * p.ny + ys;
+    xs = p.nx - 1;
+  }
+  if (ex == -1 && x == p.nx - 1) {
+    if (SLAB) return p.ghost_hi + (int64_t)halo_slot(J) * p.ny * p.nz + zs * p.ny + ys;
+    xs = 0;
+  }
+  return src + (int64_t)J * p.ks + fidx(p, xs, ys, zs);
+}
+
+template <int J, bool SLAB>
+__device__ __forceinline__ void cload_all(double (&f)[19], const double* __restrict__ src, int x,
+                                          int y, int z, int64_t fc, const KParams& p,
+                                          uint32_t w) {
+  if constexpr (J < 19) {
+    f[J] = __ldg(cpull_addr<J, SLAB>(src, x, y, z, fc, p, w));
+    cload_all<J + 1, SLAB>(f, src, x, y, z, fc, p, w);
+  }
+}
+
+// CLI / moving-wall closures; f[J] already holds g_k(x) (boundary.cpp:24-41).
+template <int J>
+__device__ __forceinline__ void clinks_all(double (&f)[19], const double* __restrict__ src,
+                                           int64_t fc, const KParams& p, uint32_t w,
+                                           int32_t base) {
+  if constexpr (J < 19) {
+    if ((w >> J) & 1u) {
+      constexpr int K = opp(J);
+      const int32_t r = base + __popc(w & ((1u << J) - 1u) & kBounceMask);
+      const double rec = __ldg(p.links + r);
+      const double gj = __ldg(src + (int64_t)J * p.ks + fc);
+      if (rec == rec) {
+        if (!isinf(rec))
+          f[J] = DADD(DSUB(DMUL(rec, f[K]), DMUL(rec, gj)), f[J]);
+        else
+          f[J] = DSUB(f[J], p.mw[K]);
+      }
+    }
+    clinks_all<J + 1>(f, src, fc, p, w, base);
+  }
+}
+
+template <bool SLAB>
+__device__ __forceinline__ void write_sends(const KParams& p, int x, int y, int z,
+                                            const double (&f)[19]) {
+  if (!SLAB) return;
+  const int64_t hp = (int64_t)p.ny * p.nz;
+  const int64_t h = (int64_t)z * p.ny + y;
+  if (x == 0) {
+    p.send_lo[0 * hp + h] = f[2];
+    p.send_lo[1 * hp + h] = f[8];
+    p.send_lo[2 * hp + h] = f[10];
+    p.send_lo[3 * hp + h] = f[12];
+    p.send_lo[4 * hp + h] = f[14];
+  }
+  if (x == p.nx - 1) {
+    p.send_hi[0 * hp + h] = f[1];
+    p.send_hi[1 * hp + h] = f[7];
+    p.send_hi[2 * hp + h] = f[9];
+    p.send_hi[3 * hp + h] = f[11];
+    p.send_hi[4 * hp + h] = f[13];
+  }
+}
+
+template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+__device__ __forceinline__ void csweep_cell(const KParams& p, const double* __restrict__ src,
+                                            double* __restrict__ dst, int x, int y, int z) {
+  const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
+  const uint32_t w = __ldg(p.cellw + c);
+  if (w & kNonFluid) return;
+  const int64_t fc = fidx(p, x, y, z);
+  double f[19];
+  cload_all<0, SLAB>(f, src, x, y, z, fc, p, w);
+  if (RECORDS && (w & kBounceMask)) clinks_all<1>(f, src, fc, p, w, __ldg(p.cellbase + c));
+  if (OP == OP_STREAM_COLLIDE) {
+    if (GLBM)
+      collide_glbm<RHO1>(f, p, z);
+    else
+      collide_core<RHO1>(f, p);
+#pragma unroll
+    for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + fc, f[j]);
+    write_sends<SLAB>(p, x, y, z, f);
+  } else {  // KP: dense observable buffer
+#pragma unroll
+    for (int j = 0; j < 19; ++j) dst[(int64_t)j * p.ksd + c] = f[j];
+  }
+}
+
+// One thread per cell of the box (part ALL / INTERIOR) ...
+template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+__global__ void __launch_bounds__(128) k_csweep_cells(const KParams p,
+                                                      const double* __restrict__ src,
+                                                      double* __restrict__ dst, int part) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= p.nx) return;
+  if (part == PART_INTERIOR && in_edge_band(x, p.nx)) return;
+  csweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, blockIdx.y, blockIdx.z);
+}
+// ... or of the two x edge bands (slab split; grid (2, ceil(ny/4), nz)).
+template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+__global__ void __launch_bounds__(128) k_csweep_edges(const KParams p,
+                                                      const double* __restrict__ src,
+                                                      double* __restrict__ dst) {
+  const int w = edge_band(p.nx);
+  const int xx = threadIdx.x & 31;
+  const int y = blockIdx.y * 4 + (threadIdx.x >> 5);
+  const int z = blockIdx.z;
+  if (xx >= w || y >= p.ny) return;
+  const int x = blockIdx.x ? p.nx - w + xx : xx;
+  if (blockIdx.x && x < w) return;
+  csweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z);
+}
+
+// K0: dense pre-collision f -> compact post-collision g (simulation.cpp:150-274).
+template <bool RHO1, bool GLBM, bool SLAB>
+__global__ void __launch_bounds__(128) k_collide_to_compact(const KParams p,
+                                                            const double* __restrict__ f0,
+                                                            double* __restrict__ dst) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= p.nx) return;
+  const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
+  if (__ldg(p.cellw + c) & kNonFluid) return;
+  double f[19];
+#pragma unroll
+  for (int j = 0; j < 19; ++j) f[j] = __ldg(f0 + (int64_t)j * p.ksd + c);
+  if (GLBM)
+    collide_glbm<RHO1>(f, p, z);
+  else
+    collide_core<RHO1>(f, p);
+  const int64_t fc = fidx(p, x, y, z);
+#pragma unroll
+  for (int j = 0; j < 19; ++j) dst[(int64_t)j * p.ks + fc] = f[j];
+  write_sends<SLAB>(p, x, y, z, f);
+}
+
+// Warp-exclusive prefix sum of n; the warp total in *total.
+__device__ __forceinline__ int warp_scan_excl(int n, int lane, int* total) {
+  int v = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  *total = __shfl_sync(0xffffffffu, v, 31);
+  return v - n;
+}
+
+// Pull source of direction j for the lane at x = 0 (e_x = +1) or x = nx-1
+// (e_x = -1): the periodic partner cell x = nx-1 / 0 of the source row (its
+// chunk entry `pe`), or the slab ghost column.  The source is fluid.
+template <bool SLAB>
+__device__ __forceinline__ const double* wrap_src(const KParams& p, const double* src,
+                                                  ChunkEnt pe, int j, int x, int y, int z) {
+  int ys = y - EY[j], zs = z - EZ[j];
+  if (ys < 0) ys += p.ny;
+  if (ys >= p.ny) ys -= p.ny;
+  if (zs < 0) zs += p.nz;
+  if (zs >= p.nz) zs -= p.nz;
+  const bool plus = EX[j] == 1;
+  if (SLAB)
+    return (plus ? p.ghost_lo : p.ghost_hi) + (int64_t)halo_slot(j) * p.ny * p.nz +
+           (int64_t)zs * p.ny + ys;
+  const int64_t idx =
+      plus ? (int64_t)pe.rank + __popc(pe.mask & ((1u << ((p.nx - 1) & 31)) - 1u)) : (int64_t)pe.rank;
+  return src + (int64_t)j * p.ks + idx;
+}
+
+// ---------------------------------------------------------------------------
+// K1 / KP: asynchronous-copy pipeline over the compact layout.
+//
+// A block owns a 128-cell x segment of one row (4 warps = 4 chunks) and
+// marches through `zper` z-planes.  While plane z is collided, each thread's
+// 19 loads for plane z+1 are in flight as 8-byte cp.async copies into its own
+// shared-memory slots, and the cell words and chunk entries of plane z+3 are
+// on their way (a 3-slot ring).  The pull source of direction j lies in
+// source row r = row_of(j); with the row's chunk entry {rank, mask},
+//     q_r = rank + popc(mask & lanemask_lt)
+// is the slot of the fluid cell at (or after) this x in that row, and the
+// source slot is q_r (e_x = 0), q_r - 1 (e_x = +1) or q_r + bit(mask, lane)
+// (e_x = -1) -- exact because a pulled source is always fluid.  Bounce
+// directions load g_k(x) from the cell's own slot instead (f_j = g_k(x) for
+// SBB; CLI / moving-wall links are closed from a per-warp pool exactly as in
+// kernels.cu's k_sweep_pipe).  Addresses are 32-bit slot offsets from the
+// buffer base (plane j at p.poff[j]); only lanes on the periodic x faces
+// take the general path (partner chunk / slab ghosts).
+// ---------------------------------------------------------------------------
+constexpr int kCW = 4;            // warps (= chunks) per block
+constexpr int kCBXp = kCW * 32;   // cells per block
+__host__ __device__ constexpr int cp_stages(bool records) { return records ? 1 : 2; }
+__host__ __device__ constexpr int cp_minb(bool records) { return records ? 5 : 4; }
+#ifndef PGPU_CPOOL
+#define PGPU_CPOOL 192
+#endif
+constexpr int kCPool = PGPU_CPOOL;    // per-warp, per-stage extras (record + g_j(x) per link)
+constexpr int kCLinkCap = kCPool / 2;
+
+// Packed row tables (2 bits per row, value + 1).
+constexpr uint32_t pack_rows(int v0, int v1, int v2, int v3, int v4, int v5, int v6, int v7, int v8) {
+  return (uint32_t)(v0 + 1) | (uint32_t)(v1 + 1) << 2 | (uint32_t)(v2 + 1) << 4 |
+         (uint32_t)(v3 + 1) << 6 | (uint32_t)(v4 + 1) << 8 | (uint32_t)(v5 + 1) << 10 |
+         (uint32_t)(v6 + 1) << 12 | (uint32_t)(v7 + 1) << 14 | (uint32_t)(v8 + 1) << 16;
+}
+constexpr uint32_t kRowEYp = pack_rows(row_ey(0), row_ey(1), row_ey(2), row_ey(3), row_ey(4),
+                                       row_ey(5), row_ey(6), row_ey(7), row_ey(8));
+constexpr uint32_t kRowEZp = pack_rows(row_ez(0), row_ez(1), row_ez(2), row_ez(3), row_ez(4),
+                                       row_ez(5), row_ez(6), row_ez(7), row_ez(8));
+__device__ __forceinline__ int rt_row_ey(int r) { return (int)((kRowEYp >> (2 * r)) & 3u) - 1; }
+__device__ __forceinline__ int rt_row_ez(int r) { return (int)((kRowEZp >> (2 * r)) & 3u) - 1; }
+
+struct CLinkDesc {
+  int32_t rec;  // index into p.links
+  int32_t oj;   // owner thread << 8 | j
+};
+struct CLane {
+  uint32_t w;  // cell word of the plane (kNonFluid: the lane skips it)
+  int32_t fc;  // compact slot of the cell
+};
+struct alignas(16) CMeta {  // one plane, loaded two planes ahead of its issue
+  uint32_t cw[kCBXp];
+  ChunkEnt ent[kCW][16];  // per warp: 0..8 source rows, 9..13 x-wrap partners of rows 0..4,
+                          // 14.rank = first link record of the chunk
+};
+template <bool RECORDS>
+struct alignas(16) CSmem {
+  static constexpr int S = cp_stages(RECORDS);
+  static constexpr int PW = RECORDS ? kCPool + kCLinkCap : 1;  // doubles per warp and stage
+  double main[S][19][kCBXp];
+  double pool[S][kCW][PW];
+  CLane lane[S][kCBXp];
+  int32_t cbase[S][kCW];
+  CMeta meta[3];
+};
+
+__device__ __forceinline__ void cpublish_links(CLinkDesc* desc, uint32_t w, int32_t base, int off,
+                                               int tx) {
+  uint32_t m = w & kBounceMask;
+  int i = 0;
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    const int e = off + i;
+    if (e < kCLinkCap) desc[e] = CLinkDesc{base + i, (tx << 8) | j};
+    ++i;
+  }
+}
+
+// Closure of one link in the stage (boundary.cpp:24-41 in pull form): slot j
+// of the owner holds g_k(x), slot k its pull value.
+__device__ __forceinline__ void cclose_link(double* stage, int owner, int j, double rec, double gj,
+                                            const KParams& p) {
+  if (rec == rec) {
+    const int k = (j & 1) ? j + 1 : j - 1;
+    double* sj = stage + j * kCBXp + owner;
+    const double gk = *sj;
+    if (!isinf(rec))
+      *sj = DADD(DSUB(DMUL(rec, stage[k * kCBXp + owner]), DMUL(rec, gj)), gk);
+    else
+      *sj = DSUB(gk, p.mw[k]);
+  }  // NaN: simple bounce-back, slot j already holds g_k(x)
+}
+
+template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+__global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
+    k_sweep_cpipe(const KParams p, const double* __restrict__ src, double* __restrict__ dst,
+                  int part, int zper) {
+  using Sm = CSmem<RECORDS>;
+  constexpr int kS = Sm::S;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Sm& S = *reinterpret_cast<Sm*>(smem_raw);
+  const int tx = threadIdx.x, lane = tx & 31, warp = tx >> 5;
+  const int xc = blockIdx.x * kCW + warp;
+  const int x = xc * 32 + lane;
+  const int y = blockIdx.y;
+  const int z0 = blockIdx.z * zper;
+  const int z1 = min(z0 + zper, p.nz);
+  const bool valid = x < p.nx;
+  const bool active = valid && !(part == PART_INTERIOR && in_edge_band(x, p.nx));
+  const uint32_t ltl = (1u << lane) - 1u;
+  const bool wrapchunk = xc == 0 || xc == p.nchunk - 1;
+
+  auto meta_load = [&](int z, int m) {
+    CMeta& M = S.meta[m];
+    const int64_t row = (int64_t)z * p.ny + y;
+    if (valid)
+      cpa4(&M.cw[tx], p.cellw + row * p.nx + x);
+    else
+      M.cw[tx] = kNonFluid;
+    if (lane < 15 && xc < p.nchunk) {
+      if (lane < 14) {
+        const int r = lane < 9 ? lane : lane - 9;
+        int ys = y - rt_row_ey(r), zs = z - rt_row_ez(r);
+        const bool ok = wrap_coord(ys, p.ny, p.py) & wrap_coord(zs, p.nz, p.pz);
+        if (ok && (lane < 9 || (!SLAB && wrapchunk)))
+          cpa8(&M.ent[warp][lane],
+               p.ctab + ((int64_t)zs * p.ny + ys) * p.nchunk +
+                   (lane < 9 ? xc : (xc == 0 ? p.nchunk - 1 : 0)));
+        else
+          M.ent[warp][lane] = ChunkEnt{0u, 0u};
+      } else if (RECORDS) {
+        cpa4(&M.ent[warp][14].rank, p.chunkbase + row * p.nchunk + xc);
+      }
+    }
+  };
+
+  // issue plane z (meta slot m) into stage s; returns the warp's link count
+  auto issue = [&](int z, int s, int m) -> int {
+    const CMeta& M = S.meta[m];
+    const uint32_t cw = M.cw[tx];
+    const bool fl = !(cw & kNonFluid);
+    const ChunkEnt* E = M.ent[warp];
+    int q[9];
+    uint32_t bits = 0;  // bit r: the source row r has a fluid cell at this x (rows 0..4)
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      const ChunkEnt e = E[r];
+      q[r] = (int)e.rank + __popc(e.mask & ltl);
+      if (r < 5) bits |= ((e.mask >> lane) & 1u) << r;
+    }
+    const int fc = q[0];
+    S.lane[s][tx] = CLane{(fl && active) ? cw : kNonFluid, fc};
+    if (lane == 0 && RECORDS) S.cbase[s][warp] = (int32_t)E[14].rank;
+    if (fl && active) {
+      double* const st = &S.main[s][0][tx];
+      if (!(x == 0 || x == p.nx - 1)) {
+#pragma unroll
+        for (int j = 0; j < 19; ++j) {
+          int idx;
+          if (j == 0) {
+            idx = fc;
+          } else if ((cw >> j) & 1u) {
+            idx = fc + p.poff[opp(j)];  // bounce: g_k(x)
+          } else {
+            const int r = row_of(j);
+            idx = q[r] + p.poff[j];
+            if (EX[j] == 1) idx -= 1;
+            if (EX[j] == -1) idx += (bits >> r) & 1u;
+          }
+          cpa8(st + j * kCBXp, src + (uint32_t)idx);
+        }
+      } else {  // periodic x face / slab edge column: partner chunk or ghost
+#pragma unroll
+        for (int j = 0; j < 19; ++j) {
+          const double* a;
+          if (j == 0) {
+            a = src + (uint32_t)fc;
+          } else if ((cw >> j) & 1u) {
+            a = src + (uint32_t)(fc + p.poff[opp(j)]);
+          } else if ((EX[j] == 1 && x == 0) || (EX[j] == -1 && x == p.nx - 1)) {
+            a = wrap_src<SLAB>(p, src, E[9 + row_of(j)], j, x, y, z);
+          } else {
+            const int r = row_of(j);
+            int idx = q[r] + p.poff[j];
+            if (EX[j] == 1) idx -= 1;
+            if (EX[j] == -1) idx += (bits >> r) & 1u;
+            a = src + (uint32_t)idx;
+          }
+          cpa8(st + j * kCBXp, a);
+        }
+      }
+    }
+    int total = 0;
+    if (RECORDS) {
+      const int n = fl ? __popc(cw & kBounceMask) : 0;  // every cell of the chunk keeps its records
+      const int off = warp_scan_excl(n, lane, &total);
+      if (total) {
+        double* pool = S.pool[s][warp];
+        CLinkDesc* desc = reinterpret_cast<CLinkDesc*>(pool + kCPool);
+        if (n) cpublish_links(desc, cw, (int32_t)E[14].rank + off, off, tx);
+        __syncwarp();
+        const int nl = min(total, kCLinkCap);
+        for (int e = lane; e < nl; e += 32) {
+          const CLinkDesc d = desc[e];
+          const int j = d.oj & 31;
+          cpa8(pool + 2 * e, p.links + d.rec);
+          cpa8(pool + 2 * e + 1, src + (uint32_t)(S.lane[s][d.oj >> 8].fc + p.poff[j]));
+        }
+      }
+    }
+    return total;
+  };
+
+  // prologue: meta of planes z0, z0+1; issue z0; meta of z0+2
+  meta_load(z0, 0);
+  if (z0 + 1 < z1) meta_load(z0 + 1, 1);
+  cpa_commit();
+  cpa_wait_all();
+  __syncwarp();
+  int cnt_cur = issue(z0, 0, 0);
+  __syncwarp();
+  if (z0 + 2 < z1) meta_load(z0 + 2, 2);
+  cpa_commit();
+  int ms = 0;  // meta slot of plane z
+  for (int i = 0, z = z0; z < z1; ++i, ++z) {
+    const int s = kS == 2 ? (i & 1) : 0;
+    const int m1 = ms == 2 ? 0 : ms + 1;
+    int cnt_next = 0;
+    if (kS == 2) {
+      if (z + 1 < z1) {
+        cnt_next = issue(z + 1, s ^ 1, m1);
+        __syncwarp();
+        if (z + 3 < z1) meta_load(z + 3, ms);
+      }
+      cpa_commit();
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // plane z landed (this lane)
+    } else {
+      cpa_wait_all();
+    }
+    __syncwarp();  // ... and every lane's copies
+    const CLane li = S.lane[s][tx];
+    if (RECORDS && cnt_cur) {  // link closures of plane z (one-stage sweeps)
+      double* const stage = &S.main[s][0][0];
+      const double* pool = S.pool[s][warp];
+      const CLinkDesc* desc = reinterpret_cast<const CLinkDesc*>(pool + kCPool);
+      const int ncoop = min(cnt_cur, kCLinkCap);
+      for (int e = lane; e < ncoop; e += 32) {
+        const CLinkDesc d = desc[e];
+        cclose_link(stage, d.oj >> 8, d.oj & 31, pool[2 * e], pool[2 * e + 1], p);
+      }
+      if (cnt_cur > kCLinkCap) {  // warp-uniform: pool overflow, each lane closes the rest itself
+        const uint32_t w = S.meta[ms].cw[tx];  // meta slot of plane z is still intact here
+        const bool lf = valid && !(w & kNonFluid);
+        int tot;
+        const int off = warp_scan_excl(lf ? __popc(w & kBounceMask) : 0, lane, &tot);
+        uint32_t mm = lf ? (w & kBounceMask) : 0u;
+        int k = 0;
+        while (mm) {
+          const int j = __ffs(mm) - 1;
+          mm &= mm - 1;
+          if (off + k >= kCLinkCap)
+            cclose_link(stage, tx, j, __ldg(p.links + S.cbase[s][warp] + off + k),
+                        __ldg(src + (uint32_t)(li.fc + p.poff[j])), p);
+          ++k;
+        }
+      }
+      __syncwarp();
+    }
+    const bool fluid = !(li.w & kNonFluid);
+    double f[19];
+    if (fluid) {
+#pragma unroll
+      for (int j = 0; j < 19; ++j) f[j] = S.main[s][j][tx];
+    }
+    if (kS == 1) {  // stage consumed: refill it with plane z+1
+      __syncwarp();
+      if (z + 1 < z1) {
+        cnt_next = issue(z + 1, 0, m1);
+        __syncwarp();
+        if (z + 3 < z1) meta_load(z + 3, ms);
+      }
+      cpa_commit();
+    }
+    if (fluid) {
+      if (OP == OP_STREAM_COLLIDE) {
+        if (GLBM)
+          collide_glbm<RHO1>(f, p, z);
+        else
+          collide_core<RHO1>(f, p);
+#pragma unroll
+        for (int j = 0; j < 19; ++j) __stcs(dst + (uint32_t)(li.fc + p.poff[j]), f[j]);
+        write_sends<SLAB>(p, x, y, z, f);
+      } else {  // KP into the dense observable buffer
+        double* const d = dst + ((int64_t)z * p.ny + y) * p.nx + x;
+#pragma unroll
+        for (int j = 0; j < 19; ++j) d[(int64_t)j * p.ksd] = f[j];
+      }
+    }
+    cnt_cur = cnt_next;
+    ms = m1;
+  }
+  cpa_wait_all();
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+constexpr int kCBX = 128;
+dim3 ccell_block(const KParams& p) { return dim3(p.nx < kCBX ? ((p.nx + 31) / 32) * 32 : kCBX); }
+dim3 ccell_grid(const KParams& p) {
+  const int bx = ccell_block(p).x;
+  return dim3((p.nx + bx - 1) / bx, p.ny, p.nz);
+}
+
+// z-planes per warp: long marching columns, but >= ~4 waves of blocks over
+// 148 SMs x 4 resident blocks.
+int cpipe_zper(const KParams& p) {
+  if (const char* e = std::getenv("PGPU_ZPER")) return std::max(1, std::min(atoi(e), p.nz));
+  const int64_t cols = (int64_t)((p.nchunk + kCW - 1) / kCW) * p.ny;
+  const int zper = (int)std::min<int64_t>(8, std::max<int64_t>(1, cols * p.nz / (148 * 4 * 4)));
+  return std::min(zper, p.nz);
+}
+
+template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+                      cudaStream_t s) {
+  if (cfg.part == PART_EDGES) {
+    k_csweep_edges<RHO1, GLBM, RECORDS, SLAB, OP>
+        <<<dim3(2, (p.ny + 3) / 4, p.nz), 128, 0, s>>>(p, src, dst);
+  } else if (g_plain_sweep()) {
+    k_csweep_cells<RHO1, GLBM, RECORDS, SLAB, OP><<<ccell_grid(p), ccell_block(p), 0, s>>>(
+        p, src, dst, cfg.part);
+  } else {
+    const int zper = cpipe_zper(p);
+    const dim3 grid((p.nchunk + kCW - 1) / kCW, p.ny, (p.nz + zper - 1) / zper);
+    constexpr int smem = (int)sizeof(CSmem<RECORDS>);
+    static bool attr = [] {
+      cudaFuncSetAttribute(k_sweep_cpipe<RHO1, GLBM, RECORDS, SLAB, OP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      return true;
+    }();
+    (void)attr;
+    k_sweep_cpipe<RHO1, GLBM, RECORDS, SLAB, OP><<<grid, kCBXp, smem, s>>>(p, src, dst, cfg.part,
+                                                                         zper);
+  }
+}
+
+template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB>
+void cdispatch_op(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+                  cudaStream_t s) {
+  if (cfg.op == OP_STREAM_COLLIDE)
+    launch_compact_t<RHO1, GLBM, RECORDS, SLAB, OP_STREAM_COLLIDE>(cfg, p, src, dst, s);
+  else  // KP has no collision: one instantiation per records/slab
+    launch_compact_t<true, false, RECORDS, SLAB, OP_STREAM_ONLY>(cfg, p, src, dst, s);
+}
+template <bool RHO1, bool GLBM>
+void cdispatch(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+               cudaStream_t s) {
+  if (cfg.records) {
+    if (cfg.slab) cdispatch_op<RHO1, GLBM, true, true>(cfg, p, src, dst, s);
+    else cdispatch_op<RHO1, GLBM, true, false>(cfg, p, src, dst, s);
+  } else {
+    if (cfg.slab) cdispatch_op<RHO1, GLBM, false, true>(cfg, p, src, dst, s);
+    else cdispatch_op<RHO1, GLBM, false, false>(cfg, p, src, dst, s);
+  }
+}
+
+}  // namespace
+
+void launch_sweep_compact(const SweepConfig& cfg, const KParams& p, const double* src,
+                          double* dst, cudaStream_t s) {
+  const bool rho1 = p.rho0 == 1.0;
+  if (rho1) {
+    if (cfg.glbm) cdispatch<true, true>(cfg, p, src, dst, s);
+    else cdispatch<true, false>(cfg, p, src, dst, s);
+  } else {
+    if (cfg.glbm) cdispatch<false, true>(cfg, p, src, dst, s);
+    else cdispatch<false, false>(cfg, p, src, dst, s);
+  }
+}
+
+void launch_collide_to_compact(bool glbm, bool slab, const KParams& p, const double* dense,
+                               double* dst, cudaStream_t s) {
+  const dim3 g = ccell_grid(p), b = ccell_block(p);
+  const bool rho1 = p.rho0 == 1.0;
+#define PGPU_K0C(R, G, S) k_collide_to_compact<R, G, S><<<g, b, 0, s>>>(p, dense, dst)
+  if (rho1) {
+    if (glbm) { if (slab) PGPU_K0C(true, true, true); else PGPU_K0C(true, true, false); }
+    else { if (slab) PGPU_K0C(true, false, true); else PGPU_K0C(true, false, false); }
+  } else {
+    if (glbm) { if (slab) PGPU_K0C(false, true, true); else PGPU_K0C(false, true, false); }
+    else { if (slab) PGPU_K0C(false, false, true); else PGPU_K0C(false, false, false); }
+  }
+#undef PGPU_K0C
+}
+
+}  // namespace pgpu

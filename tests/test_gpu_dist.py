@@ -10,6 +10,14 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["dense", "compact"], autouse=True)
+def layout(request, monkeypatch):
+    """Every test here runs on both PDF layouts (PGPU_LAYOUT is read at
+    pgpu_create): the dense reference layout and the fluid-only one."""
+    monkeypatch.setenv("PGPU_LAYOUT", request.param)
+    return request.param
+
+
 def bed_workload(pg, scheme, nx=128, glbm=False):
     from paper_1507_06565_b200 import configs
     rng = np.random.default_rng(5)
