@@ -702,24 +702,29 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
       const double state_bytes = 2.0 * 19.0 * 8.0 * (double)s->ks;
       s->persistent = !s->slab && (e ? e[0] == '1' : state_bytes <= 48e6);
     }
-    {  // layout: fluid-only unless the domain is L2-resident (persistent sweep);
-       // PGPU_LAYOUT=dense|compact overrides
-      const char* e = std::getenv("PGPU_LAYOUT");
-      s->compact = e ? e[0] == 'c' : !s->persistent;
-      if (s->compact) s->persistent = false;
-    }
+    // Layout: fluid-only where it saves traffic -- domains that are not
+    // L2-resident (persistent sweep) and have solid cells inside (< 97 %
+    // fluid; a walled channel keeps the dense layout, whose sweep is the
+    // faster one there).  PGPU_LAYOUT=dense|compact overrides.
     int64_t sweep_ks = s->ks;
-    if (s->compact) {
-      const int64_t rows = (int64_t)s->ny * s->nz;
-      CK(cudaMalloc(&s->d_ctab, sizeof(ChunkEnt) * rows * s->kp.nchunk));
-      const int64_t nf = build_ctab(s->d_cellw, s->nx, rows, s->kp.nchunk, s->d_ctab, s->stream);
-      sweep_ks = std::max<int64_t>(32, (nf + 31) / 32 * 32);
-      if (19 * sweep_ks >= (int64_t)std::numeric_limits<int32_t>::max()) {
-        // 32-bit slot offsets do not reach: keep the dense layout
-        s->compact = false;
-        CK(cudaFree(s->d_ctab));
-        s->d_ctab = nullptr;
-        sweep_ks = s->ks;
+    {
+      const char* e = std::getenv("PGPU_LAYOUT");
+      const bool want = e ? e[0] == 'c' : !s->persistent;
+      if (want) {
+        const int64_t rows = (int64_t)s->ny * s->nz;
+        CK(cudaMalloc(&s->d_ctab, sizeof(ChunkEnt) * rows * s->kp.nchunk));
+        const int64_t nf = build_ctab(s->d_cellw, s->nx, rows, s->kp.nchunk, s->d_ctab, s->stream);
+        const int64_t ksc = std::max<int64_t>(32, (nf + 31) / 32 * 32);
+        // 32-bit slot offsets must reach all 19 planes
+        s->compact = 19 * ksc < (int64_t)std::numeric_limits<int32_t>::max() &&
+                     (e || (double)nf < 0.97 * (double)s->cells);
+        if (s->compact) {
+          sweep_ks = ksc;
+          s->persistent = false;
+        } else {
+          CK(cudaFree(s->d_ctab));
+          s->d_ctab = nullptr;
+        }
       }
     }
     if (s->compact) {

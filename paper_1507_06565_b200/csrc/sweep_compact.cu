@@ -308,8 +308,21 @@ __device__ __forceinline__ const double* wrap_src(const KParams& p, const double
 // ---------------------------------------------------------------------------
 constexpr int kCW = 4;            // warps (= chunks) per block
 constexpr int kCBXp = kCW * 32;   // cells per block
-__host__ __device__ constexpr int cp_stages(bool records) { return records ? 1 : 2; }
-__host__ __device__ constexpr int cp_minb(bool records) { return records ? 5 : 4; }
+#ifndef PGPU_CLI_STAGES
+#define PGPU_CLI_STAGES 1
+#endif
+#ifndef PGPU_CLI_MINB
+#define PGPU_CLI_MINB 4
+#endif
+#ifndef PGPU_SBB_MINB
+#define PGPU_SBB_MINB 4
+#endif
+__host__ __device__ constexpr int cp_stages(bool records) { return records ? PGPU_CLI_STAGES : 2; }
+__host__ __device__ constexpr int cp_minb(bool records) {
+  return records ? PGPU_CLI_MINB : PGPU_SBB_MINB;
+}
+// CLane.w bit of a fluid cell that the launch's part does not sweep
+constexpr uint32_t kInactive = 1u << 20;
 #ifndef PGPU_CPOOL
 #define PGPU_CPOOL 192
 #endif
@@ -334,7 +347,7 @@ struct CLinkDesc {
   int32_t oj;   // owner thread << 8 | j
 };
 struct CLane {
-  uint32_t w;  // cell word of the plane (kNonFluid: the lane skips it)
+  uint32_t w;  // cell word of the plane (| kInactive: a fluid cell this part skips)
   int32_t fc;  // compact slot of the cell
 };
 struct alignas(16) CMeta {  // one plane, loaded two planes ahead of its issue
@@ -439,7 +452,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
       if (r < 5) bits |= ((e.mask >> lane) & 1u) << r;
     }
     const int fc = q[0];
-    S.lane[s][tx] = CLane{(fl && active) ? cw : kNonFluid, fc};
+    S.lane[s][tx] = CLane{active ? cw : (cw | kInactive), fc};
     if (lane == 0 && RECORDS) S.cbase[s][warp] = (int32_t)E[14].rank;
     if (fl && active) {
       double* const st = &S.main[s][0][tx];
@@ -539,8 +552,8 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
         cclose_link(stage, d.oj >> 8, d.oj & 31, pool[2 * e], pool[2 * e + 1], p);
       }
       if (cnt_cur > kCLinkCap) {  // warp-uniform: pool overflow, each lane closes the rest itself
-        const uint32_t w = S.meta[ms].cw[tx];  // meta slot of plane z is still intact here
-        const bool lf = valid && !(w & kNonFluid);
+        const uint32_t w = li.w;
+        const bool lf = !(w & kNonFluid);  // lanes past the row hold kNonFluid
         int tot;
         const int off = warp_scan_excl(lf ? __popc(w & kBounceMask) : 0, lane, &tot);
         uint32_t mm = lf ? (w & kBounceMask) : 0u;
@@ -556,7 +569,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
       }
       __syncwarp();
     }
-    const bool fluid = !(li.w & kNonFluid);
+    const bool fluid = !(li.w & (kNonFluid | kInactive));
     double f[19];
     if (fluid) {
 #pragma unroll
