@@ -321,6 +321,9 @@ __host__ __device__ constexpr int cp_stages(bool records) { return records ? PGP
 __host__ __device__ constexpr int cp_minb(bool records) {
   return records ? PGPU_CLI_MINB : PGPU_SBB_MINB;
 }
+#ifndef PGPU_STCS
+#define PGPU_STCS 1  // streaming (evict-first) stores of the new state
+#endif
 // CLane.w bit of a fluid cell that the launch's part does not sweep
 constexpr uint32_t kInactive = 1u << 20;
 #ifndef PGPU_CPOOL
@@ -403,13 +406,18 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Sm& S = *reinterpret_cast<Sm*>(smem_raw);
   const int tx = threadIdx.x, lane = tx & 31, warp = tx >> 5;
-  const int xc = blockIdx.x * kCW + warp;
+  // warps are independent: a block covers 4 chunks of one row, or (edge part,
+  // x-slab split) the first and last chunk of two rows
+  const bool edges = part == PART_EDGES;
+  const int xc = edges ? ((warp & 1) ? p.nchunk - 1 : 0) : blockIdx.x * kCW + warp;
+  const int y = edges ? blockIdx.y * 2 + (warp >> 1) : blockIdx.y;
   const int x = xc * 32 + lane;
-  const int y = blockIdx.y;
   const int z0 = blockIdx.z * zper;
   const int z1 = min(z0 + zper, p.nz);
-  const bool valid = x < p.nx;
-  const bool active = valid && !(part == PART_INTERIOR && in_edge_band(x, p.nx));
+  const bool wok = xc < p.nchunk && y < p.ny;
+  const bool valid = wok && x < p.nx;
+  const bool active = valid && (part == PART_ALL || (in_edge_band(x, p.nx) == edges));
+  if (!__any_sync(0xffffffffu, active)) return;  // whole warp (no block-level sync below)
   const uint32_t ltl = (1u << lane) - 1u;
   const bool wrapchunk = xc == 0 || xc == p.nchunk - 1;
 
@@ -420,7 +428,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
       cpa4(&M.cw[tx], p.cellw + row * p.nx + x);
     else
       M.cw[tx] = kNonFluid;
-    if (lane < 15 && xc < p.nchunk) {
+    if (lane < 15 && wok) {
       if (lane < 14) {
         const int r = lane < 9 ? lane : lane - 9;
         int ys = y - rt_row_ey(r), zs = z - rt_row_ez(r);
@@ -591,7 +599,12 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
         else
           collide_core<RHO1>(f, p);
 #pragma unroll
-        for (int j = 0; j < 19; ++j) __stcs(dst + (uint32_t)(li.fc + p.poff[j]), f[j]);
+        for (int j = 0; j < 19; ++j) {
+          if (PGPU_STCS)
+            __stcs(dst + (uint32_t)(li.fc + p.poff[j]), f[j]);
+          else
+            dst[(uint32_t)(li.fc + p.poff[j])] = f[j];
+        }
         write_sends<SLAB>(p, x, y, z, f);
       } else {  // KP into the dense observable buffer
         double* const d = dst + ((int64_t)z * p.ny + y) * p.nx + x;
@@ -627,7 +640,9 @@ int cpipe_zper(const KParams& p) {
 template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
 void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
                       cudaStream_t s) {
-  if (cfg.part == PART_EDGES) {
+  // the pipelined kernel sweeps the slab edge bands when each band is one chunk
+  const bool edge_chunks = p.nx % 32 == 0 && p.nx >= 64;
+  if (cfg.part == PART_EDGES && (!edge_chunks || g_plain_sweep())) {
     k_csweep_edges<RHO1, GLBM, RECORDS, SLAB, OP>
         <<<dim3(2, (p.ny + 3) / 4, p.nz), 128, 0, s>>>(p, src, dst);
   } else if (g_plain_sweep()) {
@@ -635,7 +650,9 @@ void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* sr
         p, src, dst, cfg.part);
   } else {
     const int zper = cpipe_zper(p);
-    const dim3 grid((p.nchunk + kCW - 1) / kCW, p.ny, (p.nz + zper - 1) / zper);
+    const dim3 grid = cfg.part == PART_EDGES
+                          ? dim3(1, (p.ny + 1) / 2, (p.nz + zper - 1) / zper)
+                          : dim3((p.nchunk + kCW - 1) / kCW, p.ny, (p.nz + zper - 1) / zper);
     constexpr int smem = (int)sizeof(CSmem<RECORDS>);
     static bool attr = [] {
       cudaFuncSetAttribute(k_sweep_cpipe<RHO1, GLBM, RECORDS, SLAB, OP>,
