@@ -315,7 +315,7 @@ constexpr int kCBXp = kCW * 32;   // cells per block
 #define PGPU_CLI_MINB 4
 #endif
 #ifndef PGPU_SBB_MINB
-#define PGPU_SBB_MINB 4
+#define PGPU_SBB_MINB 3
 #endif
 __host__ __device__ constexpr int cp_stages(bool records) { return records ? PGPU_CLI_STAGES : 2; }
 __host__ __device__ constexpr int cp_minb(bool records) {
