@@ -926,4 +926,17 @@ void launch_fill_equilibrium(const KParams& p, int64_t cells, double* f, const d
                                                                      feq);
 }
 
+// Load the observable kernels' code once per process (CUDA loads modules
+// lazily at first launch, ~10 ms on the first observable otherwise).
+void preload_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_macro_fields<true>);
+  cudaFuncGetAttributes(&a, k_macro_fields<false>);
+  cudaFuncGetAttributes(&a, k_plane_sums);
+  cudaFuncGetAttributes(&a, k_max_speed2<true>);
+  cudaFuncGetAttributes(&a, k_max_speed2<false>);
+  cudaFuncGetAttributes(&a, k_fill_equilibrium);
+  cudaGetLastError();
+}
+
 }  // namespace pgpu

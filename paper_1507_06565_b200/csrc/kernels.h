@@ -37,6 +37,7 @@ void launch_plane_sums(const KParams& p, const double* u, double* sums, cudaStre
 void launch_max_speed2(bool glbm, const KParams& p, const double* f,
                        unsigned long long* vmax2_bits, int* nonfinite, int* err,
                        cudaStream_t s);
+void preload_kernels();
 void launch_fill_equilibrium(const KParams& p, int64_t cells, double* f, const double* feq,
                              cudaStream_t s);
 

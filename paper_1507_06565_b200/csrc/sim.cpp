@@ -21,6 +21,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <vector>
 
@@ -656,6 +657,8 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     std::unique_ptr<pgpu_sim> s(new pgpu_sim());
     s->device = device;
     CK(cudaSetDevice(device));
+    static std::once_flag preload;
+    std::call_once(preload, preload_kernels);
     // L2 fetch granularity hint (bytes): the sweep's loads are 8-byte-per-cell
     // and sector-sparse next to solid cells (experiment knob PGPU_L2_FETCH).
     if (const char* e = std::getenv("PGPU_L2_FETCH")) {
