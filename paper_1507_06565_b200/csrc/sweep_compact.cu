@@ -419,28 +419,39 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
   const bool active = valid && (part == PART_ALL || (in_edge_band(x, p.nx) == edges));
   if (!__any_sync(0xffffffffu, active)) return;  // whole warp (no block-level sync below)
   const uint32_t ltl = (1u << lane) - 1u;
-  const bool wrapchunk = xc == 0 || xc == p.nchunk - 1;
+  // per-lane parts of the meta addresses that do not change along z: the
+  // in-plane offset of this lane's chunk entry (lanes 0..8 source rows,
+  // 9..13 x-wrap partners, 14 the chunk's link base), -1: nothing to load
+  int eoff = -1;
+  if (lane < 15 && wok) {
+    if (lane < 14) {
+      const int r = lane < 9 ? lane : lane - 9;
+      int ys = y - rt_row_ey(r);
+      const bool wrapchunk = xc == 0 || xc == p.nchunk - 1;
+      if (wrap_coord(ys, p.ny, p.py) && (lane < 9 || (!SLAB && wrapchunk)))
+        eoff = ys * p.nchunk + (lane < 9 ? xc : (xc == 0 ? p.nchunk - 1 : 0));
+    } else if (RECORDS) {
+      eoff = y * p.nchunk + xc;
+    }
+  }
 
   auto meta_load = [&](int z, int m) {
     CMeta& M = S.meta[m];
-    const int64_t row = (int64_t)z * p.ny + y;
     if (valid)
-      cpa4(&M.cw[tx], p.cellw + row * p.nx + x);
+      cpa4(&M.cw[tx], p.cellw + ((int64_t)z * p.ny + y) * p.nx + x);
     else
       M.cw[tx] = kNonFluid;
-    if (lane < 15 && wok) {
+    if (lane < 15) {
+      const int64_t plane = (int64_t)p.ny * p.nchunk;
       if (lane < 14) {
-        const int r = lane < 9 ? lane : lane - 9;
-        int ys = y - rt_row_ey(r), zs = z - rt_row_ez(r);
-        const bool ok = wrap_coord(ys, p.ny, p.py) & wrap_coord(zs, p.nz, p.pz);
-        if (ok && (lane < 9 || (!SLAB && wrapchunk)))
-          cpa8(&M.ent[warp][lane],
-               p.ctab + ((int64_t)zs * p.ny + ys) * p.nchunk +
-                   (lane < 9 ? xc : (xc == 0 ? p.nchunk - 1 : 0)));
+        int zs = z - rt_row_ez(lane < 9 ? lane : lane - 9);
+        const bool ok = wrap_coord(zs, p.nz, p.pz) && eoff >= 0;
+        if (ok)
+          cpa8(&M.ent[warp][lane], p.ctab + zs * plane + eoff);
         else
           M.ent[warp][lane] = ChunkEnt{0u, 0u};
-      } else if (RECORDS) {
-        cpa4(&M.ent[warp][14].rank, p.chunkbase + row * p.nchunk + xc);
+      } else if (eoff >= 0) {
+        cpa4(&M.ent[warp][14].rank, p.chunkbase + z * plane + eoff);
       }
     }
   };
