@@ -315,9 +315,14 @@ constexpr int kCBXp = kCW * 32;   // cells per block
 #define PGPU_CLI_MINB 4
 #endif
 #ifndef PGPU_SBB_MINB
-#define PGPU_SBB_MINB 3
+#define PGPU_SBB_MINB 4
 #endif
-__host__ __device__ constexpr int cp_stages(bool records) { return records ? PGPU_CLI_STAGES : 2; }
+#ifndef PGPU_SBB_STAGES
+#define PGPU_SBB_STAGES 1
+#endif
+__host__ __device__ constexpr int cp_stages(bool records) {
+  return records ? PGPU_CLI_STAGES : PGPU_SBB_STAGES;
+}
 __host__ __device__ constexpr int cp_minb(bool records) {
   return records ? PGPU_CLI_MINB : PGPU_SBB_MINB;
 }

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+for v in product sbb1s4 sbb1s3; do
+  if [ $v = product ]; then unset PGPU_LIB; else export PGPU_LIB=paper_1507_06565_b200/_variants/$v/libporolb_cuda.so; fi
+  for rep in 1 2; do python bench.py --scheme SBB --steps 200 --warmup 20 --no-cpu-baseline --no-e2e 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print("C4-SBB '$v'", round(d["value"]), round(d["roofline"]["frac"],3))'; done
+done
