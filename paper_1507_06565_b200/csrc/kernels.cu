@@ -179,8 +179,16 @@ constexpr int kPipeBX = 128;
 // shared-memory stages at 4 blocks/SM; sweeps with link records (CLI /
 // moving walls) use one stage (the landed plane is moved to registers and the
 // stage refilled) at 5 blocks/SM, which leaves L1 room for the pooled extras.
-__host__ __device__ constexpr int pipe_stages(bool records) { return records ? 1 : 2; }
-__host__ __device__ constexpr int pipe_minb(bool records) { return records ? 5 : 4; }
+#ifndef PGPU_DENSE_SBB_STAGES
+#define PGPU_DENSE_SBB_STAGES 2
+#endif
+#ifndef PGPU_DENSE_SBB_MINB
+#define PGPU_DENSE_SBB_MINB 4
+#endif
+__host__ __device__ constexpr int pipe_stages(bool records) {
+  return records ? 1 : PGPU_DENSE_SBB_STAGES;
+}
+__host__ __device__ constexpr int pipe_minb(bool records) { return records ? 5 : PGPU_DENSE_SBB_MINB; }
 #ifndef PGPU_POOL
 #define PGPU_POOL 192
 #endif
