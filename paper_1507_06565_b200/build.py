@@ -32,7 +32,7 @@ CXX = shutil.which("g++") or "g++"
 
 CU_SOURCES = ["kernels.cu", "sweep_compact.cu", "voxelize_device.cu", "setup.cu"]
 CPP_SOURCES = ["params.cpp", "voxelize.cpp", "synth.cpp", "sim.cpp", "io.cpp"]
-HEADERS = ["kparams.h", "kernels.h", "lattice.cuh", "host_common.h", "voxel_geometry.h", "setup.h"]
+HEADERS = ["kparams.h", "kernels.h", "lattice.cuh", "host_common.h", "voxel_geometry.h", "setup.h", "staging.h"]
 
 
 def _run(cmd: list[str]) -> None:

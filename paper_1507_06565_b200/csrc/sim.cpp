@@ -29,6 +29,7 @@
 #include "kernels.h"
 #include "kparams.h"
 #include "setup.h"
+#include "staging.h"
 
 namespace pgpu {
 void moments(const double f[19], double rho0, double& drho, double u[3]);
@@ -494,7 +495,7 @@ template <class T>
 void upload(DevBuf& b, const T* host, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   CK(cudaMalloc(&b.p, sizeof(T) * n));
-  CK(cudaMemcpyAsync(b.p, host, sizeof(T) * n, cudaMemcpyHostToDevice, st));
+  CK(StagedUpload::get().h2d(b.p, host, sizeof(T) * n, st));
 }
 
 const char* setup_error_text(int code) {
