@@ -235,6 +235,7 @@ struct pgpu_sim {
     CK(cudaMalloc(&d_recs, sizeof(LinkRec) * n_links));
     fill_records_nan(d_recs, n_links, stream);
     kp.links = d_recs;
+    kp.nrec = n_links;
     drop_graphs();
   }
 
@@ -613,6 +614,7 @@ void device_setup(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors, Lap&& 
     s->d_recs = nullptr;
   }
   s->kp.links = s->d_recs;
+  s->kp.nrec = s->d_recs ? L : 0;
   lap("link records");
 }
 

@@ -326,6 +326,9 @@ __host__ __device__ constexpr int cp_stages(bool records) {
 __host__ __device__ constexpr int cp_minb(bool records) {
   return records ? PGPU_CLI_MINB : PGPU_SBB_MINB;
 }
+#ifndef PGPU_BOUNDS
+#define PGPU_BOUNDS 0  // debug builds: trap on any out-of-range slot / record / ghost address
+#endif
 #ifndef PGPU_STCS
 #define PGPU_STCS 1  // streaming (evict-first) stores of the new state
 #endif
@@ -349,6 +352,21 @@ constexpr uint32_t kRowEZp = pack_rows(row_ez(0), row_ez(1), row_ez(2), row_ez(3
                                        row_ez(5), row_ez(6), row_ez(7), row_ez(8));
 __device__ __forceinline__ int rt_row_ey(int r) { return (int)((kRowEYp >> (2 * r)) & 3u) - 1; }
 __device__ __forceinline__ int rt_row_ez(int r) { return (int)((kRowEZp >> (2 * r)) & 3u) - 1; }
+
+__device__ __forceinline__ void bounds_ok(bool ok) {
+  if (PGPU_BOUNDS && !ok) __trap();
+}
+// slot `idx` lies in direction plane `plane` of a compact buffer
+__device__ __forceinline__ bool in_plane(const KParams& p, int idx, int plane) {
+  return idx >= p.poff[plane] && (int64_t)idx < (int64_t)p.poff[plane] + p.ks;
+}
+// address lies in a sweep buffer or a ghost column buffer
+__device__ __forceinline__ bool in_src(const KParams& p, const double* src, const double* a) {
+  const int64_t hp = 5 * (int64_t)p.ny * p.nz;
+  return (a >= src && a < src + 19 * p.ks) ||
+         (p.ghost_lo && a >= p.ghost_lo && a < p.ghost_lo + hp) ||
+         (p.ghost_hi && a >= p.ghost_hi && a < p.ghost_hi + hp);
+}
 
 struct CLinkDesc {
   int32_t rec;  // index into p.links
@@ -494,6 +512,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
             if (EX[j] == 1) idx -= 1;
             if (EX[j] == -1) idx += (bits >> r) & 1u;
           }
+          bounds_ok(in_plane(p, idx, ((cw >> j) & 1u) ? opp(j) : j));
           cpa8(st + j * kCBXp, src + (uint32_t)idx);
         }
       } else {  // periodic x face / slab edge column: partner chunk or ghost
@@ -513,6 +532,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
             if (EX[j] == -1) idx += (bits >> r) & 1u;
             a = src + (uint32_t)idx;
           }
+          bounds_ok(in_src(p, src, a));
           cpa8(st + j * kCBXp, a);
         }
       }
@@ -530,6 +550,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
         for (int e = lane; e < nl; e += 32) {
           const CLinkDesc d = desc[e];
           const int j = d.oj & 31;
+          bounds_ok(d.rec >= 0 && d.rec < p.nrec && in_plane(p, S.lane[s][d.oj >> 8].fc + p.poff[j], j));
           cpa8(pool + 2 * e, p.links + d.rec);
           cpa8(pool + 2 * e + 1, src + (uint32_t)(S.lane[s][d.oj >> 8].fc + p.poff[j]));
         }
@@ -616,6 +637,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
           collide_core<RHO1>(f, p);
 #pragma unroll
         for (int j = 0; j < 19; ++j) {
+          bounds_ok(in_plane(p, li.fc + p.poff[j], j));
           if (PGPU_STCS)
             __stcs(dst + (uint32_t)(li.fc + p.poff[j]), f[j]);
           else
