@@ -71,6 +71,7 @@ struct KParams {
   const int32_t* chunkbase;  // first link record of each 32-cell chunk of a row
   int32_t nchunk;            // chunks per row = ceil(nx / 32)
   const LinkRec* links;
+  const uint16_t* linkdesc;  // per record: owner lane (x & 31) | j << 5 (compact CLI sweep)
   int64_t nrec;              // link records (bounds checks of debug builds)
   int32_t fill_sectors;      // write zeros into fill-flagged non-fluid cells
   double wp, wm, rho0, nu, cf;

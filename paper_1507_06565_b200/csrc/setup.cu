@@ -97,9 +97,12 @@ __global__ void k_fill_sectors(uint32_t* __restrict__ cellw, int64_t cells) {
     if (cellw[c] & kNonFluid) cellw[c] |= kFillSector;
 }
 
+// chunkbase[rows * nchunk] is a sentinel = the link total, so a chunk's link
+// count is chunkbase[i + 1] - chunkbase[i].
 __global__ void k_chunkbase(const int32_t* __restrict__ base, int32_t* __restrict__ chunkbase,
-                            int nx, int64_t rows, int nchunk) {
+                            int nx, int64_t rows, int nchunk, const int64_t* __restrict__ total) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == rows * nchunk) chunkbase[i] = (int32_t)*total;
   if (i >= rows * nchunk) return;
   const int64_t r = i / nchunk;
   const int ch = (int)(i - r * nchunk);
@@ -228,6 +231,27 @@ __global__ void k_pack_ctab(const uint32_t* __restrict__ mask, const int32_t* __
   if (i < n) out[i] = ChunkEnt{(uint32_t)rank[i], mask[i]};
 }
 
+// Per link record: the owner's lane in its 32-cell chunk and the incoming
+// direction j, (x & 31) | j << 5 -- the compact CLI sweep's link list of a
+// chunk-plane is then a contiguous run of this array (no per-plane prefix
+// sum and publish in the kernel).  One thread per cell, links in (cell, j)
+// order exactly like the records.
+__global__ void k_linkdesc(const uint32_t* __restrict__ cellw, const int32_t* __restrict__ cellbase,
+                           int nx, int64_t cells, uint16_t* __restrict__ desc) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  const uint32_t w = cellw[c];
+  if (w & kNonFluid) return;
+  uint32_t m = w & kBounceMask;
+  int32_t r = cellbase[c];
+  const uint16_t lane = (uint16_t)((c % nx) & 31);
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    desc[r++] = (uint16_t)(lane | (j << 5));
+  }
+}
+
 __global__ void k_unpack_flags(const uint32_t* __restrict__ cellw, uint8_t* __restrict__ out,
                                int64_t cells) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -265,7 +289,8 @@ int64_t setup_bases(const int32_t* count, int32_t* base, int32_t* chunkbase, int
   ck(cudaStreamSynchronize(s), "total sync");
   if (total > INT32_MAX) return total;  // caller rejects; the scan would overflow
   ck(cub::DeviceScan::ExclusiveSum(scratch, scratch_bytes, count, base, cells, s), "scan");
-  k_chunkbase<<<blocks(rows * nchunk, 256), 256, 0, s>>>(base, chunkbase, nx, rows, nchunk);
+  k_chunkbase<<<blocks(rows * nchunk + 1, 256), 256, 0, s>>>(base, chunkbase, nx, rows, nchunk,
+                                                               d_total);
   ck(cudaGetLastError(), "k_chunkbase");
   return total;
 }
@@ -324,6 +349,12 @@ int64_t build_ctab(const uint32_t* cellw, int nx, int64_t rows, int nchunk, Chun
   cudaFree(rank);
   cudaFree(tmp);
   return (int64_t)last[0] + last[1];
+}
+
+void build_linkdesc(const uint32_t* cellw, const int32_t* cellbase, int nx, int64_t cells,
+                    uint16_t* desc, cudaStream_t s) {
+  k_linkdesc<<<blocks(cells, 256), 256, 0, s>>>(cellw, cellbase, nx, cells, desc);
+  ck(cudaGetLastError(), "k_linkdesc");
 }
 
 void unpack_flags(const uint32_t* cellw, uint8_t* out, int64_t cells, cudaStream_t s) {

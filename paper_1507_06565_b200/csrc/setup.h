@@ -46,7 +46,8 @@ struct LinkSetupArgs {
 
 void setup_cellwords(const CellSetupArgs& a, cudaStream_t s);
 size_t setup_scratch_bytes(int64_t cells);
-// Per-cell exclusive bases + per-chunk bases; returns the link total (host
+// Per-cell exclusive bases + per-chunk bases (+ one sentinel = the total: the
+// chunk base array has rows * nchunk + 1 entries); returns the link total (host
 // value; > INT32_MAX means the bases were not written), -1 if scratch is short.
 int64_t setup_bases(const int32_t* count, int32_t* base, int32_t* chunkbase, int nx, int64_t rows,
                     int nchunk, void* scratch, size_t scratch_bytes, int64_t* d_total,
@@ -59,6 +60,9 @@ void mark_lid_links(const uint32_t* cellw, const int32_t* base, double* recs, in
 // Fluid-only layout chunk table [rows][nchunk] {rank, mask}; returns the fluid count.
 int64_t build_ctab(const uint32_t* cellw, int nx, int64_t rows, int nchunk, ChunkEnt* ctab,
                    cudaStream_t s);
+// Per link record (x & 31) | j << 5 in record order (compact CLI sweep).
+void build_linkdesc(const uint32_t* cellw, const int32_t* cellbase, int nx, int64_t cells,
+                    uint16_t* desc, cudaStream_t s);
 void unpack_flags(const uint32_t* cellw, uint8_t* out, int64_t cells, cudaStream_t s);
 
 }  // namespace pgpu

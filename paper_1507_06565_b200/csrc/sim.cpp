@@ -95,6 +95,7 @@ struct pgpu_sim {
   int32_t* d_cellbase = nullptr;
   int32_t* d_chunkbase = nullptr;
   LinkRec* d_recs = nullptr;
+  uint16_t* d_linkdesc = nullptr;  // per record: owner lane | j << 5 (compact CLI sweep)
   PlaneCoef* d_planes = nullptr;
   double* d_feq = nullptr;
   int* d_flags = nullptr;  // [0] err, [1] nonfinite
@@ -131,6 +132,7 @@ struct pgpu_sim {
     cudaFree(d_cellbase);
     cudaFree(d_chunkbase);
     cudaFree(d_recs);
+    cudaFree(d_linkdesc);
     cudaFree(d_planes);
     cudaFree(d_feq);
     cudaFree(d_flags);
@@ -235,8 +237,18 @@ struct pgpu_sim {
     CK(cudaMalloc(&d_recs, sizeof(LinkRec) * n_links));
     fill_records_nan(d_recs, n_links, stream);
     kp.links = d_recs;
+    ensure_linkdesc();
     kp.nrec = n_links;
     drop_graphs();
+  }
+
+  // per-record link descriptors for the compact CLI sweep (+ 2: pair copies)
+  void ensure_linkdesc() {
+    if (d_linkdesc || n_links == 0) return;
+    CK(cudaMalloc(&d_linkdesc, sizeof(uint16_t) * (n_links + 2)));
+    CK(cudaMemsetAsync(d_linkdesc, 0, sizeof(uint16_t) * (n_links + 2), stream));
+    build_linkdesc(d_cellw, d_cellbase, nx, cells, d_linkdesc, stream);
+    kp.linkdesc = d_linkdesc;
   }
 
   SweepConfig sweep_cfg(int op, int part) const {
@@ -535,7 +547,7 @@ void device_setup(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors, Lap&& 
 
   CK(cudaMalloc(&s->d_cellw, sizeof(uint32_t) * cells));
   CK(cudaMalloc(&s->d_cellbase, sizeof(int32_t) * cells));
-  CK(cudaMalloc(&s->d_chunkbase, sizeof(int32_t) * rows * nchunk));
+  CK(cudaMalloc(&s->d_chunkbase, sizeof(int32_t) * (rows * nchunk + 1)));
   CK(cudaMalloc(&count.p, sizeof(int32_t) * cells));
   CellSetupArgs ca;
   ca.flags = flags.as<uint8_t>();
@@ -615,6 +627,7 @@ void device_setup(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors, Lap&& 
   }
   s->kp.links = s->d_recs;
   s->kp.nrec = s->d_recs ? L : 0;
+  if (s->d_recs) s->ensure_linkdesc();
   lap("link records");
 }
 

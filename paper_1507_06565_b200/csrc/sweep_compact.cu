@@ -379,7 +379,8 @@ struct CLane {
 struct alignas(16) CMeta {  // one plane, loaded two planes ahead of its issue
   uint32_t cw[kCBXp];
   ChunkEnt ent[kCW][16];  // per warp: 0..8 source rows, 9..13 x-wrap partners of rows 0..4,
-                          // 14.rank = first link record of the chunk
+                          // 14.rank / 15.rank = first link record of the chunk / the next one
+  uint16_t ldesc[kCW][kCLinkCap + 2];  // the chunk's link descriptors (one-stage CLI sweeps)
 };
 template <bool RECORDS>
 struct alignas(16) CSmem {
@@ -426,6 +427,9 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
                   int part, int zper) {
   using Sm = CSmem<RECORDS>;
   constexpr int kS = Sm::S;
+  // one-stage CLI sweeps take each chunk-plane's link list from the static
+  // per-record descriptors (p.linkdesc); two-stage ones build it per plane
+  constexpr bool kStaticDesc = RECORDS && kS == 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Sm& S = *reinterpret_cast<Sm*>(smem_raw);
   const int tx = threadIdx.x, lane = tx & 31, warp = tx >> 5;
@@ -446,7 +450,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
   // in-plane offset of this lane's chunk entry (lanes 0..8 source rows,
   // 9..13 x-wrap partners, 14 the chunk's link base), -1: nothing to load
   int eoff = -1;
-  if (lane < 15 && wok) {
+  if (lane < 16 && wok) {
     if (lane < 14) {
       const int r = lane < 9 ? lane : lane - 9;
       int ys = y - rt_row_ey(r);
@@ -454,7 +458,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
       if (wrap_coord(ys, p.ny, p.py) && (lane < 9 || (!SLAB && wrapchunk)))
         eoff = ys * p.nchunk + (lane < 9 ? xc : (xc == 0 ? p.nchunk - 1 : 0));
     } else if (RECORDS) {
-      eoff = y * p.nchunk + xc;
+      eoff = y * p.nchunk + xc;  // lane 14: this chunk's link base (lane 15: the next one)
     }
   }
 
@@ -464,7 +468,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
       cpa4(&M.cw[tx], p.cellw + ((int64_t)z * p.ny + y) * p.nx + x);
     else
       M.cw[tx] = kNonFluid;
-    if (lane < 15) {
+    if (lane < 16) {
       const int64_t plane = (int64_t)p.ny * p.nchunk;
       if (lane < 14) {
         int zs = z - rt_row_ez(lane < 9 ? lane : lane - 9);
@@ -473,8 +477,8 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
           cpa8(&M.ent[warp][lane], p.ctab + zs * plane + eoff);
         else
           M.ent[warp][lane] = ChunkEnt{0u, 0u};
-      } else if (eoff >= 0) {
-        cpa4(&M.ent[warp][14].rank, p.chunkbase + z * plane + eoff);
+      } else if (eoff >= 0) {  // chunk bases are contiguous; a sentinel follows the last
+        cpa4(&M.ent[warp][lane].rank, p.chunkbase + z * plane + eoff + (lane - 14));
       }
     }
   };
@@ -538,7 +542,25 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
       }
     }
     int total = 0;
-    if (RECORDS) {
+    if (RECORDS && kStaticDesc) {
+      // the chunk-plane's links are records [cb, cbn) with their (lane, j)
+      // descriptors already in the meta slot: no prefix sum, no publish loop
+      const int32_t cb = (int32_t)E[14].rank;
+      total = (int32_t)E[15].rank - cb;
+      if (total) {
+        double* pool = S.pool[s][warp];
+        const uint16_t* ld = M.ldesc[warp] + (cb & 1);
+        const int nl = min(total, kCLinkCap);
+        __syncwarp();  // every lane's S.lane entry of plane z is written
+        for (int e = lane; e < nl; e += 32) {
+          const int d = ld[e];
+          const int j = d >> 5, fco = S.lane[s][(tx & ~31) | (d & 31)].fc;
+          bounds_ok(cb + e < p.nrec && in_plane(p, fco + p.poff[j], j));
+          cpa8(pool + 2 * e, p.links + cb + e);
+          cpa8(pool + 2 * e + 1, src + (uint32_t)(fco + p.poff[j]));
+        }
+      }
+    } else if (RECORDS) {
       const int n = fl ? __popc(cw & kBounceMask) : 0;  // every cell of the chunk keeps its records
       const int off = warp_scan_excl(n, lane, &total);
       if (total) {
@@ -559,12 +581,29 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
     return total;
   };
 
+  // link descriptors of plane z (meta slot m; its chunk bases have landed) as
+  // 4-byte pairs from the even record at or below the chunk's first
+  auto desc_load = [&](int m) {
+    CMeta& M = S.meta[m];
+    const int32_t cb = (int32_t)M.ent[warp][14].rank;
+    const int n = min((int32_t)M.ent[warp][15].rank - cb, kCLinkCap);
+    const int a0 = cb & ~1, npairs = (cb + n - a0 + 1) >> 1;
+    for (int t = lane; t < npairs; t += 32) cpa4(&M.ldesc[warp][2 * t], p.linkdesc + a0 + 2 * t);
+  };
+
   // prologue: meta of planes z0, z0+1; issue z0; meta of z0+2
   meta_load(z0, 0);
   if (z0 + 1 < z1) meta_load(z0 + 1, 1);
   cpa_commit();
   cpa_wait_all();
   __syncwarp();
+  if (kStaticDesc) {
+    desc_load(0);
+    if (z0 + 1 < z1) desc_load(1);
+    cpa_commit();
+    cpa_wait_all();
+    __syncwarp();
+  }
   int cnt_cur = issue(z0, 0, 0);
   __syncwarp();
   if (z0 + 2 < z1) meta_load(z0 + 2, 2);
@@ -586,15 +625,24 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
       cpa_wait_all();
     }
     __syncwarp();  // ... and every lane's copies
+    if (kStaticDesc && z + 2 < z1) desc_load(ms == 0 ? 2 : ms - 1);  // plane z+2's chunk bases landed
     const CLane li = S.lane[s][tx];
     if (RECORDS && cnt_cur) {  // link closures of plane z (one-stage sweeps)
       double* const stage = &S.main[s][0][0];
       const double* pool = S.pool[s][warp];
-      const CLinkDesc* desc = reinterpret_cast<const CLinkDesc*>(pool + kCPool);
       const int ncoop = min(cnt_cur, kCLinkCap);
-      for (int e = lane; e < ncoop; e += 32) {
-        const CLinkDesc d = desc[e];
-        cclose_link(stage, d.oj >> 8, d.oj & 31, pool[2 * e], pool[2 * e + 1], p);
+      if (kStaticDesc) {
+        const uint16_t* ld = S.meta[ms].ldesc[warp] + (S.cbase[s][warp] & 1);
+        for (int e = lane; e < ncoop; e += 32) {
+          const int d = ld[e];
+          cclose_link(stage, (tx & ~31) | (d & 31), d >> 5, pool[2 * e], pool[2 * e + 1], p);
+        }
+      } else {
+        const CLinkDesc* desc = reinterpret_cast<const CLinkDesc*>(pool + kCPool);
+        for (int e = lane; e < ncoop; e += 32) {
+          const CLinkDesc d = desc[e];
+          cclose_link(stage, d.oj >> 8, d.oj & 31, pool[2 * e], pool[2 * e + 1], p);
+        }
       }
       if (cnt_cur > kCLinkCap) {  // warp-uniform: pool overflow, each lane closes the rest itself
         const uint32_t w = li.w;
