@@ -102,3 +102,42 @@ def test_compact_equals_dense_larger_domain(gpu, monkeypatch):
         out[layout] = sim.get_pdfs()
     m = fluid_mask(geom)
     assert np.array_equal(out["dense"][:, m], out["compact"][:, m])
+
+
+def test_compact_plain_per_cell_sweep(gpu, orc, tmp_path):
+    """PGPU_SWEEP=plain (read once at library load, hence a subprocess): the
+    per-cell compact sweep -- the reference point of the pipelined kernel and
+    the slab edge path for narrow bands -- against the oracle, SBB and CLI."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    script = f"""
+import sys, numpy as np
+sys.path.insert(0, {str(root)!r})
+sys.path.insert(0, {str(Path(__file__).resolve().parent)!r})
+import paper_1507_06565_b200 as pg
+from test_gpu_compact import geometry
+geom = geometry(pg, (45, 20, 24), 10, 2.0, 4.5, seed=5)
+p = pg.relaxation_from_magic(0.08, 3.0 / 16.0)
+p.body_force = (2e-6, 1e-6, -5e-7)
+for scheme in (0, 1):
+    sim = pg.Simulation.from_params(geom, p, pg.WallScheme(scheme))
+    sim.step(9)
+    np.save({str(tmp_path)!r} + f"/plain_{{scheme}}.npy", sim.get_pdfs())
+"""
+    env = dict(os.environ, PGPU_SWEEP="plain", PGPU_LAYOUT="compact")
+    res = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    geom = geometry(gpu, (45, 20, 24), 10, 2.0, 4.5, seed=5)
+    m = fluid_mask(geom)
+    p = gpu.relaxation_from_magic(0.08, 3.0 / 16.0)
+    p.body_force = (2e-6, 1e-6, -5e-7)
+    for scheme in (0, 1):
+        o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, scheme)
+        o.step(9)
+        got = np.load(tmp_path / f"plain_{scheme}.npy")
+        assert np.array_equal(got[:, m], o.get_pdfs()[:, m])
