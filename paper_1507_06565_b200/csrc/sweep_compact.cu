@@ -18,10 +18,12 @@
 //
 // K1 keeps the structure of kernels.cu's k_sweep_pipe (per-thread cp.async
 // pipeline, pooled link closures) with fluid-only addressing: one chunk entry
-// per source row and plane gives every pull slot with a popcount (see
+// per source row and plane gives every pull slot with a popcount, and the
+// CLI link lists come from static per-record descriptors (see
 // k_sweep_cpipe).  A TMA variant (one cp.async.bulk per direction run and
 // warp) moved the same bytes but was instruction-bound (3.35 G instructions
-// per C4 launch vs 2.16 G, 7.1 ms); it is kept in tools/experiments/.
+// per C4 launch vs 2.16 G, 7.1 ms); it is kept in tools/experiments/, and the
+// measured configuration choices are in profiles/r01b_compact_k1_ncu_summary.md.
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
@@ -301,10 +303,13 @@ __device__ __forceinline__ const double* wrap_src(const KParams& p, const double
 // source slot is q_r (e_x = 0), q_r - 1 (e_x = +1) or q_r + bit(mask, lane)
 // (e_x = -1) -- exact because a pulled source is always fluid.  Bounce
 // directions load g_k(x) from the cell's own slot instead (f_j = g_k(x) for
-// SBB; CLI / moving-wall links are closed from a per-warp pool exactly as in
-// kernels.cu's k_sweep_pipe).  Addresses are 32-bit slot offsets from the
-// buffer base (plane j at p.poff[j]); only lanes on the periodic x faces
-// take the general path (partner chunk / slab ghosts).
+// SBB).  CLI / moving-wall links: a chunk-plane's links are the records
+// [chunkbase, next chunkbase); their descriptors (owner lane | j << 5, built
+// once at setup) ride in the meta ring, the 32 lanes copy each link's record
+// and g_j(x) into a per-warp pool with the plane's populations, and close the
+// links cooperatively in shared memory before the collision.  Addresses are
+// 32-bit slot offsets from the buffer base (plane j at p.poff[j]); only lanes
+// on the periodic x faces take the general path (partner chunk / slab ghosts).
 // ---------------------------------------------------------------------------
 constexpr int kCW = 4;            // warps (= chunks) per block
 constexpr int kCBXp = kCW * 32;   // cells per block
