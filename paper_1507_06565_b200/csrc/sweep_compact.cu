@@ -94,6 +94,12 @@ __host__ __device__ constexpr int row_dir(int r, int i) {
                   : r + 10;
 }
 
+// x-slab split: each edge band (edge_band() = 32 columns) is exactly the first
+// / last 32-cell chunk of a row.
+__host__ __device__ __forceinline__ bool edge_chunks(const KParams& p) {
+  return p.nx % 32 == 0 && p.nx >= 64;
+}
+
 // Periodic wrap of a row coordinate; false if it leaves a non-periodic axis.
 __device__ __forceinline__ bool wrap_coord(int& v, int n, int periodic) {
   if (v >= 0 && v < n) return true;
@@ -441,8 +447,21 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
   // warps are independent: a block covers 4 chunks of one row, or (edge part,
   // x-slab split) the first and last chunk of two rows
   const bool edges = part == PART_EDGES;
-  const int xc = edges ? ((warp & 1) ? p.nchunk - 1 : 0) : blockIdx.x * kCW + warp;
-  const int y = edges ? blockIdx.y * 2 + (warp >> 1) : blockIdx.y;
+  // interior part with whole-chunk edge bands: warps walk the (row, interior
+  // chunk) pairs linearly, so no warp slot is spent on an edge chunk
+  const bool ilin = part == PART_INTERIOR && edge_chunks(p);
+  int xc, y;
+  if (edges) {
+    xc = (warp & 1) ? p.nchunk - 1 : 0;
+    y = blockIdx.y * 2 + (warp >> 1);
+  } else if (ilin) {
+    const int ni = p.nchunk - 2, wl = blockIdx.x * kCW + warp;
+    y = wl / ni;
+    xc = 1 + wl % ni;
+  } else {
+    xc = blockIdx.x * kCW + warp;
+    y = blockIdx.y;
+  }
   const int x = xc * 32 + lane;
   const int z0 = blockIdx.z * zper;
   const int z1 = min(z0 + zper, p.nz);
@@ -732,8 +751,7 @@ template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
 void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
                       cudaStream_t s) {
   // the pipelined kernel sweeps the slab edge bands when each band is one chunk
-  const bool edge_chunks = p.nx % 32 == 0 && p.nx >= 64;
-  if (cfg.part == PART_EDGES && (!edge_chunks || g_plain_sweep())) {
+  if (cfg.part == PART_EDGES && (!edge_chunks(p) || g_plain_sweep())) {
     k_csweep_edges<RHO1, GLBM, RECORDS, SLAB, OP>
         <<<dim3(2, (p.ny + 3) / 4, p.nz), 128, 0, s>>>(p, src, dst);
   } else if (g_plain_sweep()) {
@@ -741,9 +759,12 @@ void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* sr
         p, src, dst, cfg.part);
   } else {
     const int zper = cpipe_zper(p);
-    const dim3 grid = cfg.part == PART_EDGES
-                          ? dim3(1, (p.ny + 1) / 2, (p.nz + zper - 1) / zper)
-                          : dim3((p.nchunk + kCW - 1) / kCW, p.ny, (p.nz + zper - 1) / zper);
+    const int zg = (p.nz + zper - 1) / zper;
+    dim3 grid((p.nchunk + kCW - 1) / kCW, p.ny, zg);
+    if (cfg.part == PART_EDGES) grid = dim3(1, (p.ny + 1) / 2, zg);
+    if (cfg.part == PART_INTERIOR && edge_chunks(p))
+      grid = dim3((unsigned)(((int64_t)p.ny * (p.nchunk - 2) + kCW - 1) / kCW), 1, zg);
+    if (grid.x == 0) return;  // nx == 64 slab: everything is edge band
     constexpr int smem = (int)sizeof(CSmem<RECORDS>);
     static bool attr = [] {
       cudaFuncSetAttribute(k_sweep_cpipe<RHO1, GLBM, RECORDS, SLAB, OP>,
