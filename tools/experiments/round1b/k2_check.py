@@ -1,4 +1,4 @@
-"""Experiment check: PGPU_K2=1 (two steps per launch) vs the one-step sweep, bitwise."""
+"""Experiment check used with the temporal-blocking prototype (tools/experiments/k2_plane_sync.cu wired in behind PGPU_K2=1; not in the product build): two-steps-per-launch vs the one-step sweep, bitwise."""
 import os, sys, time, subprocess
 from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
