@@ -317,7 +317,10 @@ __device__ __forceinline__ const double* wrap_src(const KParams& p, const double
 // 32-bit slot offsets from the buffer base (plane j at p.poff[j]); only lanes
 // on the periodic x faces take the general path (partner chunk / slab ghosts).
 // ---------------------------------------------------------------------------
-constexpr int kCW = 4;            // warps (= chunks) per block
+#ifndef PGPU_CW
+#define PGPU_CW 4
+#endif
+constexpr int kCW = PGPU_CW;      // warps (= chunks) per block
 constexpr int kCBXp = kCW * 32;   // cells per block
 #ifndef PGPU_CLI_STAGES
 #define PGPU_CLI_STAGES 1
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
   int xc, y;
   if (edges) {
     xc = (warp & 1) ? p.nchunk - 1 : 0;
-    y = blockIdx.y * 2 + (warp >> 1);
+    y = blockIdx.y * (kCW / 2) + (warp >> 1);
   } else if (ilin) {
     const int ni = p.nchunk - 2, wl = blockIdx.x * kCW + warp;
     y = wl / ni;
@@ -761,7 +764,7 @@ void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* sr
     const int zper = cpipe_zper(p);
     const int zg = (p.nz + zper - 1) / zper;
     dim3 grid((p.nchunk + kCW - 1) / kCW, p.ny, zg);
-    if (cfg.part == PART_EDGES) grid = dim3(1, (p.ny + 1) / 2, zg);
+    if (cfg.part == PART_EDGES) grid = dim3(1, (p.ny + kCW / 2 - 1) / (kCW / 2), zg);
     if (cfg.part == PART_INTERIOR && edge_chunks(p))
       grid = dim3((unsigned)(((int64_t)p.ny * (p.nchunk - 2) + kCW - 1) / kCW), 1, zg);
     if (grid.x == 0) return;  // nx == 64 slab: everything is edge band
