@@ -140,7 +140,9 @@ class DistTransport:
         me = self.me
         main = me.stream
         if getattr(self, "_edge_stream", None) is None:
-            self._edge_stream = torch.cuda.Stream(device=main.device)
+            # high priority: the edge part (and the exchange ordered after it)
+            # is dispatched ahead of the interior sweep's remaining blocks
+            self._edge_stream = torch.cuda.Stream(device=main.device, priority=-1)
         edge = self._edge_stream
         edge.wait_stream(main)  # everything issued before step() on the main stream
         prev_edge = None
