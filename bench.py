@@ -291,17 +291,20 @@ def run_ours(args):
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_per_launch}
 
-    # e2e through the public API with host buffers
+    # e2e through the public API with host buffers.  The device-resident
+    # simulation stays alive meanwhile (52 GB of 180 GB on C4): reallocating
+    # the 26 GB it would free right away made cudaMalloc take up to 0.7 s in
+    # some runs (tools/e2e_probe.py), a driver effect unrelated to the path.
     e2e = None
     if world == 1 and not args.no_e2e and not args.force_slab:
-        del sim
-        torch.cuda.empty_cache()
         e2e = e2e_run(pg, configs, w, geom, args.steps, local)
     elif (world > 1 or args.force_slab) and not args.no_e2e:
         slab_geom = sim_obj.me.geometry
-        del sim, sim_obj, stepper
-        torch.cuda.empty_cache()
         e2e = e2e_run_dist(w, slab_geom, args.steps, rank, world, local, dist)
+    del sim, stepper
+    if world > 1 or args.force_slab:
+        del sim_obj
+    torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.force_slab:
