@@ -62,11 +62,7 @@ __device__ __forceinline__ int64_t fidx(const KParams& p, int x, int y, int z) {
   return (int64_t)e.rank + __popc(e.mask & ((1u << (x & 31)) - 1u));
 }
 
-// Directions with e_x = +1 / -1 (their x = 0 / x = nx-1 pulls wrap).
-constexpr uint32_t kExPlus = (1u << 1) | (1u << 7) | (1u << 9) | (1u << 11) | (1u << 13);
-constexpr uint32_t kExMinus = (1u << 2) | (1u << 8) | (1u << 10) | (1u << 12) | (1u << 14);
-
-// Source rows: row r holds the directions with (e_y, e_z) = kRowE[r]; their
+// Source rows: row r holds the directions with (e_y, e_z) = (row_ey(r), row_ez(r)); their
 // pull sources lie in row (y - e_y, z - e_z).
 //   r0 (0,0): 0 1 2   r1 (1,0): 3 7 10   r2 (-1,0): 4 8 9   r3 (0,1): 5 11 14
 //   r4 (0,-1): 6 12 13   r5 (1,1): 15   r6 (-1,-1): 16   r7 (1,-1): 17   r8 (-1,1): 18
@@ -83,15 +79,6 @@ __host__ __device__ constexpr int row_of(int j) {
          : (j == 5 || j == 11 || j == 14) ? 3
          : (j == 6 || j == 12 || j == 13) ? 4
                                           : j - 10;  // 15..18 -> 5..8
-}
-__host__ __device__ constexpr int row_ndirs(int r) { return r < 5 ? 3 : 1; }
-__host__ __device__ constexpr int row_dir(int r, int i) {
-  return r == 0 ? i
-         : r == 1 ? (i == 0 ? 3 : (i == 1 ? 7 : 10))
-         : r == 2 ? (i == 0 ? 4 : (i == 1 ? 8 : 9))
-         : r == 3 ? (i == 0 ? 5 : (i == 1 ? 11 : 14))
-         : r == 4 ? (i == 0 ? 6 : (i == 1 ? 12 : 13))
-                  : r + 10;
 }
 
 // x-slab split: each edge band (edge_band() = 32 columns) is exactly the first
