@@ -100,3 +100,21 @@ def test_sbb_scheme_ignores_second_fluid(gpu):
     sim.step(7)
     ref.step(7)
     assert np.array_equal(sim.get_pdfs(), ref.get_pdfs())
+
+
+def test_staged_upload_large_arrays(gpu):
+    """Arrays of >= 32 MB go through the pinned-chunk uploader (staging.h):
+    a 256x256x520 flag field (34 MB) and ~4.3 M links (> 32 MB per link
+    array) must arrive intact -- the device-built cell words reproduce the
+    flags byte for byte and the link list passes the exact validation."""
+    pg = gpu
+    rng = np.random.default_rng(11)
+    dims = (256, 256, 520)
+    n = 2600
+    c = np.c_[rng.uniform(0, dims[0], n), rng.uniform(0, dims[1], n), rng.uniform(1, 519, n)]
+    pack = pg.SpherePack(c, rng.uniform(3.0, 6.0, n), tuple(float(d) for d in dims))
+    g = pg.voxelize(pack, dims, (True, True, False), True, True)
+    assert g.flags.nbytes >= 32 << 20 and g.n_links * 8 >= 32 << 20
+    sim = _create(pg, g)
+    assert sim.fluid_cells == g.fluid_cells
+    assert np.array_equal(sim.flags().reshape(-1), np.asarray(g.flags).reshape(-1))
