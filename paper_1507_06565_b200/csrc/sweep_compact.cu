@@ -327,6 +327,9 @@ __host__ __device__ constexpr int cp_stages(bool records) {
 __host__ __device__ constexpr int cp_minb(bool records) {
   return records ? PGPU_CLI_MINB : PGPU_SBB_MINB;
 }
+#ifndef PGPU_SMEM_PAD
+#define PGPU_SMEM_PAD 0
+#endif
 #ifndef PGPU_BOUNDS
 #define PGPU_BOUNDS 0  // debug builds: trap on any out-of-range slot / record / ghost address
 #endif
@@ -755,7 +758,7 @@ void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* sr
     if (cfg.part == PART_INTERIOR && edge_chunks(p))
       grid = dim3((unsigned)(((int64_t)p.ny * (p.nchunk - 2) + kCW - 1) / kCW), 1, zg);
     if (grid.x == 0) return;  // nx == 64 slab: everything is edge band
-    constexpr int smem = (int)sizeof(CSmem<RECORDS>);
+    constexpr int smem = (int)sizeof(CSmem<RECORDS>) + PGPU_SMEM_PAD;  // pad: L1-capacity experiment
     static bool attr = [] {
       cudaFuncSetAttribute(k_sweep_cpipe<RHO1, GLBM, RECORDS, SLAB, OP>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
