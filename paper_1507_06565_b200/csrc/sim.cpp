@@ -538,12 +538,14 @@ void device_setup(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors, Lap&& 
     upload(glo, g->ghost_flags_lo, rows, st);
     upload(ghi, g->ghost_flags_hi, rows, st);
   }
+  lap("upload flags");
   upload(lf, g->link_fluid_cell, L, st);
+  lap("upload link cells");
   upload(ls, g->link_second_fluid, L, st);
   upload(ld, g->link_direction, L, st);
   upload(lq, g->link_q, L, st);
   if (g->link_moving) upload(lm, g->link_moving, L, st);
-  lap("upload flags+links");
+  lap("upload other link arrays");
 
   CK(cudaMalloc(&s->d_cellw, sizeof(uint32_t) * cells));
   CK(cudaMalloc(&s->d_cellbase, sizeof(int32_t) * cells));

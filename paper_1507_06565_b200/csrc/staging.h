@@ -11,7 +11,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstdint>
 #include <cstring>
@@ -103,6 +105,7 @@ class StagedUpload {
                         (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice ||
                          at.type == cudaMemoryTypeManaged);
     cudaGetLastError();
+    const size_t kChunk = chunk_;
     if (pinned || bytes < 2 * kChunk) {
       cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
       return e != cudaSuccess ? e : cudaStreamSynchronize(st);
@@ -110,7 +113,7 @@ class StagedUpload {
     std::lock_guard<std::mutex> lock(mu_);
     if (!stage_[0]) {
       for (auto& b : stage_) {
-        cudaError_t e = cudaHostAlloc(&b, kChunk, cudaHostAllocPortable);
+        cudaError_t e = cudaHostAlloc(&b, chunk_, cudaHostAllocPortable);
         if (e != cudaSuccess) return e;
       }
     }
@@ -146,8 +149,10 @@ class StagedUpload {
   }
 
  private:
-  StagedUpload() : pool_(kParts - 1) {}
-  static constexpr size_t kChunk = size_t(16) << 20;
+  StagedUpload() : pool_(kParts - 1) {
+    if (const char* e = std::getenv("PGPU_STAGE_MB")) chunk_ = size_t(std::max(1, atoi(e))) << 20;
+  }
+  size_t chunk_ = size_t(16) << 20;  // bytes per pinned chunk (PGPU_STAGE_MB overrides)
   static constexpr int kSlots = 4;
   static constexpr int kParts = 8;
   std::mutex mu_;
