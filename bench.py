@@ -330,7 +330,7 @@ def run_ours(args):
                        "cells": int(np.prod(w.dims)), "scheme": w.scheme.name,
                        "l2": "inputs larger than L2 (2 x 19 x cells x 8 B >> 126 MB)",
                        "parallelism": f"x-slab{world}" if (world > 1 or args.force_slab)
-                       else "single", **w.meta},
+                       else "single", "math": args.math, **w.meta},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -420,6 +420,10 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--scheme", default=None, choices=["SBB", "CLI"],
                     help="override the config's wall scheme (experiments only)")
+    ap.add_argument("--math", default="fast", choices=["fast", "exact"],
+                    help="pgpu_math_mode: fast = FMA-contracted collision + folded CLI links "
+                         "(<= 1e-12 vs the reference, tests/test_gpu_fast.py); exact = "
+                         "bit-identical to the reference")
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -427,6 +431,7 @@ def main():
                     help="diagnostic: run the multi-GPU slab path (edge/interior split, halo "
                          "exchange) even at N=1")
     args = ap.parse_args()
+    os.environ["PGPU_MATH"] = args.math  # read by pgpu_create
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)

@@ -69,6 +69,13 @@ enum pgpu_status {
 };
 
 enum pgpu_wall_scheme { PGPU_SBB = 0, PGPU_CLI = 1 }; /* boundary.hpp:12 */
+/* Arithmetic of the time step (no reference analogue: the reference has one).
+ * EXACT: every fp64 operation in the reference's order, results bit-identical
+ * to simulation.cpp.  FAST: the same TRT algebra FMA-contracted and
+ * regrouped, with CLI links folded into the stored state;
+ * agrees with the reference to <= 1e-12 relative (the north-star tolerance).
+ * pgpu_create starts in EXACT unless the environment sets PGPU_MATH=fast. */
+enum pgpu_math_mode { PGPU_MATH_EXACT = 0, PGPU_MATH_FAST = 1 };
 enum pgpu_glbm_viscosity { PGPU_VISC_PLAIN = 0, PGPU_VISC_RESCALED = 1, PGPU_VISC_CONSTANT_RATIO = 2 };
 
 typedef struct pgpu_sim pgpu_sim;
@@ -221,6 +228,8 @@ int pgpu_get_stream(pgpu_sim* sim, void** stream);
 int pgpu_synchronize(pgpu_sim* sim);
 
 int pgpu_get_params(pgpu_sim* sim, pgpu_fluid_params* out);
+int pgpu_set_math_mode(pgpu_sim* sim, int32_t mode);
+int pgpu_get_math_mode(pgpu_sim* sim, int32_t* mode);
 int pgpu_set_body_force(pgpu_sim* sim, const double g[3]);
 int pgpu_set_lid_velocity(pgpu_sim* sim, const double u[3]);
 /* GlbmPlaneParams (simulation.hpp:18-27); n must equal nz. */

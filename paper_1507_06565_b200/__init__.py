@@ -15,6 +15,7 @@ from .porolb import (  # noqa: F401
     GeometryError,
     GlbmPlaneParams,
     GlbmViscosity,
+    MathMode,
     NumericalInstability,
     ProfileData,
     RunStats,

@@ -87,6 +87,8 @@ SIGNATURES = {
     "pgpu_get_stream": (C.c_int, [vp, P(vp)]),
     "pgpu_synchronize": (C.c_int, [vp]),
     "pgpu_get_params": (C.c_int, [vp, P(FluidParams)]),
+    "pgpu_set_math_mode": (C.c_int, [vp, i32]),
+    "pgpu_get_math_mode": (C.c_int, [vp, P(i32)]),
     "pgpu_set_body_force": (C.c_int, [vp, P(f64)]),
     "pgpu_set_lid_velocity": (C.c_int, [vp, P(f64)]),
     "pgpu_set_porous": (C.c_int, [vp, i32, P(f64), P(f64), P(f64), P(f64), f64, i32]),

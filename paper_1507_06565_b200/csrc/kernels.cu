@@ -100,7 +100,7 @@ __device__ __forceinline__ void links_all(double (&f)[19], const double* __restr
   }
 }
 
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP, bool COHERENT = false>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP, bool COHERENT = false>
 __device__ __forceinline__ void sweep_cell(const KParams& p, const double* __restrict__ src,
                                            double* __restrict__ dst, int x, int y, int z,
                                            CellWord cw) {
@@ -116,12 +116,7 @@ __device__ __forceinline__ void sweep_cell(const KParams& p, const double* __res
   double f[19];
   load_all<0, SLAB, COHERENT>(f, src, x, y, z, c, p, w);
   if (RECORDS && (w & kBounceMask)) links_all<1, COHERENT>(f, src, c, p, w, cw.base);
-  if (OP == OP_STREAM_COLLIDE) {
-    if (GLBM)
-      collide_glbm<RHO1>(f, p, z);
-    else
-      collide_core<RHO1>(f, p);
-  }
+  if (OP == OP_STREAM_COLLIDE) collide<CM, GLBM>(f, p, z);
 #pragma unroll
   for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + c, f[j]);
   if (SLAB && OP == OP_STREAM_COLLIDE) {
@@ -156,7 +151,7 @@ constexpr int kZPer = 4;
 #define PGPU_SWEEP_MINB 5
 #endif
 
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(128, PGPU_SWEEP_MINB) k_sweep(const KParams p, const double* __restrict__ src,
                                                double* __restrict__ dst, int part) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -169,7 +164,7 @@ __global__ void __launch_bounds__(128, PGPU_SWEEP_MINB) k_sweep(const KParams p,
   for (int z = z0; z < z1; ++z) {
     const CellWord cw = next;
     if (z + 1 < z1) next = ld_cw(p, ((int64_t)(z + 1) * p.ny + y) * p.nx + x);
-    sweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z, cw);
+    sweep_cell<CM, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z, cw);
   }
 }
 
@@ -341,7 +336,7 @@ __device__ __forceinline__ void close_link(double* stage_base, int owner, int j,
 // therefore cost no registers.  Non-fluid cells that share a 32-byte sector
 // with fluid cells write zeros so no DRAM sector is ever partially written.
 // ---------------------------------------------------------------------------
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     k_sweep_pipe(const KParams p, const double* __restrict__ src, double* __restrict__ dst,
                  int part, int zper) {
@@ -487,12 +482,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
 #pragma unroll
       for (int j = 0; j < 19; ++j) __stcs(dc + p.plane_off[j], 0.0);
     } else if (fluid) {
-      if (OP == OP_STREAM_COLLIDE) {
-        if (GLBM)
-          collide_glbm<RHO1>(f, p, z);
-        else
-          collide_core<RHO1>(f, p);
-      }
+      if (OP == OP_STREAM_COLLIDE) collide<CM, GLBM>(f, p, z);
       if (kLateW) {
         cw_nn = next_w(z + 2);
         got_nn = true;
@@ -536,7 +526,7 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
 // evolving state is read with L2-coherent loads (written by other blocks in
 // the same launch); the grid barrier orders the steps.
 // ---------------------------------------------------------------------------
-template <bool RHO1, bool GLBM, bool RECORDS>
+template <int CM, bool GLBM, bool RECORDS>
 __global__ void __launch_bounds__(128) k_sweep_persistent(const KParams p, double* a, double* b,
                                                           int64_t nsteps) {
   cg::grid_group grid = cg::this_grid();
@@ -549,7 +539,7 @@ __global__ void __launch_bounds__(128) k_sweep_persistent(const KParams p, doubl
       const int x = (int)(c % p.nx);
       const int64_t r = c / p.nx;
       const int y = (int)(r % p.ny), z = (int)(r / p.ny);
-      sweep_cell<RHO1, GLBM, RECORDS, false, OP_STREAM_COLLIDE, true>(p, src, dst, x, y, z,
+      sweep_cell<CM, GLBM, RECORDS, false, OP_STREAM_COLLIDE, true>(p, src, dst, x, y, z,
                                                                       ld_cw(p, c));
     }
     grid.sync();
@@ -557,7 +547,7 @@ __global__ void __launch_bounds__(128) k_sweep_persistent(const KParams p, doubl
 }
 
 // Edge columns x = 0 and x = nx-1 only (slab overlap path).
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(128) k_sweep_edges(const KParams p,
                                                      const double* __restrict__ src,
                                                      double* __restrict__ dst) {
@@ -570,11 +560,11 @@ __global__ void __launch_bounds__(128) k_sweep_edges(const KParams p,
   const int x = blockIdx.x ? p.nx - w + xx : xx;
   if (blockIdx.x && x < w) return;  // the bands overlap when nx < 2w
   const CellWord cw = ld_cw(p, ((int64_t)z * p.ny + y) * p.nx + x);
-  sweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z, cw);
+  sweep_cell<CM, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z, cw);
 }
 
 // K0: collide every fluid cell in place (first step from a pre-collision state).
-template <bool RHO1, bool GLBM, bool SLAB>
+template <int CM, bool GLBM, bool SLAB>
 __global__ void __launch_bounds__(128) k_collide_inplace(const KParams p, double* buf) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y, z = blockIdx.z;
@@ -584,10 +574,7 @@ __global__ void __launch_bounds__(128) k_collide_inplace(const KParams p, double
   double f[19];
 #pragma unroll
   for (int j = 0; j < 19; ++j) f[j] = buf[(int64_t)j * p.ks + c];
-  if (GLBM)
-    collide_glbm<RHO1>(f, p, z);
-  else
-    collide_core<RHO1>(f, p);
+  collide<CM, GLBM>(f, p, z);
 #pragma unroll
   for (int j = 0; j < 19; ++j) buf[(int64_t)j * p.ks + c] = f[j];
   if (SLAB) {
@@ -781,55 +768,55 @@ dim3 sweep_grid(const KParams& p) {
   return dim3((p.nx + bx - 1) / bx, p.ny, (p.nz + kZPer - 1) / kZPer);
 }
 
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 void launch_sweep_t(const KParams& p, const double* src, double* dst, int part,
                     cudaStream_t s) {
   if (part == PART_EDGES) {
-    k_sweep_edges<RHO1, GLBM, RECORDS, SLAB, OP>
+    k_sweep_edges<CM, GLBM, RECORDS, SLAB, OP>
         <<<dim3(2, (p.ny + 3) / 4, p.nz), 128, 0, s>>>(p, src, dst);
   } else if (g_sweep_mode <= 1) {
     const int zper = pipe_zper(p);
     const dim3 grid((p.nx + kPipeBX - 1) / kPipeBX, p.ny, (p.nz + zper - 1) / zper);
     static bool attr = [] {
-      cudaFuncSetAttribute(k_sweep_pipe<RHO1, GLBM, RECORDS, SLAB, OP>,
+      cudaFuncSetAttribute(k_sweep_pipe<CM, GLBM, RECORDS, SLAB, OP>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, pipe_smem(RECORDS));
       if (const char* e = std::getenv("PGPU_CARVEOUT"))  // experiment knob (percent)
-        cudaFuncSetAttribute(k_sweep_pipe<RHO1, GLBM, RECORDS, SLAB, OP>,
+        cudaFuncSetAttribute(k_sweep_pipe<CM, GLBM, RECORDS, SLAB, OP>,
                              cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
       return true;
     }();
     (void)attr;
-    k_sweep_pipe<RHO1, GLBM, RECORDS, SLAB, OP><<<grid, kPipeBX, pipe_smem(RECORDS), s>>>(p, src, dst,
+    k_sweep_pipe<CM, GLBM, RECORDS, SLAB, OP><<<grid, kPipeBX, pipe_smem(RECORDS), s>>>(p, src, dst,
                                                                                  part, zper);
   } else {
-    k_sweep<RHO1, GLBM, RECORDS, SLAB, OP><<<sweep_grid(p), cell_block(p), 0, s>>>(p, src, dst,
+    k_sweep<CM, GLBM, RECORDS, SLAB, OP><<<sweep_grid(p), cell_block(p), 0, s>>>(p, src, dst,
                                                                                   part);
   }
 }
 
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB>
 void dispatch_op(int op, const KParams& p, const double* src, double* dst, int part,
                  cudaStream_t s) {
   if (op == OP_STREAM_COLLIDE)
-    launch_sweep_t<RHO1, GLBM, RECORDS, SLAB, OP_STREAM_COLLIDE>(p, src, dst, part, s);
+    launch_sweep_t<CM, GLBM, RECORDS, SLAB, OP_STREAM_COLLIDE>(p, src, dst, part, s);
   else
-    launch_sweep_t<RHO1, GLBM, RECORDS, SLAB, OP_STREAM_ONLY>(p, src, dst, part, s);
+    launch_sweep_t<CM, GLBM, RECORDS, SLAB, OP_STREAM_ONLY>(p, src, dst, part, s);
 }
-template <bool RHO1, bool GLBM, bool RECORDS>
+template <int CM, bool GLBM, bool RECORDS>
 void dispatch_slab(bool slab, int op, const KParams& p, const double* src, double* dst,
                    int part, cudaStream_t s) {
   if (slab)
-    dispatch_op<RHO1, GLBM, RECORDS, true>(op, p, src, dst, part, s);
+    dispatch_op<CM, GLBM, RECORDS, true>(op, p, src, dst, part, s);
   else
-    dispatch_op<RHO1, GLBM, RECORDS, false>(op, p, src, dst, part, s);
+    dispatch_op<CM, GLBM, RECORDS, false>(op, p, src, dst, part, s);
 }
-template <bool RHO1, bool GLBM>
+template <int CM, bool GLBM>
 void dispatch_rec(bool rec, bool slab, int op, const KParams& p, const double* src,
                   double* dst, int part, cudaStream_t s) {
   if (rec)
-    dispatch_slab<RHO1, GLBM, true>(slab, op, p, src, dst, part, s);
+    dispatch_slab<CM, GLBM, true>(slab, op, p, src, dst, part, s);
   else
-    dispatch_slab<RHO1, GLBM, false>(slab, op, p, src, dst, part, s);
+    dispatch_slab<CM, GLBM, false>(slab, op, p, src, dst, part, s);
 }
 }  // namespace
 
@@ -839,23 +826,25 @@ void launch_sweep(const SweepConfig& cfg, const KParams& p, const double* src, d
     launch_sweep_compact(cfg, p, src, dst, s);
     return;
   }
-  const bool rho1 = p.rho0 == 1.0;
-  if (rho1) {
-    if (cfg.glbm)
-      dispatch_rec<true, true>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
-    else
-      dispatch_rec<true, false>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
-  } else {
-    if (cfg.glbm)
-      dispatch_rec<false, true>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
-    else
-      dispatch_rec<false, false>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
+  switch (collide_mode(p)) {
+    case CM_FAST:
+    case CM_FAST_FOLD:  // (folding is a fluid-only-layout feature)
+      if (cfg.glbm) dispatch_rec<CM_FAST, true>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
+      else dispatch_rec<CM_FAST, false>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
+      break;
+    case CM_EXACT_RHO1:
+      if (cfg.glbm) dispatch_rec<CM_EXACT_RHO1, true>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
+      else dispatch_rec<CM_EXACT_RHO1, false>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
+      break;
+    default:
+      if (cfg.glbm) dispatch_rec<CM_EXACT, true>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
+      else dispatch_rec<CM_EXACT, false>(cfg.records, cfg.slab, cfg.op, p, src, dst, cfg.part, s);
   }
 }
 
-template <bool RHO1, bool GLBM, bool RECORDS>
+template <int CM, bool GLBM, bool RECORDS>
 int64_t persistent_t(const KParams& p, double* a, double* b, int64_t nsteps, cudaStream_t s) {
-  auto kern = k_sweep_persistent<RHO1, GLBM, RECORDS>;
+  auto kern = k_sweep_persistent<CM, GLBM, RECORDS>;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -872,37 +861,45 @@ int64_t persistent_t(const KParams& p, double* a, double* b, int64_t nsteps, cud
              : -1;
 }
 
+template <int CM>
+int64_t persistent_cm(const SweepConfig& cfg, const KParams& p, double* a, double* b,
+                      int64_t nsteps, cudaStream_t s) {
+  if (cfg.glbm) return cfg.records ? persistent_t<CM, true, true>(p, a, b, nsteps, s)
+                                   : persistent_t<CM, true, false>(p, a, b, nsteps, s);
+  return cfg.records ? persistent_t<CM, false, true>(p, a, b, nsteps, s)
+                     : persistent_t<CM, false, false>(p, a, b, nsteps, s);
+}
+
 int launch_sweep_persistent(const SweepConfig& cfg, const KParams& p, double* a, double* b,
                             int64_t nsteps, cudaStream_t s) {
-  const bool rho1 = p.rho0 == 1.0;
-  int64_t r;
-  if (rho1) {
-    if (cfg.glbm) r = cfg.records ? persistent_t<true, true, true>(p, a, b, nsteps, s)
-                                  : persistent_t<true, true, false>(p, a, b, nsteps, s);
-    else r = cfg.records ? persistent_t<true, false, true>(p, a, b, nsteps, s)
-                         : persistent_t<true, false, false>(p, a, b, nsteps, s);
-  } else {
-    if (cfg.glbm) r = cfg.records ? persistent_t<false, true, true>(p, a, b, nsteps, s)
-                                  : persistent_t<false, true, false>(p, a, b, nsteps, s);
-    else r = cfg.records ? persistent_t<false, false, true>(p, a, b, nsteps, s)
-                         : persistent_t<false, false, false>(p, a, b, nsteps, s);
+  switch (collide_mode(p)) {
+    case CM_FAST:
+    case CM_FAST_FOLD: return (int)persistent_cm<CM_FAST>(cfg, p, a, b, nsteps, s);
+    case CM_EXACT_RHO1: return (int)persistent_cm<CM_EXACT_RHO1>(cfg, p, a, b, nsteps, s);
+    default: return (int)persistent_cm<CM_EXACT>(cfg, p, a, b, nsteps, s);
   }
-  return (int)r;
+}
+
+template <int CM>
+void collide_inplace_cm(bool glbm, bool slab, const KParams& p, double* buf, cudaStream_t s) {
+  const dim3 g = cell_grid2(p), b = cell_block(p);
+  if (glbm) {
+    if (slab) k_collide_inplace<CM, true, true><<<g, b, 0, s>>>(p, buf);
+    else k_collide_inplace<CM, true, false><<<g, b, 0, s>>>(p, buf);
+  } else {
+    if (slab) k_collide_inplace<CM, false, true><<<g, b, 0, s>>>(p, buf);
+    else k_collide_inplace<CM, false, false><<<g, b, 0, s>>>(p, buf);
+  }
 }
 
 void launch_collide_inplace(bool glbm, bool slab, const KParams& p, double* buf,
                             cudaStream_t s) {
-  const dim3 g = cell_grid2(p), b = cell_block(p);
-  const bool rho1 = p.rho0 == 1.0;
-#define PGPU_K0(R, G, S) k_collide_inplace<R, G, S><<<g, b, 0, s>>>(p, buf)
-  if (rho1) {
-    if (glbm) { if (slab) PGPU_K0(true, true, true); else PGPU_K0(true, true, false); }
-    else { if (slab) PGPU_K0(true, false, true); else PGPU_K0(true, false, false); }
-  } else {
-    if (glbm) { if (slab) PGPU_K0(false, true, true); else PGPU_K0(false, true, false); }
-    else { if (slab) PGPU_K0(false, false, true); else PGPU_K0(false, false, false); }
+  switch (collide_mode(p)) {
+    case CM_FAST:
+    case CM_FAST_FOLD: collide_inplace_cm<CM_FAST>(glbm, slab, p, buf, s); break;
+    case CM_EXACT_RHO1: collide_inplace_cm<CM_EXACT_RHO1>(glbm, slab, p, buf, s); break;
+    default: collide_inplace_cm<CM_EXACT>(glbm, slab, p, buf, s);
   }
-#undef PGPU_K0
 }
 
 void launch_macro_fields(bool glbm, const KParams& p, const double* f, double* drho,

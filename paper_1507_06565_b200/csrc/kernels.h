@@ -22,9 +22,10 @@ void launch_sweep(const SweepConfig& cfg, const KParams& p, const double* src, d
                   cudaStream_t s);
 void launch_sweep_compact(const SweepConfig& cfg, const KParams& p, const double* src,
                           double* dst, cudaStream_t s);
-// K0 of the fluid-only layout: dense pre-collision state -> compact post state.
-void launch_collide_to_compact(bool glbm, bool slab, const KParams& p, const double* dense,
-                               double* dst, cudaStream_t s);
+// K0 of the fluid-only layout: dense pre-collision state -> compact post state
+// (with records in math mode fast: folded CLI slots, kparams.h KParams::fast).
+void launch_collide_to_compact(bool glbm, bool slab, bool records, const KParams& p,
+                               const double* dense, double* dst, cudaStream_t s);
 // One cooperative launch running nsteps K1 sweeps (a -> b -> a ...); returns 0
 // on success, -1 if the cooperative launch is not possible.
 int launch_sweep_persistent(const SweepConfig& cfg, const KParams& p, double* a, double* b,

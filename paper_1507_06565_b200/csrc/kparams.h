@@ -38,6 +38,25 @@ struct alignas(8) CellWord {
   int32_t base;  // first link record of the cell
 };
 
+// Constants of the contracted ("fast") TRT collision, math mode
+// PGPU_MATH_FAST (lattice.cuh collide_core_fast / collide_glbm_fast).  The
+// reference's per-pair update (simulation.cpp:180-193)
+//   a' = a - wp(s/2 - feq+) - wm(d/2 - feq-) + fpop,  b' = b - wp(...) + wm(...) - fpop
+// with s = a + b, d = a - b is regrouped as a' = P + M, b' = P - M where
+//   P = hp*s + (kw1*drho + kw2*uu) + C*eu^2,   M = hm*d + D*eu + fpop
+// (per weight class: 0 = axis pairs w = 1/18, 1 = diagonal pairs w = 1/36),
+// and the rest population as f0' = w0*f0 + a0*drho + b0*uu.  Same algebra,
+// FMA-contracted and reassociated: agrees with the reference to rounding
+// (<= 1e-12 relative is the north-star tolerance; tests/test_gpu_fast.py).
+struct FastCoef {
+  double hp, hm;           // (1 - wp)/2, (1 - wm)/2
+  double w0, a0, b0;       // 1 - wp, wp/3, -wp*rho0*1.5/3 (/eq_eps for GLBM)
+  double kw1[2], kw2[2];   // wp*w, -1.5*wp*w*rho0 (/eq_eps)
+  double C[2], D[2];       // 4.5*wp*w*rho0 (/eq_eps), 3*wm*w*rho0
+  double fw[2];            // GLBM: force_pref * w
+  double inv_rho0;
+};
+
 // GLBM per-plane coefficients (simulation.cpp:213-253), evaluated on the host
 // with the reference's operation order so the kernel reproduces it bit for bit.
 struct PlaneCoef {
@@ -56,6 +75,8 @@ struct PlaneCoef {
   // reciprocal), mode 2 general (divide).
   int32_t eq_mode, denom_mode;
   double inv_eq_eps, inv_denom;
+  FastCoef fc;         // math mode PGPU_MATH_FAST
+  double f_inv_denom;  // 1 / denom_lin (fast mode, c_F == 0)
 };
 
 // Everything a sweep kernel needs, passed by value.
@@ -75,6 +96,15 @@ struct KParams {
   int64_t nrec;              // link records (bounds checks of debug builds)
   int32_t fill_sectors;      // write zeros into fill-flagged non-fluid cells
   double wp, wm, rho0, nu, cf;
+  // Math mode PGPU_MATH_FAST: contracted collision (FastCoef) and, in the
+  // fluid-only layout with link records, folded CLI links: the otherwise
+  // unread slot k = opp(j) of a cell with a CLI link in direction j stores
+  // h = g_k(x) - c*g_j(x) instead of g_k(x), so the closure is
+  // f_j = c*g_k(x - e_k) + h and needs no g_j(x) load (records: SBB = 0).
+  int32_t fast;
+  int32_t fold;    // fast mode, fluid-only layout, records present: links folded
+  int32_t moving;  // some link is a moving wall (records hold +inf for it)
+  FastCoef fc;
   double fpop[9];   // core force term ((3*w)*rho0)*eg per pair (simulation.cpp:190)
   double wr3[9];    // (w*rho0)*3 per pair                      (simulation.cpp:185)
   double mw[19];    // moving-wall term 2*w*rho0*3*(e.u_w) per link direction (boundary.cpp:38-40)

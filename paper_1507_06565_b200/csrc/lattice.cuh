@@ -197,4 +197,127 @@ __device__ __forceinline__ void collide_glbm(double (&fk)[19], const KParams& p,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Math mode PGPU_MATH_FAST: the same TRT algebra regrouped and FMA-contracted
+// (kparams.h FastCoef).  Half the fp64 instructions of the literal-order
+// collision; agrees with it to rounding, not bit for bit.
+// ---------------------------------------------------------------------------
+// e.u for pair q (direction k = 2q+1) with the compile-time lattice vector.
+__device__ __forceinline__ double fast_eu(int q, double ux, double uy, double uz) {
+  const int k = 1 + 2 * q;
+  double r = 0.0;
+  bool first = true;
+  auto acc = [&](int e, double v) {
+    if (e == 0) return;
+    if (first) r = e > 0 ? v : -v;
+    else r = e > 0 ? r + v : r - v;
+    first = false;
+  };
+  acc(EX[k], ux);
+  acc(EY[k], uy);
+  acc(EZ[k], uz);
+  return r;
+}
+
+// In place: f[k] <- a + b, f[kb] <- a - b for every pair; returns drho and
+// the momentum (reference moments, simulation.cpp:166-174, reassociated).
+__device__ __forceinline__ void fast_moments(double (&f)[19], double& drho, double& vx, double& vy,
+                                             double& vz) {
+  double s[9], d[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    s[q] = f[1 + 2 * q] + f[2 + 2 * q];
+    d[q] = f[1 + 2 * q] - f[2 + 2 * q];
+    f[1 + 2 * q] = s[q];
+    f[2 + 2 * q] = d[q];
+  }
+  // pairwise sums (shorter dependency chains than the reference's serial sum)
+  drho = ((f[0] + s[0]) + (s[1] + s[2])) + ((s[3] + s[4]) + (s[5] + s[6])) + (s[7] + s[8]);
+  // pairs: 0 (1,0,0) 1 (0,1,0) 2 (0,0,1) 3 (1,1,0) 4 (1,-1,0) 5 (1,0,1) 6 (1,0,-1)
+  //        7 (0,1,1) 8 (0,1,-1)
+  vx = (d[0] + d[3]) + (d[4] + d[5]) + d[6];
+  vy = (d[1] + d[3]) - (d[4] - d[7]) + d[8];
+  vz = (d[2] + d[5]) - (d[6] - d[7]) - d[8];
+}
+
+// Pair updates from s/d in f: a' = P + M, b' = P - M.
+__device__ __forceinline__ void fast_pairs(double (&f)[19], const FastCoef& c, double B0,
+                                           double B1, double ux, double uy, double uz,
+                                           const double (&fpop)[9]) {
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    const int cl = q < 3 ? 0 : 1;
+    const double eu = fast_eu(q, ux, uy, uz);
+    const double P = fma(c.hp, f[1 + 2 * q], fma(c.C[cl], eu * eu, cl ? B1 : B0));
+    const double M = fma(c.hm, f[2 + 2 * q], fma(c.D[cl], eu, fpop[q]));
+    f[1 + 2 * q] = P + M;
+    f[2 + 2 * q] = P - M;
+  }
+}
+
+__device__ __forceinline__ void collide_core_fast(double (&f)[19], const KParams& p) {
+  const FastCoef& c = p.fc;
+  double drho, vx, vy, vz;
+  fast_moments(f, drho, vx, vy, vz);
+  const double ux = vx * c.inv_rho0, uy = vy * c.inv_rho0, uz = vz * c.inv_rho0;
+  const double uu = fma(uz, uz, fma(uy, uy, ux * ux));
+  f[0] = fma(c.w0, f[0], fma(c.a0, drho, c.b0 * uu));
+  const double B0 = fma(c.kw1[0], drho, c.kw2[0] * uu);
+  const double B1 = fma(c.kw1[1], drho, c.kw2[1] * uu);
+  fast_pairs(f, c, B0, B1, ux, uy, uz, p.fpop);
+}
+
+// GLBM (simulation.cpp:198-274) in the same regrouped form; the per-plane
+// constants (incl. 1/eq_eps and the plane's omegas) are in pc.fc.
+__device__ __forceinline__ void collide_glbm_fast(double (&f)[19], const KParams& p, int z) {
+  const PlaneCoef& pc = p.planes[z];
+  const FastCoef& c = pc.fc;
+  double drho, vx, vy, vz;
+  fast_moments(f, drho, vx, vy, vz);
+  const double vhx = fma(vx, c.inv_rho0, pc.half_eps_g[0]);
+  const double vhy = fma(vy, c.inv_rho0, pc.half_eps_g[1]);
+  const double vhz = fma(vz, c.inv_rho0, pc.half_eps_g[2]);
+  double inv, drag;
+  if (p.cf == 0.0) {
+    inv = pc.f_inv_denom;
+  } else {
+    const double vmag = sqrt(fma(vhz, vhz, fma(vhy, vhy, vhx * vhx)));
+    inv = 1.0 / (pc.c0 + sqrt(fma(pc.c1, vmag, pc.c0 * pc.c0)));
+  }
+  const double ux = vhx * inv, uy = vhy * inv, uz = vhz * inv;
+  const double uu = fma(uz, uz, fma(uy, uy, ux * ux));
+  if (p.cf != 0.0)
+    drag = fma(pc.drag_q, sqrt(uu), pc.drag_lin);
+  else
+    drag = pc.drag_lin0;
+  const double Fx = fma(-drag, ux, pc.eps_g[0]);
+  const double Fy = fma(-drag, uy, pc.eps_g[1]);
+  const double Fz = fma(-drag, uz, pc.eps_g[2]);
+  f[0] = fma(c.w0, f[0], fma(c.a0, drho, c.b0 * uu));
+  const double B0 = fma(c.kw1[0], drho, c.kw2[0] * uu);
+  const double B1 = fma(c.kw1[1], drho, c.kw2[1] * uu);
+  double fpop[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) fpop[q] = c.fw[q < 3 ? 0 : 1] * fast_eu(q, Fx, Fy, Fz);
+  fast_pairs(f, c, B0, B1, ux, uy, uz, fpop);
+}
+
+// Collision mode (template parameter CM of the sweep kernels):
+//   0 literal order, general rho0   1 literal order, rho0 == 1   2 fast (any rho0)
+//   3 fast + folded CLI links (fluid-only layout, kparams.h KParams::fold)
+enum CollideMode { CM_EXACT = 0, CM_EXACT_RHO1 = 1, CM_FAST = 2, CM_FAST_FOLD = 3 };
+__host__ __device__ __forceinline__ int collide_mode(const KParams& p) {
+  return p.fast ? (p.fold ? CM_FAST_FOLD : CM_FAST) : (p.rho0 == 1.0 ? CM_EXACT_RHO1 : CM_EXACT);
+}
+template <int CM, bool GLBM>
+__device__ __forceinline__ void collide(double (&f)[19], const KParams& p, int z) {
+  if constexpr (CM >= CM_FAST) {
+    if constexpr (GLBM) collide_glbm_fast(f, p, z);
+    else collide_core_fast(f, p);
+  } else {
+    if constexpr (GLBM) collide_glbm<CM == CM_EXACT_RHO1>(f, p, z);
+    else collide_core<CM == CM_EXACT_RHO1>(f, p);
+  }
+}
+
 }  // namespace pgpu

@@ -186,6 +186,16 @@ __global__ void k_fill_nan(double* __restrict__ recs, int64_t n) {
   if (i < n) recs[i] = __longlong_as_double(0x7FF8000000000000ll);
 }
 
+// Records of the folded-link sweeps (math mode fast): SBB (NaN) -> 0.
+__global__ void k_fold_records(const double* __restrict__ recs, double* __restrict__ out,
+                               int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double r = recs[i];
+    out[i] = r == r ? r : 0.0;
+  }
+}
+
 // simulation.cpp:104-112: links whose wall neighbour lies in plane nz-1 move.
 __global__ void k_mark_lid(const uint32_t* __restrict__ cellw, const int32_t* __restrict__ base,
                            double* __restrict__ recs, int nx, int ny, int nz,
@@ -314,6 +324,12 @@ void fill_records_nan(double* recs, int64_t n, cudaStream_t s) {
   if (n == 0) return;
   k_fill_nan<<<blocks(n, 256), 256, 0, s>>>(recs, n);
   ck(cudaGetLastError(), "k_fill_nan");
+}
+
+void fold_records(const double* recs, double* out, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  k_fold_records<<<blocks(n, 256), 256, 0, s>>>(recs, out, n);
+  ck(cudaGetLastError(), "k_fold_records");
 }
 
 void mark_lid_links(const uint32_t* cellw, const int32_t* base, double* recs, int nx, int ny,

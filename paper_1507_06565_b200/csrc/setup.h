@@ -55,6 +55,8 @@ int64_t setup_bases(const int32_t* count, int32_t* base, int32_t* chunkbase, int
 void setup_links(const LinkSetupArgs& a, uint32_t* seen_bits, unsigned long long* d_err,
                  unsigned long long* d_fallbacks, int* d_moving, cudaStream_t s);
 void fill_records_nan(double* recs, int64_t n, cudaStream_t s);
+// Records of the folded-link sweeps (math mode fast): NaN (SBB) -> 0.
+void fold_records(const double* recs, double* out, int64_t n, cudaStream_t s);
 void mark_lid_links(const uint32_t* cellw, const int32_t* base, double* recs, int nx, int ny,
                     int nz, int* d_any, cudaStream_t s);
 // Fluid-only layout chunk table [rows][nchunk] {rank, mask}; returns the fluid count.

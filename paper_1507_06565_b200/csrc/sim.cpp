@@ -95,6 +95,11 @@ struct pgpu_sim {
   int32_t* d_cellbase = nullptr;
   int32_t* d_chunkbase = nullptr;
   LinkRec* d_recs = nullptr;
+  // math mode PGPU_MATH_FAST: contracted collision; in the fluid-only layout
+  // CLI links are folded (kparams.h KParams::fast) and read d_recs_fold
+  // (the records with SBB = 0)
+  bool fast = false;
+  LinkRec* d_recs_fold = nullptr;
   uint16_t* d_linkdesc = nullptr;  // per record: owner lane | j << 5 (compact CLI sweep)
   PlaneCoef* d_planes = nullptr;
   double* d_feq = nullptr;
@@ -132,6 +137,7 @@ struct pgpu_sim {
     cudaFree(d_cellbase);
     cudaFree(d_chunkbase);
     cudaFree(d_recs);
+    cudaFree(d_recs_fold);
     cudaFree(d_linkdesc);
     cudaFree(d_planes);
     cudaFree(d_feq);
@@ -179,8 +185,48 @@ struct pgpu_sim {
       kp.hg[i] = 0.5 * g[i] / rho0;  // simulation.cpp:367
       kp.g[i] = g[i];
     }
+    kp.fast = fast ? 1 : 0;
+    fill_fast(kp.fc, params.omega_plus, params.omega_minus, rho0, 1.0, 0.0);
     if (porous) upload_planes();
+    update_links();
     drop_graphs();
+  }
+
+  // FastCoef (kparams.h) of a TRT collision with omegas wp/wm; inv_eq =
+  // 1/eq_eps of the GLBM equilibrium (1 for the core collision)
+  static void fill_fast(FastCoef& c, double wp, double wm, double rho0, double inv_eq,
+                        double force_pref) {
+    c.hp = 0.5 * (1.0 - wp);
+    c.hm = 0.5 * (1.0 - wm);
+    c.w0 = 1.0 - wp;
+    c.a0 = wp / 3.0;
+    c.b0 = -0.5 * wp * rho0 * inv_eq;
+    for (int cl = 0; cl < 2; ++cl) {
+      const double w = cl == 0 ? 1.0 / 18.0 : 1.0 / 36.0;
+      c.kw1[cl] = wp * w;
+      c.kw2[cl] = -1.5 * wp * w * rho0 * inv_eq;
+      c.C[cl] = 4.5 * wp * w * rho0 * inv_eq;
+      c.D[cl] = 3.0 * wm * w * rho0;
+      c.fw[cl] = force_pref * w;
+    }
+    c.inv_rho0 = 1.0 / rho0;
+  }
+
+  // PGPU_FOLD=1: fold CLI links in fast mode (measured slower on C4/C3, off by default)
+  bool fold_enabled = false;
+  bool fold_links() const { return fast && fold_enabled && compact && d_recs != nullptr; }
+  // Link records the kernels read: the folded-link sweeps take SBB = 0.
+  void update_links() {
+    kp.moving = any_moving ? 1 : 0;
+    kp.fold = fold_links() ? 1 : 0;
+    if (fold_links()) {
+      if (!d_recs_fold) CK(cudaMalloc(&d_recs_fold, sizeof(LinkRec) * n_links));
+      fold_records(d_recs, d_recs_fold, n_links, stream);
+      CK(cudaGetLastError());
+      kp.links = d_recs_fold;
+    } else {
+      kp.links = d_recs;
+    }
   }
 
   void upload_planes() {
@@ -220,6 +266,8 @@ struct pgpu_sim {
       };
       c.eq_mode = mode_of(c.eq_eps, c.inv_eq_eps);
       c.denom_mode = mode_of(c.denom_lin, c.inv_denom);
+      fill_fast(c.fc, c.wp, c.wm, rho0, 1.0 / c.eq_eps, c.force_pref);
+      c.f_inv_denom = 1.0 / c.denom_lin;
     }
     if (!d_planes) CK(cudaMalloc(&d_planes, sizeof(PlaneCoef) * nz));
     CK(cudaMemcpyAsync(d_planes, pc.data(), sizeof(PlaneCoef) * nz, cudaMemcpyHostToDevice,
@@ -236,8 +284,8 @@ struct pgpu_sim {
     if (d_recs || n_links == 0) return;
     CK(cudaMalloc(&d_recs, sizeof(LinkRec) * n_links));
     fill_records_nan(d_recs, n_links, stream);
-    kp.links = d_recs;
     ensure_linkdesc();
+    update_links();
     kp.nrec = n_links;
     drop_graphs();
   }
@@ -290,7 +338,8 @@ struct pgpu_sim {
   void k0() {
     set_ghost_ptrs();
     if (compact)
-      launch_collide_to_compact(glbm_active, slab, kp, pre, f[cur], stream);
+      launch_collide_to_compact(glbm_active, slab, sweep_cfg(0, 0).records, kp, pre, f[cur],
+                                stream);
     else
       launch_collide_inplace(glbm_active, slab, kp, f[cur], stream);
     check_launch();
@@ -715,6 +764,8 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
                    std::chrono::duration<double, std::milli>(t1 - t0).count());
       t0 = t1;
     };
+    if (const char* e = std::getenv("PGPU_MATH")) s->fast = e[0] == 'f';
+    if (const char* e = std::getenv("PGPU_FOLD")) s->fold_enabled = e[0] == '1';
     const char* fill_env = std::getenv("PGPU_FILL_SECTORS");
     device_setup(s.get(), g, !(fill_env && fill_env[0] == '0'), lap);
 
@@ -829,6 +880,32 @@ int pgpu_get_params(pgpu_sim* sim, pgpu_fluid_params* out) {
   });
 }
 
+// Math mode (not in the reference: the reference has one arithmetic):
+// PGPU_MATH_EXACT reproduces the reference bit for bit, PGPU_MATH_FAST is the
+// contracted collision with folded CLI links (<= 1e-12 relative).  A switch
+// mid-run materialises f(n) first when the stored state's meaning changes.
+int pgpu_set_math_mode(pgpu_sim* sim, int32_t mode) {
+  return guard([&] {
+    SIM_CHECK();
+    if (mode != PGPU_MATH_EXACT && mode != PGPU_MATH_FAST) throw ConfigError("unknown math mode");
+    const bool want = mode == PGPU_MATH_FAST;
+    if (want == sim->fast) return;
+    if (sim->slab && sim->pending) throw ConfigError("split step in progress");
+    if (sim->post && sim->compact && sim->d_recs) sim->ensure_pre();  // folded <-> plain slots
+    sim->sync();
+    sim->fast = want;
+    sim->refresh_params();
+    sim->sync();
+  });
+}
+
+int pgpu_get_math_mode(pgpu_sim* sim, int32_t* mode) {
+  return guard([&] {
+    SIM_CHECK();
+    *mode = sim->fast ? PGPU_MATH_FAST : PGPU_MATH_EXACT;
+  });
+}
+
 int pgpu_set_body_force(pgpu_sim* sim, const double g[3]) {
   return guard([&] {
     SIM_CHECK();
@@ -844,6 +921,12 @@ int pgpu_set_lid_velocity(pgpu_sim* sim, const double u[3]) {
     SIM_CHECK();
     sim->sync();
     for (int i = 0; i < 3; ++i) sim->lid[i] = u[i];
+    // The stored post-collision state g(n-1) still owes the pull
+    // f(n) = P(g(n-1)) with the OLD wall velocity (the reference streamed and
+    // bounced step n before this call, simulation.cpp:325-342): materialise
+    // f(n) first, the next step re-collides from it.  (Also required by the
+    // folded CLI slots of math mode fast.)
+    if (sim->post) sim->ensure_pre();
     sim->ensure_records();  // SBB scheme: all-SBB records first
     if (sim->d_recs) {
       DevBuf any;

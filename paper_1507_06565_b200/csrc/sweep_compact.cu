@@ -156,6 +156,76 @@ __device__ __forceinline__ void clinks_all(double (&f)[19], const double* __rest
   }
 }
 
+// Math mode fast, fluid-only layout with records: folded CLI links (kparams.h
+// KParams::fast).  f[J] holds h (slot k = opp J of the cell); CLI records
+// close f_J = c*g_k(x - e_k) + h; moving walls (+inf, only when p.moving)
+// keep h = g_k(x) unfolded and subtract the wall term exactly like
+// boundary.cpp:34-41; SBB records are 0 (nothing to do).  f[K] of a CLI link
+// is a pull value (x - e_k is fluid), never the target of another closure.
+__device__ __forceinline__ void close_fold(double& fj, double fk, double rec, const KParams& p,
+                                           int k) {
+  if (rec != 0.0) fj = (p.moving && isinf(rec)) ? DSUB(fj, p.mw[k]) : fma(rec, fk, fj);
+}
+template <int J>
+__device__ __forceinline__ void clinks_fold_all(double (&f)[19], const KParams& p, uint32_t w,
+                                                int32_t base) {
+  if constexpr (J < 19) {
+    if ((w >> J) & 1u) {
+      const int32_t r = base + __popc(w & ((1u << J) - 1u) & kBounceMask);
+      close_fold(f[J], f[opp(J)], __ldg(p.links + r), p, opp(J));
+    }
+    clinks_fold_all<J + 1>(f, p, w, base);
+  }
+}
+// Epilogue of a folded sweep: for each link of the cell (bounce bits `bm`, its
+// records rec(0), rec(1), ... in (cell, j) order) store h = g_k - c*g_j in
+// slot k = opp(j) of the new post-collision state.  Both links of a pair read
+// the un-folded values.
+template <class Rec>
+__device__ __forceinline__ void fold_epilogue(double (&f)[19], uint32_t bm, const KParams& p,
+                                              Rec&& rec) {
+  int r = 0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    const int k = 1 + 2 * q, kb = k + 1;
+    const double gk = f[k], gkb = f[kb];
+    if ((bm >> k) & 1u) {  // link closing f_k: its h lives in slot kb
+      const double c = rec(r++);
+      if (!(p.moving && isinf(c))) f[kb] = fma(-c, gk, gkb);
+    }
+    if ((bm >> kb) & 1u) {
+      const double c = rec(r++);
+      if (!(p.moving && isinf(c))) f[k] = fma(-c, gkb, gk);
+    }
+  }
+}
+
+// The same for a warp of the pipelined sweep whose chunk-plane records all sit
+// in the shared-memory pool (no moving walls): `um` = the warp's union of
+// bounce bits (uniform), so directions no lane links are skipped without
+// divergence; the rest is predicated (pool reads past the lane's own records
+// land in the pool and are unused).
+__device__ __forceinline__ void fold_epilogue_pool(double (&f)[19], uint32_t bm, uint32_t um,
+                                                   const double* pool, int r) {
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    const int k = 1 + 2 * q, kb = k + 1;
+    const double gk = f[k], gkb = f[kb];
+    if ((um >> k) & 1u) {
+      const bool b = (bm >> k) & 1u;
+      const double c = pool[r];
+      if (b) f[kb] = fma(-c, gk, gkb);
+      r += b;
+    }
+    if ((um >> kb) & 1u) {
+      const bool b = (bm >> kb) & 1u;
+      const double c = pool[r];
+      if (b) f[k] = fma(-c, gkb, gk);
+      r += b;
+    }
+  }
+}
+
 template <bool SLAB>
 __device__ __forceinline__ void write_sends(const KParams& p, int x, int y, int z,
                                             const double (&f)[19]) {
@@ -178,21 +248,25 @@ __device__ __forceinline__ void write_sends(const KParams& p, int x, int y, int 
   }
 }
 
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __device__ __forceinline__ void csweep_cell(const KParams& p, const double* __restrict__ src,
                                             double* __restrict__ dst, int x, int y, int z) {
   const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
   const uint32_t w = __ldg(p.cellw + c);
   if (w & kNonFluid) return;
   const int64_t fc = fidx(p, x, y, z);
+  constexpr bool FOLD = RECORDS && CM == CM_FAST_FOLD;
   double f[19];
   cload_all<0, SLAB>(f, src, x, y, z, fc, p, w);
-  if (RECORDS && (w & kBounceMask)) clinks_all<1>(f, src, fc, p, w, __ldg(p.cellbase + c));
+  const int32_t base = (RECORDS && (w & kBounceMask)) ? __ldg(p.cellbase + c) : 0;
+  if (RECORDS && (w & kBounceMask)) {
+    if (FOLD) clinks_fold_all<1>(f, p, w, base);
+    else clinks_all<1>(f, src, fc, p, w, base);
+  }
   if (OP == OP_STREAM_COLLIDE) {
-    if (GLBM)
-      collide_glbm<RHO1>(f, p, z);
-    else
-      collide_core<RHO1>(f, p);
+    collide<CM, GLBM>(f, p, z);
+    if (FOLD && (w & kBounceMask))
+      fold_epilogue(f, w & kBounceMask, p, [&](int i) { return __ldg(p.links + base + i); });
 #pragma unroll
     for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + fc, f[j]);
     write_sends<SLAB>(p, x, y, z, f);
@@ -203,17 +277,17 @@ __device__ __forceinline__ void csweep_cell(const KParams& p, const double* __re
 }
 
 // One thread per cell of the box (part ALL / INTERIOR) ...
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(128) k_csweep_cells(const KParams p,
                                                       const double* __restrict__ src,
                                                       double* __restrict__ dst, int part) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= p.nx) return;
   if (part == PART_INTERIOR && in_edge_band(x, p.nx)) return;
-  csweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, blockIdx.y, blockIdx.z);
+  csweep_cell<CM, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, blockIdx.y, blockIdx.z);
 }
 // ... or of the two x edge bands (slab split; grid (2, ceil(ny/4), nz)).
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(128) k_csweep_edges(const KParams p,
                                                       const double* __restrict__ src,
                                                       double* __restrict__ dst) {
@@ -224,11 +298,11 @@ __global__ void __launch_bounds__(128) k_csweep_edges(const KParams p,
   if (xx >= w || y >= p.ny) return;
   const int x = blockIdx.x ? p.nx - w + xx : xx;
   if (blockIdx.x && x < w) return;
-  csweep_cell<RHO1, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z);
+  csweep_cell<CM, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z);
 }
 
 // K0: dense pre-collision f -> compact post-collision g (simulation.cpp:150-274).
-template <bool RHO1, bool GLBM, bool SLAB>
+template <int CM, bool GLBM, bool SLAB, bool FOLD>
 __global__ void __launch_bounds__(128) k_collide_to_compact(const KParams p,
                                                             const double* __restrict__ f0,
                                                             double* __restrict__ dst) {
@@ -236,14 +310,16 @@ __global__ void __launch_bounds__(128) k_collide_to_compact(const KParams p,
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= p.nx) return;
   const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
-  if (__ldg(p.cellw + c) & kNonFluid) return;
+  const uint32_t w = __ldg(p.cellw + c);
+  if (w & kNonFluid) return;
   double f[19];
 #pragma unroll
   for (int j = 0; j < 19; ++j) f[j] = __ldg(f0 + (int64_t)j * p.ksd + c);
-  if (GLBM)
-    collide_glbm<RHO1>(f, p, z);
-  else
-    collide_core<RHO1>(f, p);
+  collide<CM, GLBM>(f, p, z);
+  if (FOLD && (w & kBounceMask)) {
+    const int32_t base = __ldg(p.cellbase + c);
+    fold_epilogue(f, w & kBounceMask, p, [&](int i) { return __ldg(p.links + base + i); });
+  }
   const int64_t fc = fidx(p, x, y, z);
 #pragma unroll
   for (int j = 0; j < 19; ++j) dst[(int64_t)j * p.ks + fc] = f[j];
@@ -357,6 +433,7 @@ constexpr uint32_t kRowEZp = pack_rows(row_ez(0), row_ez(1), row_ez(2), row_ez(3
 __device__ __forceinline__ int rt_row_ey(int r) { return (int)((kRowEYp >> (2 * r)) & 3u) - 1; }
 __device__ __forceinline__ int rt_row_ez(int r) { return (int)((kRowEZp >> (2 * r)) & 3u) - 1; }
 
+__device__ __forceinline__ int opp_rt(int j) { return (j & 1) ? j + 1 : j - 1; }
 __device__ __forceinline__ void bounds_ok(bool ok) {
   if (PGPU_BOUNDS && !ok) __trap();
 }
@@ -386,10 +463,13 @@ struct alignas(16) CMeta {  // one plane, loaded two planes ahead of its issue
                           // 14.rank / 15.rank = first link record of the chunk / the next one
   uint16_t ldesc[kCW][kCLinkCap + 2];  // the chunk's link descriptors (one-stage CLI sweeps)
 };
-template <bool RECORDS>
+// FOLD (folded CLI links, math mode fast): the pool holds only the records,
+// for two planes (by z parity): the epilogue of plane z reads them after the
+// stage has been refilled with plane z+1.
+template <bool RECORDS, bool FOLD>
 struct alignas(16) CSmem {
   static constexpr int S = cp_stages(RECORDS);
-  static constexpr int PW = RECORDS ? kCPool + kCLinkCap : 1;  // doubles per warp and stage
+  static constexpr int PW = FOLD ? 2 * kCLinkCap : (RECORDS ? kCPool + kCLinkCap : 1);
   double main[S][19][kCBXp];
   double pool[S][kCW][PW];
   CLane lane[S][kCBXp];
@@ -425,12 +505,14 @@ __device__ __forceinline__ void cclose_link(double* stage, int owner, int j, dou
   }  // NaN: simple bounce-back, slot j already holds g_k(x)
 }
 
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
     k_sweep_cpipe(const KParams p, const double* __restrict__ src, double* __restrict__ dst,
                   int part, int zper) {
-  using Sm = CSmem<RECORDS>;
+  constexpr bool FOLD = RECORDS && CM == CM_FAST_FOLD;
+  using Sm = CSmem<RECORDS, FOLD>;
   constexpr int kS = Sm::S;
+  static_assert(!FOLD || kS == 1, "folded links: one-stage pipeline");
   // one-stage CLI sweeps take each chunk-plane's link list from the static
   // per-record descriptors (p.linkdesc); two-stage ones build it per plane
   constexpr bool kStaticDesc = RECORDS && kS == 1;
@@ -564,7 +646,14 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
       // descriptors already in the meta slot: no prefix sum, no publish loop
       const int32_t cb = (int32_t)E[14].rank;
       total = (int32_t)E[15].rank - cb;
-      if (total) {
+      if (FOLD && total) {  // records only, contiguous: no descriptors needed here
+        double* pool = S.pool[s][warp] + (z & 1) * kCLinkCap;
+        const int nl = min(total, kCLinkCap);
+        for (int e = lane; e < nl; e += 32) {
+          bounds_ok(cb + e < p.nrec);
+          cpa8(pool + e, p.links + cb + e);
+        }
+      } else if (total) {
         double* pool = S.pool[s][warp];
         const uint16_t* ld = M.ldesc[warp] + (cb & 1);
         const int nl = min(total, kCLinkCap);
@@ -644,7 +733,43 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
     __syncwarp();  // ... and every lane's copies
     if (kStaticDesc && z + 2 < z1) desc_load(ms == 0 ? 2 : ms - 1);  // plane z+2's chunk bases landed
     const CLane li = S.lane[s][tx];
-    if (RECORDS && cnt_cur) {  // link closures of plane z (one-stage sweeps)
+    // folded links: this lane's first record in the chunk-plane's list and the
+    // list base (the epilogue runs after the stage is refilled with plane z+1)
+    int foff = 0;
+    int32_t fcb = 0;
+    uint32_t fum = 0;  // the warp's union of bounce bits
+    if (FOLD && cnt_cur) {  // warp-uniform
+      int tot;
+      const uint32_t lbm = (li.w & kNonFluid) ? 0u : (li.w & kBounceMask);
+      foff = warp_scan_excl(__popc(lbm), lane, &tot);
+      fum = __reduce_or_sync(0xffffffffu, lbm);
+      fcb = S.cbase[s][warp];
+    }
+    const double* const fpool = S.pool[0][warp] + (z & 1) * kCLinkCap;
+    if (FOLD && cnt_cur) {  // folded closures of plane z: f_j = c * (pull of k) + h
+      double* const stage = &S.main[s][0][0];
+      const int ncoop = min(cnt_cur, kCLinkCap);
+      const uint16_t* ld = S.meta[ms].ldesc[warp] + (fcb & 1);
+      for (int e = lane; e < ncoop; e += 32) {
+        const int d = ld[e];
+        const int owner = (tx & ~31) | (d & 31), j = d >> 5, k = opp_rt(j);
+        close_fold(stage[j * kCBXp + owner], stage[k * kCBXp + owner], fpool[e], p, k);
+      }
+      if (cnt_cur > kCLinkCap && !(li.w & kNonFluid)) {  // pool overflow: own links past the cap
+        uint32_t mm = li.w & kBounceMask;
+        int i = foff;
+        while (mm) {
+          const int j = __ffs(mm) - 1;
+          mm &= mm - 1;
+          if (i >= kCLinkCap) {
+            const int k = opp_rt(j);
+            close_fold(stage[j * kCBXp + tx], stage[k * kCBXp + tx], __ldg(p.links + fcb + i), p, k);
+          }
+          ++i;
+        }
+      }
+      __syncwarp();
+    } else if (RECORDS && cnt_cur) {  // link closures of plane z (one-stage sweeps)
       double* const stage = &S.main[s][0][0];
       const double* pool = S.pool[s][warp];
       const int ncoop = min(cnt_cur, kCLinkCap);
@@ -696,10 +821,16 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
     }
     if (fluid) {
       if (OP == OP_STREAM_COLLIDE) {
-        if (GLBM)
-          collide_glbm<RHO1>(f, p, z);
-        else
-          collide_core<RHO1>(f, p);
+        collide<CM, GLBM>(f, p, z);
+        if (FOLD && cnt_cur) {
+          if (cnt_cur <= kCLinkCap && !p.moving)
+            fold_epilogue_pool(f, li.w & kBounceMask, fum, fpool, foff);
+          else
+            fold_epilogue(f, li.w & kBounceMask, p, [&](int i) {
+              const int r = foff + i;
+              return r < kCLinkCap ? fpool[r] : __ldg(p.links + fcb + r);
+            });
+        }
 #pragma unroll
         for (int j = 0; j < 19; ++j) {
           bounds_ok(in_plane(p, li.fc + p.poff[j], j));
@@ -740,15 +871,15 @@ int cpipe_zper(const KParams& p) {
   return std::min(zper, p.nz);
 }
 
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB, int OP>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
                       cudaStream_t s) {
   // the pipelined kernel sweeps the slab edge bands when each band is one chunk
   if (cfg.part == PART_EDGES && (!edge_chunks(p) || g_plain_sweep())) {
-    k_csweep_edges<RHO1, GLBM, RECORDS, SLAB, OP>
+    k_csweep_edges<CM, GLBM, RECORDS, SLAB, OP>
         <<<dim3(2, (p.ny + 3) / 4, p.nz), 128, 0, s>>>(p, src, dst);
   } else if (g_plain_sweep()) {
-    k_csweep_cells<RHO1, GLBM, RECORDS, SLAB, OP><<<ccell_grid(p), ccell_block(p), 0, s>>>(
+    k_csweep_cells<CM, GLBM, RECORDS, SLAB, OP><<<ccell_grid(p), ccell_block(p), 0, s>>>(
         p, src, dst, cfg.part);
   } else {
     const int zper = cpipe_zper(p);
@@ -758,35 +889,55 @@ void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* sr
     if (cfg.part == PART_INTERIOR && edge_chunks(p))
       grid = dim3((unsigned)(((int64_t)p.ny * (p.nchunk - 2) + kCW - 1) / kCW), 1, zg);
     if (grid.x == 0) return;  // nx == 64 slab: everything is edge band
-    constexpr int smem = (int)sizeof(CSmem<RECORDS>) + PGPU_SMEM_PAD;  // pad: L1-capacity experiment
+    constexpr int smem = (int)sizeof(CSmem<RECORDS, RECORDS && CM == CM_FAST_FOLD>) + PGPU_SMEM_PAD;  // pad: L1-capacity experiment
     static bool attr = [] {
-      cudaFuncSetAttribute(k_sweep_cpipe<RHO1, GLBM, RECORDS, SLAB, OP>,
+      cudaFuncSetAttribute(k_sweep_cpipe<CM, GLBM, RECORDS, SLAB, OP>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       return true;
     }();
     (void)attr;
-    k_sweep_cpipe<RHO1, GLBM, RECORDS, SLAB, OP><<<grid, kCBXp, smem, s>>>(p, src, dst, cfg.part,
+    k_sweep_cpipe<CM, GLBM, RECORDS, SLAB, OP><<<grid, kCBXp, smem, s>>>(p, src, dst, cfg.part,
                                                                          zper);
   }
 }
 
-template <bool RHO1, bool GLBM, bool RECORDS, bool SLAB>
+template <int CM, bool GLBM, bool RECORDS, bool SLAB>
 void cdispatch_op(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
                   cudaStream_t s) {
   if (cfg.op == OP_STREAM_COLLIDE)
-    launch_compact_t<RHO1, GLBM, RECORDS, SLAB, OP_STREAM_COLLIDE>(cfg, p, src, dst, s);
-  else  // KP has no collision: one instantiation per records/slab
-    launch_compact_t<true, false, RECORDS, SLAB, OP_STREAM_ONLY>(cfg, p, src, dst, s);
+    launch_compact_t<CM, GLBM, RECORDS, SLAB, OP_STREAM_COLLIDE>(cfg, p, src, dst, s);
+  else  // KP has no collision: one instantiation per records/slab (and link folding)
+    launch_compact_t<(CM == CM_FAST_FOLD && RECORDS) ? CM_FAST_FOLD : CM_EXACT_RHO1, false, RECORDS, SLAB,
+                     OP_STREAM_ONLY>(cfg, p, src, dst, s);
 }
-template <bool RHO1, bool GLBM>
+template <int CM, bool GLBM>
 void cdispatch(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
                cudaStream_t s) {
   if (cfg.records) {
-    if (cfg.slab) cdispatch_op<RHO1, GLBM, true, true>(cfg, p, src, dst, s);
-    else cdispatch_op<RHO1, GLBM, true, false>(cfg, p, src, dst, s);
+    if (cfg.slab) cdispatch_op<CM, GLBM, true, true>(cfg, p, src, dst, s);
+    else cdispatch_op<CM, GLBM, true, false>(cfg, p, src, dst, s);
   } else {
-    if (cfg.slab) cdispatch_op<RHO1, GLBM, false, true>(cfg, p, src, dst, s);
-    else cdispatch_op<RHO1, GLBM, false, false>(cfg, p, src, dst, s);
+    if (cfg.slab) cdispatch_op<CM, GLBM, false, true>(cfg, p, src, dst, s);
+    else cdispatch_op<CM, GLBM, false, false>(cfg, p, src, dst, s);
+  }
+}
+template <int CM>
+void cdispatch_cm(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+                  cudaStream_t s) {
+  if (cfg.glbm) cdispatch<CM, true>(cfg, p, src, dst, s);
+  else cdispatch<CM, false>(cfg, p, src, dst, s);
+}
+
+template <int CM, bool FOLD>
+void collide_to_compact_cm(bool glbm, bool slab, const KParams& p, const double* dense,
+                           double* dst, cudaStream_t s) {
+  const dim3 g = ccell_grid(p), b = ccell_block(p);
+  if (glbm) {
+    if (slab) k_collide_to_compact<CM, true, true, FOLD><<<g, b, 0, s>>>(p, dense, dst);
+    else k_collide_to_compact<CM, true, false, FOLD><<<g, b, 0, s>>>(p, dense, dst);
+  } else {
+    if (slab) k_collide_to_compact<CM, false, true, FOLD><<<g, b, 0, s>>>(p, dense, dst);
+    else k_collide_to_compact<CM, false, false, FOLD><<<g, b, 0, s>>>(p, dense, dst);
   }
 }
 
@@ -794,29 +945,25 @@ void cdispatch(const SweepConfig& cfg, const KParams& p, const double* src, doub
 
 void launch_sweep_compact(const SweepConfig& cfg, const KParams& p, const double* src,
                           double* dst, cudaStream_t s) {
-  const bool rho1 = p.rho0 == 1.0;
-  if (rho1) {
-    if (cfg.glbm) cdispatch<true, true>(cfg, p, src, dst, s);
-    else cdispatch<true, false>(cfg, p, src, dst, s);
-  } else {
-    if (cfg.glbm) cdispatch<false, true>(cfg, p, src, dst, s);
-    else cdispatch<false, false>(cfg, p, src, dst, s);
+  switch (collide_mode(p)) {
+    case CM_FAST: cdispatch_cm<CM_FAST>(cfg, p, src, dst, s); break;
+    case CM_FAST_FOLD: cdispatch_cm<CM_FAST_FOLD>(cfg, p, src, dst, s); break;
+    case CM_EXACT_RHO1: cdispatch_cm<CM_EXACT_RHO1>(cfg, p, src, dst, s); break;
+    default: cdispatch_cm<CM_EXACT>(cfg, p, src, dst, s);
   }
 }
 
-void launch_collide_to_compact(bool glbm, bool slab, const KParams& p, const double* dense,
-                               double* dst, cudaStream_t s) {
-  const dim3 g = ccell_grid(p), b = ccell_block(p);
-  const bool rho1 = p.rho0 == 1.0;
-#define PGPU_K0C(R, G, S) k_collide_to_compact<R, G, S><<<g, b, 0, s>>>(p, dense, dst)
-  if (rho1) {
-    if (glbm) { if (slab) PGPU_K0C(true, true, true); else PGPU_K0C(true, true, false); }
-    else { if (slab) PGPU_K0C(true, false, true); else PGPU_K0C(true, false, false); }
-  } else {
-    if (glbm) { if (slab) PGPU_K0C(false, true, true); else PGPU_K0C(false, true, false); }
-    else { if (slab) PGPU_K0C(false, false, true); else PGPU_K0C(false, false, false); }
+void launch_collide_to_compact(bool glbm, bool slab, bool records, const KParams& p,
+                               const double* dense, double* dst, cudaStream_t s) {
+  switch (collide_mode(p)) {
+    case CM_FAST: collide_to_compact_cm<CM_FAST, false>(glbm, slab, p, dense, dst, s); break;
+    case CM_FAST_FOLD:
+      if (records) collide_to_compact_cm<CM_FAST_FOLD, true>(glbm, slab, p, dense, dst, s);
+      else collide_to_compact_cm<CM_FAST, false>(glbm, slab, p, dense, dst, s);
+      break;
+    case CM_EXACT_RHO1: collide_to_compact_cm<CM_EXACT_RHO1, false>(glbm, slab, p, dense, dst, s); break;
+    default: collide_to_compact_cm<CM_EXACT, false>(glbm, slab, p, dense, dst, s);
   }
-#undef PGPU_K0C
 }
 
 }  // namespace pgpu

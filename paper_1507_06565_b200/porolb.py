@@ -66,6 +66,13 @@ class WallScheme(enum.IntEnum):
     CLI = 1
 
 
+class MathMode(enum.IntEnum):
+    """pgpu_math_mode (include/porolb_gpu.h): EXACT is bit-identical to the
+    reference; FAST is FMA-contracted with folded CLI links (<= 1e-12)."""
+    EXACT = 0
+    FAST = 1
+
+
 class GlbmViscosity(enum.IntEnum):
     Plain = 0
     Rescaled = 1
@@ -466,6 +473,16 @@ class Simulation:
 
     def set_body_force(self, g) -> None:
         _check(lib.pgpu_set_body_force(self._h, _vec3(g)))
+
+    @property
+    def math_mode(self) -> MathMode:
+        m = C.c_int32()
+        _check(lib.pgpu_get_math_mode(self._h, C.byref(m)))
+        return MathMode(m.value)
+
+    @math_mode.setter
+    def math_mode(self, mode) -> None:
+        _check(lib.pgpu_set_math_mode(self._h, int(mode)))
 
     def set_lid_velocity(self, u) -> None:
         _check(lib.pgpu_set_lid_velocity(self._h, _vec3(u)))

@@ -163,6 +163,31 @@ def test_moving_lid(gpu, orc):
     compare_all(sim, o, geom, "lid")
 
 
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_lid_set_mid_run(gpu, orc, scheme):
+    """simulation.cpp:104-112 between steps: step n's streaming and bounce-back
+    already happened with the old wall velocity (the device materialises f(n)
+    before switching).  Spheres touch the lid so CLI links turn moving."""
+    pg = gpu
+    dims = (24, 16, 20)
+    c = np.array([[6.0, 5.0, 17.5], [15.0, 11.0, 18.2], [12.0, 8.0, 5.0]])
+    pack = pg.SpherePack(c, np.array([2.6, 2.2, 3.5]), tuple(float(d) for d in dims))
+    geom = pg.voxelize(pack, dims, (True, True, False), True, True)
+    sim, o = pair(pg, orc, geom, 1.0 / 6.0, 3.0 / 16.0, (1e-6, 0, 0), scheme)
+    sim.step(7)
+    o.step(7)
+    sim.set_lid_velocity((0.01, 0.002, 0.0))
+    o.set_lid_velocity((0.01, 0.002, 0.0))
+    sim.step(20)
+    o.step(20)
+    compare_all(sim, o, geom, "lid mid-run")
+    sim.set_lid_velocity((-0.004, 0.0, 0.001))
+    o.set_lid_velocity((-0.004, 0.0, 0.001))
+    sim.step(17)
+    o.step(17)
+    compare_all(sim, o, geom, "lid changed")
+
+
 @pytest.mark.parametrize("cf,eps_in_eq", [(0.0, True), (0.0, False), (0.3, True)])
 def test_glbm(gpu, orc, cf, eps_in_eq):
     pg = gpu
