@@ -31,6 +31,28 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+
+def physical_cores() -> int:
+    """Physical cores among the CPUs this process may run on (SMT siblings
+    counted once), from /sys topology; falls back to the logical count."""
+    try:
+        cpus = sorted(os.sched_getaffinity(0))
+        seen = set()
+        for c in cpus:
+            f = Path(f"/sys/devices/system/cpu/cpu{c}/topology/thread_siblings_list")
+            seen.add(f.read_text().strip() if f.exists() else str(c))
+        return max(1, len(seen))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+# CPU legs (cpu_baseline, --impl reference): one OpenMP thread per physical
+# core, bound compactly (BASELINE.md §4).  Set before any OpenMP runtime starts.
+CPU_THREADS = physical_cores()
+os.environ.setdefault("OMP_NUM_THREADS", str(CPU_THREADS))
+os.environ.setdefault("OMP_PLACES", "cores")
+os.environ.setdefault("OMP_PROC_BIND", "close")
+
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM_GBS = 6650.0
 BYTES_PER_FLUID_CELL = 304  # 19 fp64 reads + 19 fp64 writes (SURVEY §8d)
@@ -116,85 +138,85 @@ def dist_env():
     return rank, world, local
 
 
-def ncu_traffic(config_name: str):
-    """dram bytes per launch of the hot kernel from the committed ncu capture."""
+def ncu_traffic(config_name: str, math: str, kernel_hash: str):
+    """DRAM bytes per launch of the hot kernel from the committed ncu capture
+    (profiles/ncu_traffic.json), only when it was measured on this kernel
+    build (same kernel_hash, see paper_1507_06565_b200/build.py) and math mode."""
     f = ROOT / "profiles" / "ncu_traffic.json"
     try:
-        d = json.loads(f.read_text())
-        e = d.get(config_name)
-        return None if e is None else float(e["dram_bytes_per_launch"])
-    except Exception:
+        e = json.loads(f.read_text()).get(f"{config_name}|{math}")
+        if e is None or e.get("kernel_hash") != kernel_hash:
+            return None
+        return float(e["dram_bytes_per_launch"])
+    except Exception:  # noqa: BLE001
         return None
+
+
+def config_dict(name, fluid, cells, links, scheme, world, meta):
+    """The `config` of the JSON line, identical in both arms."""
+    return {"workload": name, "fluid_cells": int(fluid), "cells": int(cells),
+            "links": int(links), "scheme": scheme,
+            "l2": "inputs larger than L2 (2 x 19 x cells x 8 B > 126 MB)"
+            if 2 * 19 * 8 * cells > 126e6 else "state L2-resident",
+            "parallelism": f"x-slab{world}" if world > 1 else "single", **meta}
 
 
 # ---------------------------------------------------------------------------
 # CPU reference timing (oracle/_ref: the reference compiled from its sources)
 # ---------------------------------------------------------------------------
-def reference_cpu_run(workload, geom, steps: int, warmup: int):
-    from oracle.oracle import RefLib
-
-    ref = RefLib()
-    threads = ref.set_threads(os.cpu_count() or 1)
-    params = workload.params()
-    sim = ref.simulation(geom, params.nu, params.omega_plus, params.omega_minus,
-                         params.lambda_magic, params.body_force, int(workload.scheme))
-    gp = workload.glbm_params()
-    if gp is not None:
-        sim.set_porous(gp.eps, gp.permeability, gp.omega_plus, gp.omega_minus, 0.0, True)
-    sim.step(warmup)
-    t0 = time.perf_counter()
-    sim.step(steps)
-    dt = time.perf_counter() - t0
-    return geom.fluid_cells * steps / dt / 1e6, threads, dt
-
-
-def reference_cpu_run_bounded(workload, geom, steps: int, warmup: int, budget_s: float = 90.0):
-    """The reference arm: `steps` time steps, capped so the timed part stays
-    within ~budget_s (MLUPS is a rate; the sample is stated in the JSON line).
-    The first warm-up step also sizes the cap."""
-    from oracle.oracle import RefLib
-
-    ref = RefLib()
-    threads = ref.set_threads(os.cpu_count() or 1)
-    params = workload.params()
-    sim = ref.simulation(geom, params.nu, params.omega_plus, params.omega_minus,
-                         params.lambda_magic, params.body_force, int(workload.scheme))
-    gp = workload.glbm_params()
-    if gp is not None:
-        sim.set_porous(gp.eps, gp.permeability, gp.omega_plus, gp.omega_minus, 0.0, True)
-    w = max(1, min(warmup, 3))
+def reference_cpu_sample(sim, fluid_cells: int, budget_s: float, warmup: int = 3,
+                         max_steps: int = 1_000_000):
+    """The one sampler of both CPU legs: `warmup` (>= 3) untimed steps of the
+    reference Simulation::step(), then as many steps as fit in ~budget_s
+    (at most max_steps).  Returns (fluid MLUPS, steps, seconds, warmup)."""
+    w = max(3, int(warmup))
     t0 = time.perf_counter()
     sim.step(w)
     per = (time.perf_counter() - t0) / w
-    n = max(1, min(steps, int(budget_s / max(per, 1e-9))))
+    n = max(1, min(int(max_steps), int(budget_s / max(per, 1e-9))))
     t0 = time.perf_counter()
     sim.step(n)
     dt = time.perf_counter() - t0
-    return geom.fluid_cells * n / dt / 1e6, threads, dt, n, w
+    return fluid_cells * n / dt / 1e6, n, dt, w
+
+
+def cpu_sample_text(name, n, w, dt, threads):
+    return (f"{name}: {n} time steps of the reference Simulation::step() (oracle/_ref, OpenMP "
+            f"{threads} threads = physical cores, OMP_PLACES=cores OMP_PROC_BIND=close) after "
+            f"{w} warm-up steps, {dt:.1f} s")
 
 
 def run_reference_arm(args):
+    """The reference CPU solver on the same workload, built and run with
+    oracle code only (oracle/ref_workloads.py: harness spheres, the oracle
+    voxelizer checked against the reference-made golden geometry, and the
+    reference Simulation from oracle/_ref).  The product library is never
+    loaded in this process."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1507_06565_b200 import configs
+    from oracle import ref_workloads
+    from oracle.oracle import RefLib
 
-    w = configs.ALL[args.config]()
-    geom = w.geometry()  # bit-identical to the reference voxelizer (tests/test_voxelize.py)
-    mlups, threads, dt, n, wu = reference_cpu_run_bounded(w, geom, args.steps, args.warmup)
-    sample = (f"{w.name}: {n} of the requested {args.steps} time steps of the reference "
-              f"Simulation::step() (capped at ~90 s of CPU time) after {wu} warm-up steps, "
-              f"OpenMP {threads} threads, {dt:.1f} s")
+    w, geom, meta = ref_workloads.build(args.config)
+    checked = meta.pop("geometry_checked", None)
+    ref = RefLib()
+    threads = ref.set_threads(CPU_THREADS)
+    sim = ref_workloads.reference_simulation(ref, w, geom)
+    mlups, n, dt, wu = reference_cpu_sample(sim, geom.fluid_cells, args.ref_budget,
+                                            min(max(args.warmup, 3), 10), args.steps)
     line = {
         "metric": "D3Q19 TRT fp64 fluid MLUPS", "value": mlups, "unit": "MLUPS",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / n * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "fluid_cells": geom.fluid_cells, "cells": geom.cells,
-                   "links": geom.n_links, "scheme": w.scheme.name, **w.meta},
+        "config": config_dict(w.name, geom.fluid_cells, geom.cells, geom.n_links, w.scheme, 1,
+                              meta),
         "cpu_baseline": {"value": mlups, "unit": "MLUPS", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": cpu_sample_text(w.name, n, wu, dt, threads)
+                         + f" (of the requested {args.steps}, capped at ~{args.ref_budget:.0f} s)"},
         "e2e": {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "geometry": checked,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -251,10 +273,12 @@ def run_ours(args):
         stepper(args.warmup)
     torch.cuda.synchronize()
     fluid_total = fluid_local
+    links_local = geom.n_links if geom is not None else sim_obj.me.geometry.n_links
+    links_total = links_local
     if dist is not None:
-        t = torch.tensor([fluid_local], dtype=torch.float64, device="cuda")
+        t = torch.tensor([fluid_local, links_local], dtype=torch.float64, device="cuda")
         dist.all_reduce(t)
-        fluid_total = int(t.item())
+        fluid_total, links_total = int(t[0].item()), int(t[1].item())
         dist.barrier()
 
     clocks = ClockSampler(local)
@@ -286,10 +310,11 @@ def run_ours(args):
     peak, peak_src = hbm_peak()
     bytes_per_launch = BYTES_PER_FLUID_CELL * fluid_local
     achieved = bytes_per_launch / (ms_per_step * 1e-3) / 1e9
-    traffic = ncu_traffic(w.name) if world == 1 else None
+    khash = pg.build_info().get("kernel_hash", "unknown")
+    traffic = ncu_traffic(w.name, args.math, khash) if world == 1 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": bytes_per_launch}
+                "algorithmic_bytes_per_launch": bytes_per_launch, "kernel_hash": khash}
 
     # e2e through the public API with host buffers.  The device-resident
     # simulation stays alive meanwhile (52 GB of 180 GB on C4): reallocating
@@ -306,17 +331,29 @@ def run_ours(args):
         del sim_obj
     torch.cuda.empty_cache()
 
+    per_config = None
+    if rank == 0 and world == 1 and not args.force_slab and not args.no_per_config:
+        per_config = per_config_run(pg, configs, args.config, local, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.force_slab:
         try:
-            cpu_steps = args.cpu_steps
-            mlups, threads, dt = reference_cpu_run(w, geom, cpu_steps, 1)
+            from oracle.oracle import RefLib
+
+            ref = RefLib()
+            threads = ref.set_threads(CPU_THREADS)
+            p = w.params()
+            rsim = ref.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.lambda_magic,
+                                  p.body_force, int(w.scheme))
+            gp = w.glbm_params()
+            if gp is not None:
+                rsim.set_porous(gp.eps, gp.permeability, gp.omega_plus, gp.omega_minus, 0.0, True)
+            mlups, n, dt, wu = reference_cpu_sample(rsim, geom.fluid_cells, args.cpu_budget)
+            del rsim
             cpu = {"value": mlups, "unit": "MLUPS", "cores": threads, "kind": "reference",
-                   "sample": f"{w.name}: {cpu_steps} time steps of the reference "
-                             f"Simulation::step() (oracle/_ref, OpenMP) after 1 warm-up step, "
-                             f"{dt:.1f} s"}
+                   "sample": cpu_sample_text(w.name, n, wu, dt, threads)}
         except Exception as exc:  # noqa: BLE001
-            cpu = {"value": None, "unit": "MLUPS", "cores": os.cpu_count(), "kind": "reference",
+            cpu = {"value": None, "unit": "MLUPS", "cores": CPU_THREADS, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
 
     if rank == 0:
@@ -326,22 +363,61 @@ def run_ours(args):
             "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": w.name, "fluid_cells": fluid_total,
-                       "cells": int(np.prod(w.dims)), "scheme": w.scheme.name,
-                       "l2": "inputs larger than L2 (2 x 19 x cells x 8 B >> 126 MB)",
-                       "parallelism": f"x-slab{world}" if (world > 1 or args.force_slab)
-                       else "single", "math": args.math, **w.meta},
+            "config": config_dict(w.name, fluid_total, int(np.prod(w.dims)) if world == 1
+                                  else int(np.prod(w.dims)), links_total, w.scheme.name,
+                                  world if (world > 1 or not args.force_slab) else 1, w.meta),
+            "math": args.math,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
             "total_cell_mlups": int(np.prod(w.dims)) * args.steps / (ms * 1e-3) / 1e6,
+            "per_config": per_config,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def per_config_run(pg, configs, skip, device, peak):
+    """The other BASELINE configs timed in the same process (fluid MLUPS and
+    the 304-B roofline fraction of their hot kernel), each a device-resident
+    run of >= 200 steps (>= ~0.2 s) after 20 warm-up steps."""
+    import torch
+
+    out = {}
+    for key in ("C1", "C2", "C3", "C4", "C5"):
+        if key == skip:
+            continue
+        if key == "C4":
+            continue  # the headline workload (or too large to add to it)
+        w = configs.ALL[key]()
+        geom = w.geometry()
+        sim = configs.make_simulation(w, geom, device=device)
+        stream = torch.cuda.Stream(device=device)
+        sim.set_stream(stream.cuda_stream)
+        sim.step(20)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = 200
+        while True:
+            e0.record(stream)
+            sim.step(steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            if ms > 150.0 or steps >= 20000:
+                break
+            steps *= 4
+        mlups = geom.fluid_cells * steps / (ms * 1e-3) / 1e6
+        gbs = BYTES_PER_FLUID_CELL * geom.fluid_cells * steps / (ms * 1e-3) / 1e9
+        out[key] = {"workload": w.name, "value": mlups, "unit": "MLUPS", "steps": steps,
+                    "ms_per_step": ms / steps, "frac": gbs / peak,
+                    "layout": sim.layout, "fluid_cells": geom.fluid_cells}
+        del sim
+    return out
 
 
 def e2e_run(pg, configs, w, geom, steps, device):
@@ -424,7 +500,11 @@ def main():
                     help="pgpu_math_mode: fast = FMA-contracted collision + folded CLI links "
                          "(<= 1e-12 vs the reference, tests/test_gpu_fast.py); exact = "
                          "bit-identical to the reference")
-    ap.add_argument("--cpu-steps", type=int, default=12)
+    ap.add_argument("--cpu-budget", type=float, default=15.0,
+                    help="seconds of reference steps in the cpu_baseline leg (after 3 warm-ups)")
+    ap.add_argument("--ref-budget", type=float, default=20.0,
+                    help="seconds of reference steps per --impl reference run (after >= 3 warm-ups)")
+    ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-slab", action="store_true",

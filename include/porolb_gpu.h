@@ -168,6 +168,9 @@ typedef struct {
 /* ---- errors / library ---------------------------------------------------- */
 const char* pgpu_last_error(void);
 int pgpu_abi_version(void);
+/* "kernel_hash=<16 hex>": identifies the sweep kernels' build (sources +
+ * nvcc flags); profiles/ncu_traffic.json entries are keyed by it. */
+int pgpu_build_info(char* buf, int32_t cap);
 /* Number of visible CUDA devices (0 without a GPU; never fails). */
 int pgpu_device_count(void);
 
@@ -229,6 +232,9 @@ int pgpu_synchronize(pgpu_sim* sim);
 
 int pgpu_get_params(pgpu_sim* sim, pgpu_fluid_params* out);
 int pgpu_set_math_mode(pgpu_sim* sim, int32_t mode);
+/* PDF layout chosen at creation (PGPU_LAYOUT overrides). */
+enum pgpu_layout { PGPU_LAYOUT_DENSE = 0, PGPU_LAYOUT_FLUID_ONLY = 1, PGPU_LAYOUT_DENSE_PERSISTENT = 2 };
+int pgpu_get_layout(pgpu_sim* sim, int32_t* layout);
 int pgpu_get_math_mode(pgpu_sim* sim, int32_t* mode);
 int pgpu_set_body_force(pgpu_sim* sim, const double g[3]);
 int pgpu_set_lid_velocity(pgpu_sim* sim, const double u[3]);

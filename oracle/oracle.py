@@ -470,6 +470,10 @@ class OracleLib:
         L.orc_voxelize.argtypes = [i64, P(f64), P(f64), P(f64), P(f64), P(f64), f64, P(C.c_int),
                                    P(C.c_int), C.c_int, C.c_int, f64, P(u8), P(f64), i64, P(i64),
                                    P(i64), P(i32), P(f32), P(u8), P(i64), P(i64), P(C.c_int)]
+        L.orc_voxelize_fast.argtypes = L.orc_voxelize.argtypes
+        L.orc_generate_spheres.argtypes = [C.c_int, C.c_uint64, P(f64), f64, f64, f64, f64, f64,
+                                           f64, i64, i64, P(f64), P(f64), P(f64), P(f64), P(i64),
+                                           P(f64)]
         L.orc_tables.argtypes = [P(C.c_int), P(f64), P(C.c_int)]
 
     def tables(self):
@@ -555,6 +559,52 @@ class OracleLib:
                      ls[:n].copy(), ld[:n].copy(), lq[:n].copy(), lm[:n].copy(), por, fl.value,
                      qfb.value, 1.0 if wall_lo else None,
                      float(dims[2] - 1) if wall_hi else None)
+
+    def voxelize_fast(self, centers, radii, box, dims, periodic=(True, True, False),
+                      wall_lo=False, wall_hi=False, plate_z=0.0, q_clamp_min=0.05) -> OGeom:
+        """orc_voxelize_fast: grid-accelerated, OpenMP; byte-identical output."""
+        cols, r = _pack_arrays(centers, radii)
+        cells = int(np.prod(dims))
+        flags = np.zeros(cells, dtype=np.uint8)
+        por = np.zeros(dims[2])
+        nl, fl, qfb = C.c_int64(), C.c_int64(), C.c_int()
+        cap = 0
+        for _ in range(2):  # first call sizes the link arrays (status 6)
+            lf = np.zeros(cap, dtype=np.int64)
+            ls = np.zeros(cap, dtype=np.int64)
+            ld = np.zeros(cap, dtype=np.int32)
+            lq = np.zeros(cap, dtype=np.float32)
+            lm = np.zeros(cap, dtype=np.uint8)
+            st = self.lib.orc_voxelize_fast(
+                r.size, _p(cols[0], f64), _p(cols[1], f64), _p(cols[2], f64), _p(r, f64),
+                _v3(box), plate_z, _i3(dims), _i3(periodic), int(wall_lo), int(wall_hi),
+                q_clamp_min, _p(flags, u8), _p(por, f64), cap, _p(lf, i64), _p(ls, i64),
+                _p(ld, i32), _p(lq, f32), _p(lm, u8), C.byref(nl), C.byref(fl), C.byref(qfb))
+            if st == 6 and cap == 0:
+                cap = nl.value
+                continue
+            break
+        if st:
+            raise OracleError(st, "voxelize_fast")
+        n = nl.value
+        return OGeom(tuple(dims), tuple(bool(p) for p in periodic), flags, lf[:n], ls[:n],
+                     ld[:n], lq[:n], lm[:n], por, fl.value, qfb.value,
+                     1.0 if wall_lo else None, float(dims[2] - 1) if wall_hi else None)
+
+    def generate_spheres(self, mode, seed, box, z_lo, z_hi, r_min, r_max, bed_volume,
+                         target_porosity, max_attempts, capacity):
+        """Harness sphere generator (mode 0 RSA, 1 Boolean); returns
+        (centers (n, 3), radii (n,), analytic porosity)."""
+        cx, cy, cz, r = (np.zeros(capacity) for _ in range(4))
+        n, por = C.c_int64(), C.c_double()
+        st = self.lib.orc_generate_spheres(int(mode), int(seed), _v3(box), z_lo, z_hi, r_min,
+                                           r_max, bed_volume, target_porosity, int(max_attempts),
+                                           int(capacity), _p(cx, f64), _p(cy, f64), _p(cz, f64),
+                                           _p(r, f64), C.byref(n), C.byref(por))
+        if st:
+            raise OracleError(st, "generate_spheres")
+        k = n.value
+        return np.c_[cx[:k], cy[:k], cz[:k]], r[:k].copy(), por.value
 
     def simulation(self, geom, nu, wp, wm, g, scheme, rho0=1.0) -> "OracleSim":
         return OracleSim(self, geom, nu, wp, wm, g, scheme, rho0)

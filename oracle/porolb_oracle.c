@@ -675,3 +675,357 @@ int orc_voxelize(int64_t n_sph, const double* cx, const double* cy, const double
   free(sph);
   return 0;
 }
+
+/* -------------------------------------------------------------------------
+ * Harness sphere generator (the reference ships none that reaches the
+ * BASELINE porosities): the same seeded recipe as the product's
+ * synthetic generator (random sequential addition without overlap, mode 0,
+ * or Boolean model, mode 1), restated here so that the reference arm of
+ * bench.py builds its workload without the product.  Randomness follows the
+ * reference convention: std::mt19937_64 + uniform01 = (rng() >> 11) * 2^-53
+ * (geometry.cpp:19-21), four draws per attempt in the order x, y, z, r.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  uint64_t mt[312];
+  int mti;
+} orc_mt64;
+
+static void mt64_seed(orc_mt64* s, uint64_t seed) {
+  s->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    s->mt[i] = 6364136223846793005ULL * (s->mt[i - 1] ^ (s->mt[i - 1] >> 62)) + (uint64_t)i;
+  s->mti = 312;
+}
+
+static uint64_t mt64_next(orc_mt64* s) {
+  static const uint64_t mag[2] = {0ULL, 0xB5026F5AA96619E9ULL};
+  const uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL;
+  if (s->mti >= 312) {
+    int i;
+    uint64_t x;
+    for (i = 0; i < 312 - 156; ++i) {
+      x = (s->mt[i] & UM) | (s->mt[i + 1] & LM);
+      s->mt[i] = s->mt[i + 156] ^ (x >> 1) ^ mag[(int)(x & 1ULL)];
+    }
+    for (; i < 311; ++i) {
+      x = (s->mt[i] & UM) | (s->mt[i + 1] & LM);
+      s->mt[i] = s->mt[i + (156 - 312)] ^ (x >> 1) ^ mag[(int)(x & 1ULL)];
+    }
+    x = (s->mt[311] & UM) | (s->mt[0] & LM);
+    s->mt[311] = s->mt[155] ^ (x >> 1) ^ mag[(int)(x & 1ULL)];
+    s->mti = 0;
+  }
+  uint64_t x = s->mt[s->mti++];
+  x ^= (x >> 29) & 0x5555555555555555ULL;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+  x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+  x ^= (x >> 43);
+  return x;
+}
+
+static double mt64_u01(orc_mt64* s) { return (double)(mt64_next(s) >> 11) * 0x1.0p-53; }
+
+/* Returns 0 ok, 1 bad arguments, 6 capacity exceeded. */
+int orc_generate_spheres(int mode, uint64_t seed, const double box[3], double z_lo, double z_hi,
+                         double r_min, double r_max, double bed_volume, double target_porosity,
+                         int64_t max_attempts, int64_t capacity, double* cx, double* cy,
+                         double* cz, double* r, int64_t* n_out, double* porosity_out) {
+  if (!(r_min > 0.0 && r_max >= r_min) || !(bed_volume > 0.0) || (mode != 0 && mode != 1))
+    return 1;
+  orc_mt64* rng = (orc_mt64*)malloc(sizeof(orc_mt64));
+  mt64_seed(rng, seed);
+  const double lx = box[0], ly = box[1], h = 2.0 * r_max;
+  int gx = (int)floor(lx / h); if (gx < 1) gx = 1;
+  int gy = (int)floor(ly / h); if (gy < 1) gy = 1;
+  int gz = (int)ceil((z_hi - z_lo) / h) + 1; if (gz < 1) gz = 1;
+  const double hx = lx / gx, hy = ly / gy;
+  /* RSA neighbour grid: per-bin singly linked lists (head[bin], next[sphere]) */
+  int32_t* head = NULL;
+  int32_t* next = NULL;
+  if (mode == 0) {
+    head = (int32_t*)malloc(sizeof(int32_t) * (size_t)gx * gy * gz);
+    for (int64_t i = 0; i < (int64_t)gx * gy * gz; ++i) head[i] = -1;
+    next = (int32_t*)malloc(sizeof(int32_t) * (size_t)(capacity > 0 ? capacity : 1));
+  }
+  int64_t n = 0;
+  double vol = 0.0, poro = 1.0;
+  int st = 0;
+  const double kPi = 3.14159265358979323846;
+  for (int64_t a = 0; a < max_attempts; ++a) {
+    const double x = mt64_u01(rng) * lx;
+    const double y = mt64_u01(rng) * ly;
+    const double z = z_lo + mt64_u01(rng) * (z_hi - z_lo);
+    const double rr = r_min + mt64_u01(rng) * (r_max - r_min);
+    int bin = 0;
+    if (mode == 0) {
+      int ix = (int)floor(x / hx), iy = (int)floor(y / hy), iz = (int)floor((z - z_lo) / h);
+      ix = ix < 0 ? 0 : (ix > gx - 1 ? gx - 1 : ix);
+      iy = iy < 0 ? 0 : (iy > gy - 1 ? gy - 1 : iy);
+      iz = iz < 0 ? 0 : (iz > gz - 1 ? gz - 1 : iz);
+      int ok = 1;
+      for (int dz = -1; dz <= 1 && ok; ++dz) {
+        const int zz = iz + dz;
+        if (zz < 0 || zz >= gz) continue;
+        for (int dy = -1; dy <= 1 && ok; ++dy) {
+          const int yy = ((iy + dy) % gy + gy) % gy;
+          for (int dx = -1; dx <= 1 && ok; ++dx) {
+            const int xx = ((ix + dx) % gx + gx) % gx;
+            for (int32_t j = head[((int64_t)zz * gy + yy) * gx + xx]; j >= 0; j = next[j]) {
+              double ddx = fabs(x - cx[j]), ddy = fabs(y - cy[j]);
+              ddx = ddx < lx - ddx ? ddx : lx - ddx; /* minimum image */
+              ddy = ddy < ly - ddy ? ddy : ly - ddy;
+              const double ddz = z - cz[j], rs = rr + r[j];
+              if (ddx * ddx + ddy * ddy + ddz * ddz < rs * rs) {
+                ok = 0;
+                break;
+              }
+            }
+          }
+        }
+      }
+      if (!ok) continue;
+      bin = (iz * gy + iy) * gx + ix;
+    }
+    if (n >= capacity) {
+      st = 6;
+      break;
+    }
+    if (mode == 0) {
+      next[n] = head[bin];
+      head[bin] = (int32_t)n;
+    }
+    cx[n] = x;
+    cy[n] = y;
+    cz[n] = z;
+    r[n] = rr;
+    ++n;
+    vol += 4.0 / 3.0 * kPi * rr * rr * rr;
+    poro = (mode == 0) ? 1.0 - vol / bed_volume : exp(-vol / bed_volume);
+    if (poro <= target_porosity) break;
+  }
+  free(head);
+  free(next);
+  free(rng);
+  *n_out = n;
+  *porosity_out = poro;
+  return st;
+}
+
+/* -------------------------------------------------------------------------
+ * orc_voxelize_fast: the same voxelizer (geometry.cpp:442-632), with the
+ * link q search restricted to the sphere images binned in a uniform grid by
+ * their +-(r+2) reject boxes, and planes processed on all OpenMP threads.
+ * min() over the candidates is order-independent and the reject test is the
+ * reference's own comparison, so the output equals orc_voxelize (and the
+ * reference's) byte for byte (tests/test_oracle.py).  Needed for
+ * the C4 workload (the brute-force scan takes about an hour there).
+ * ------------------------------------------------------------------------- */
+int orc_voxelize_fast(int64_t n_sph, const double* cx, const double* cy, const double* cz,
+                      const double* cr, const double box[3], double plate_z, const int dims[3],
+                      const int periodic[3], int wall_lo, int wall_hi, double q_clamp_min,
+                      uint8_t* flags, double* porosity, int64_t cap, int64_t* lf, int64_t* ls,
+                      int32_t* ld, float* lq, uint8_t* lm, int64_t* n_links_out,
+                      int64_t* fluid_out, int* q_fallback_out) {
+  orc_init();
+  const int nx = dims[0], ny = dims[1], nz = dims[2];
+  if (nx <= 0 || ny <= 0 || nz <= 0) return 1;
+  const int64_t cells = (int64_t)nx * ny * nz;
+#define IDX(x, y, z) ((((int64_t)(z)) * ny + (y)) * nx + (x))
+  const int ixm = periodic[0] ? 1 : 0, iym = periodic[1] ? 1 : 0;
+  osphere* sph = (osphere*)malloc(sizeof(osphere) * (size_t)(n_sph * 9 + 1));
+  int64_t ns = 0;
+  for (int64_t i = 0; i < n_sph; ++i)
+    for (int ix = -ixm; ix <= ixm; ++ix)
+      for (int iy = -iym; iy <= iym; ++iy) {
+        osphere s;
+        s.c[0] = cx[i] + ix * box[0];
+        s.c[1] = cy[i] + iy * box[1];
+        s.c[2] = cz[i];
+        s.r = cr[i];
+        if (s.c[0] + s.r < 0.0 || s.c[0] - s.r > nx || s.c[1] + s.r < 0.0 || s.c[1] - s.r > ny)
+          continue;
+        sph[ns++] = s;
+      }
+  /* per-plane lists of the images whose rasterization box covers the plane */
+  int64_t* zcount = (int64_t*)calloc((size_t)nz + 1, sizeof(int64_t));
+  for (int64_t i = 0; i < ns; ++i) {
+    int z0 = (int)floor(sph[i].c[2] - sph[i].r - 0.5); if (z0 < 0) z0 = 0;
+    int z1 = (int)ceil(sph[i].c[2] + sph[i].r); if (z1 > nz - 1) z1 = nz - 1;
+    for (int z = z0; z <= z1; ++z) ++zcount[z + 1];
+  }
+  for (int z = 0; z < nz; ++z) zcount[z + 1] += zcount[z];
+  int64_t* zfill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nz + 1));
+  memcpy(zfill, zcount, sizeof(int64_t) * (size_t)(nz + 1));
+  int64_t* zlist = (int64_t*)malloc(sizeof(int64_t) * (size_t)(zcount[nz] + 1));
+  for (int64_t i = 0; i < ns; ++i) {
+    int z0 = (int)floor(sph[i].c[2] - sph[i].r - 0.5); if (z0 < 0) z0 = 0;
+    int z1 = (int)ceil(sph[i].c[2] + sph[i].r); if (z1 > nz - 1) z1 = nz - 1;
+    for (int z = z0; z <= z1; ++z) zlist[zfill[z]++] = i;
+  }
+  const int kplate = plate_z > 0.0 ? (int)floor(plate_z - 0.5) : -1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int z = 0; z < nz; ++z) {
+    uint8_t* fz = flags + (int64_t)z * nx * ny;
+    memset(fz, 0, (size_t)nx * ny);
+    if (z <= kplate) memset(fz, 1, (size_t)nx * ny); /* geometry.cpp:501-510 */
+    for (int64_t t = zcount[z]; t < zcount[z + 1]; ++t) { /* geometry.cpp:512-533 */
+      const osphere* s = &sph[zlist[t]];
+      int x0 = (int)floor(s->c[0] - s->r - 0.5); if (x0 < 0) x0 = 0;
+      int x1 = (int)ceil(s->c[0] + s->r); if (x1 > nx - 1) x1 = nx - 1;
+      int y0 = (int)floor(s->c[1] - s->r - 0.5); if (y0 < 0) y0 = 0;
+      int y1 = (int)ceil(s->c[1] + s->r); if (y1 > ny - 1) y1 = ny - 1;
+      const double r2 = s->r * s->r, dz = z + 0.5 - s->c[2];
+      for (int y = y0; y <= y1; ++y)
+        for (int x = x0; x <= x1; ++x) {
+          const double dx = x + 0.5 - s->c[0], dy = y + 0.5 - s->c[1];
+          if (dx * dx + dy * dy + dz * dz < r2) fz[(int64_t)y * nx + x] = 1;
+        }
+    }
+    if ((wall_lo && z == 0) || (wall_hi && z == nz - 1)) memset(fz, 2, (size_t)nx * ny);
+  }
+  free(zlist);
+  free(zfill);
+  free(zcount);
+  double planes[2];
+  int nplanes = 0;
+  if (wall_lo) planes[nplanes++] = 1.0;
+  if (wall_hi) planes[nplanes++] = (double)(nz - 1);
+  int64_t fluid_total = 0;
+  int64_t* plinks = (int64_t*)calloc((size_t)nz + 1, sizeof(int64_t));
+  int open_face = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : fluid_total) reduction(| : open_face)
+  for (int z = 0; z < nz; ++z) { /* porosity (geometry.cpp:553-565) + link counts */
+    int64_t fl = 0, nl = 0;
+    for (int y = 0; y < ny; ++y)
+      for (int x = 0; x < nx; ++x) {
+        if (flags[IDX(x, y, z)] != 0) continue;
+        ++fl;
+        for (int k = 1; k < Q; ++k) {
+          const int xn = wrap_coord(x + ORC_E[k][0], nx, periodic[0]);
+          const int yn = wrap_coord(y + ORC_E[k][1], ny, periodic[1]);
+          const int zn = wrap_coord(z + ORC_E[k][2], nz, periodic[2]);
+          if (xn < 0 || yn < 0 || zn < 0) {
+            open_face = 1;
+            continue;
+          }
+          if (flags[IDX(xn, yn, zn)] != 0) ++nl;
+        }
+      }
+    porosity[z] = (double)fl / ((double)nx * ny);
+    fluid_total += fl;
+    plinks[z + 1] = nl;
+  }
+  *fluid_out = fluid_total;
+  *n_links_out = 0;
+  *q_fallback_out = 0;
+  if (fluid_total == 0 || open_face) {
+    free(plinks);
+    free(sph);
+    return fluid_total == 0 ? 3 : 1;
+  }
+  for (int z = 0; z < nz; ++z) plinks[z + 1] += plinks[z];
+  if (plinks[nz] > cap) { /* capacity: *n_links_out = the count needed */
+    *n_links_out = plinks[nz];
+    free(plinks);
+    free(sph);
+    return 6;
+  }
+  /* uniform grid of the images' reject boxes [c - r - 2, c + r + 2] */
+  const int B = 8;
+  const int gx = (nx + B - 1) / B, gy = (ny + B - 1) / B, gz = (nz + B - 1) / B;
+  const int64_t nb = (int64_t)gx * gy * gz;
+  int64_t* bcount = (int64_t*)calloc((size_t)nb + 1, sizeof(int64_t));
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t* bfill = NULL;
+    int64_t* blist = NULL;
+    if (pass == 1) {
+      for (int64_t b = 0; b < nb; ++b) bcount[b + 1] += bcount[b];
+      bfill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nb + 1));
+      memcpy(bfill, bcount, sizeof(int64_t) * (size_t)(nb + 1));
+      blist = (int64_t*)malloc(sizeof(int64_t) * (size_t)(bcount[nb] + 1));
+    }
+    for (int64_t i = 0; i < ns; ++i) {
+      const osphere* s = &sph[i];
+      int lo[3], hi[3];
+      const int n3[3] = {gx, gy, gz};
+      int empty = 0;
+      for (int a = 0; a < 3; ++a) {
+        /* cell centres p with c - r - 2 <= p <= c + r + 2 (+1 cell of slack) */
+        lo[a] = (int)floor((s->c[a] - s->r - 3.0) / B);
+        hi[a] = (int)floor((s->c[a] + s->r + 3.0) / B);
+        if (lo[a] < 0) lo[a] = 0;
+        if (hi[a] > n3[a] - 1) hi[a] = n3[a] - 1;
+        if (lo[a] > hi[a]) empty = 1;
+      }
+      if (empty) continue;
+      for (int bz = lo[2]; bz <= hi[2]; ++bz)
+        for (int by = lo[1]; by <= hi[1]; ++by)
+          for (int bx = lo[0]; bx <= hi[0]; ++bx) {
+            const int64_t b = ((int64_t)bz * gy + by) * gx + bx;
+            if (pass == 0) ++bcount[b + 1];
+            else blist[bfill[b]++] = i;
+          }
+    }
+    if (pass == 1) {
+      free(bfill);
+      int qfb = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : qfb)
+      for (int z = 0; z < nz; ++z) { /* links, geometry.cpp:567-631, (cell, k) order */
+        int64_t nl = plinks[z];
+        for (int y = 0; y < ny; ++y)
+          for (int x = 0; x < nx; ++x) {
+            const int64_t cell = IDX(x, y, z);
+            if (flags[cell] != 0) continue;
+            const int64_t b = ((int64_t)(z / B) * gy + y / B) * gx + x / B;
+            for (int k = 1; k < Q; ++k) {
+              const int xn = wrap_coord(x + ORC_E[k][0], nx, periodic[0]);
+              const int yn = wrap_coord(y + ORC_E[k][1], ny, periodic[1]);
+              const int zn = wrap_coord(z + ORC_E[k][2], nz, periodic[2]);
+              if (flags[IDX(xn, yn, zn)] == 0) continue;
+              const int kb = ORC_OPP[k];
+              int64_t second = -1;
+              const int xp = wrap_coord(x + ORC_E[kb][0], nx, periodic[0]);
+              const int yp = wrap_coord(y + ORC_E[kb][1], ny, periodic[1]);
+              const int zp = wrap_coord(z + ORC_E[kb][2], nz, periodic[2]);
+              if (xp >= 0 && yp >= 0 && zp >= 0) {
+                const int64_t pc = IDX(xp, yp, zp);
+                if (flags[pc] == 0) second = pc;
+              }
+              const double pc3[3] = {x + 0.5, y + 0.5, z + 0.5};
+              double q = INFINITY, t;
+              for (int64_t u = bcount[b]; u < bcount[b + 1]; ++u) {
+                const osphere* s = &sph[blist[u]];
+                if (pc3[0] < s->c[0] - s->r - 2.0 || pc3[0] > s->c[0] + s->r + 2.0 ||
+                    pc3[1] < s->c[1] - s->r - 2.0 || pc3[1] > s->c[1] + s->r + 2.0 ||
+                    pc3[2] < s->c[2] - s->r - 2.0 || pc3[2] > s->c[2] + s->r + 2.0)
+                  continue;
+                if (ray_sphere(pc3, ORC_E[k], s, &t) && t < q) q = t;
+              }
+              if (plate_z > 0.0 && ray_plane_z(pc3, ORC_E[k], plate_z, &t) && t < q) q = t;
+              for (int i = 0; i < nplanes; ++i)
+                if (ray_plane_z(pc3, ORC_E[k], planes[i], &t) && t < q) q = t;
+              if (!isfinite(q)) {
+                q = 0.5;
+                ++qfb;
+              }
+              const double qc = q < q_clamp_min ? q_clamp_min : (1.0 < q ? 1.0 : q);
+              lf[nl] = cell;
+              ls[nl] = second;
+              ld[nl] = k;
+              lq[nl] = (float)qc;
+              lm[nl] = 0;
+              ++nl;
+            }
+          }
+      }
+      *q_fallback_out = qfb;
+      free(blist);
+    }
+  }
+#undef IDX
+  *n_links_out = plinks[nz];
+  free(bcount);
+  free(plinks);
+  free(sph);
+  return 0;
+}

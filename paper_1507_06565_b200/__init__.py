@@ -23,6 +23,7 @@ from .porolb import (  # noqa: F401
     SpherePack,
     VoxelGeometry,
     WallScheme,
+    build_info,
     device_count,
     equilibrium,
     generate_spheres,

@@ -63,6 +63,7 @@ class VoxelizeOptionsC(C.Structure):
 SIGNATURES = {
     "pgpu_last_error": (C.c_char_p, []),
     "pgpu_abi_version": (C.c_int, []),
+    "pgpu_build_info": (C.c_int, [C.c_char_p, i32]),
     "pgpu_device_count": (C.c_int, []),
     "pgpu_relaxation_from_magic": (C.c_int, [f64, f64, P(FluidParams)]),
     "pgpu_equilibrium": (C.c_int, [f64, P(f64), f64, P(f64)]),
@@ -88,6 +89,7 @@ SIGNATURES = {
     "pgpu_synchronize": (C.c_int, [vp]),
     "pgpu_get_params": (C.c_int, [vp, P(FluidParams)]),
     "pgpu_set_math_mode": (C.c_int, [vp, i32]),
+    "pgpu_get_layout": (C.c_int, [vp, P(i32)]),
     "pgpu_get_math_mode": (C.c_int, [vp, P(i32)]),
     "pgpu_set_body_force": (C.c_int, [vp, P(f64)]),
     "pgpu_set_lid_velocity": (C.c_int, [vp, P(f64)]),

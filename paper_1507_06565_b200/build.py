@@ -48,6 +48,27 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+KERNEL_FLAGS = ["-O3", "-lineinfo", "-std=c++17"]
+
+
+def kernel_hash(defines: tuple = ()) -> str:
+    """sha256 (16 hex) of everything that determines the sweep kernels' code:
+    the CUDA sources and headers, nvcc flags/defines and nvcc's version.  It is
+    compiled into the library (pgpu_build_info) so bench.py reports a
+    committed ncu traffic figure only for the kernel build it was measured on."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in CU_SOURCES + [x for x in HEADERS if not x.endswith(".h") or x in ("kparams.h", "kernels.h")]:
+        h.update(f.encode())
+        h.update((CSRC / f).read_bytes())
+    h.update(" ".join(GENCODE + KERNEL_FLAGS + list(defines)).encode())
+    try:
+        h.update(subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.encode())
+    except OSError:
+        pass
+    return h.hexdigest()[:16]
+
+
 def build_product(force: bool = False, defines: tuple = (), lib: Path = LIB,
                   obj: Path = OBJ) -> Path:
     """Compile and link the product library.  `defines` (e.g. ("PGPU_POOL=64",))
@@ -56,6 +77,7 @@ def build_product(force: bool = False, defines: tuple = (), lib: Path = LIB,
     LIB = lib
     OBJ.mkdir(parents=True, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
+    khash = kernel_hash(defines)
     hdrs = [CSRC / h for h in HEADERS] + [ROOT / "include" / "porolb_gpu.h"]
     jobs = []
     objs = []
@@ -63,18 +85,22 @@ def build_product(force: bool = False, defines: tuple = (), lib: Path = LIB,
         o = OBJ / (Path(src).stem + ".o")
         objs.append(o)
         if force or _stale(o, [CSRC / src] + hdrs):
-            jobs.append([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            jobs.append([NVCC, *GENCODE, *KERNEL_FLAGS, "-Xcompiler", "-fPIC",
                          "-Xptxas", "-warn-spills", *dflags, "-c", str(CSRC / src), "-o", str(o)])
+    stamp = OBJ / "kernel_hash.txt"
+    hash_changed = not stamp.exists() or stamp.read_text() != khash
     for src in CPP_SOURCES:
         o = OBJ / (Path(src).stem + ".o")
         objs.append(o)
-        if force or _stale(o, [CSRC / src] + hdrs):
+        if force or _stale(o, [CSRC / src] + hdrs) or (src == "params.cpp" and hash_changed):
             jobs.append([CXX, "-std=c++17", "-O3", "-fPIC", "-pthread", "-ffp-contract=off",
-                         "-Wall", "-Wno-unused-function", f"-I{CUDA_INC}", *dflags, "-c",
+                         "-Wall", "-Wno-unused-function", f"-I{CUDA_INC}", *dflags,
+                         f'-DPGPU_KERNEL_HASH="{khash}"', "-c",
                          str(CSRC / src), "-o", str(o)])
     if jobs:
         with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
             list(ex.map(_run, jobs))
+    stamp.write_text(khash)
     if force or jobs or _stale(LIB, objs):
         _run([NVCC, *GENCODE, "-shared", "-cudart", "static", "-o", str(LIB),
               *[str(o) for o in objs], "-Xcompiler", "-pthread"])

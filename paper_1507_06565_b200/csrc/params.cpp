@@ -1,5 +1,6 @@
 // Lattice-level host functions of the drop-in API.  Same formulas and
 // operation order as the reference (cited per function); -ffp-contract=off.
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -84,6 +85,18 @@ extern "C" {
 
 const char* pgpu_last_error(void) { return g_last_error.c_str(); }
 int pgpu_abi_version(void) { return PGPU_ABI_VERSION; }
+
+#ifndef PGPU_KERNEL_HASH
+#define PGPU_KERNEL_HASH "unknown"
+#endif
+// "kernel_hash=<16 hex>": sha256 of the sweep kernels' sources + nvcc flags
+// (paper_1507_06565_b200/build.py kernel_hash); keys profiles/ncu_traffic.json.
+int pgpu_build_info(char* buf, int32_t cap) {
+  return guard([&] {
+    if (!buf || cap <= 0) throw std::invalid_argument("null buffer");
+    std::snprintf(buf, (size_t)cap, "kernel_hash=%s", PGPU_KERNEL_HASH);
+  });
+}
 
 int pgpu_relaxation_from_magic(double nu, double lambda_magic, pgpu_fluid_params* out) {
   return guard([&] {

@@ -899,6 +899,14 @@ int pgpu_set_math_mode(pgpu_sim* sim, int32_t mode) {
   });
 }
 
+int pgpu_get_layout(pgpu_sim* sim, int32_t* layout) {
+  return guard([&] {
+    SIM_CHECK();
+    *layout = sim->compact ? PGPU_LAYOUT_FLUID_ONLY
+                           : (sim->persistent ? PGPU_LAYOUT_DENSE_PERSISTENT : PGPU_LAYOUT_DENSE);
+  });
+}
+
 int pgpu_get_math_mode(pgpu_sim* sim, int32_t* mode) {
   return guard([&] {
     SIM_CHECK();

@@ -475,6 +475,13 @@ class Simulation:
         _check(lib.pgpu_set_body_force(self._h, _vec3(g)))
 
     @property
+    def layout(self) -> str:
+        """"dense", "fluid-only" or "dense-persistent" (pgpu_get_layout)."""
+        m = C.c_int32()
+        _check(lib.pgpu_get_layout(self._h, C.byref(m)))
+        return ("dense", "fluid-only", "dense-persistent")[m.value]
+
+    @property
     def math_mode(self) -> MathMode:
         m = C.c_int32()
         _check(lib.pgpu_get_math_mode(self._h, C.byref(m)))
@@ -673,6 +680,13 @@ def run_to_steady(sim: Simulation, tolerance: float = 1e-8, check_interval: int 
     stats = RunStats(int(st.steps), st.mlups, st.seconds, bool(st.converged), st.residual,
                      int(st.cli_fallbacks))
     return stats, _profile(bufs, meta)
+
+
+def build_info() -> dict:
+    """pgpu_build_info as a dict ({"kernel_hash": ...})."""
+    buf = C.create_string_buffer(256)
+    _check(lib.pgpu_build_info(buf, 256))
+    return dict(kv.split("=", 1) for kv in buf.value.decode().split(";") if "=" in kv)
 
 
 def device_count() -> int:

@@ -36,6 +36,39 @@ def test_reference_arm_json_line(ref):
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
 
 
+def test_reference_arm_never_loads_the_product(ref):
+    """--impl reference builds its workload from oracle code only (spheres,
+    voxelizer checked against the reference-made golden geometry) and times
+    oracle/_ref: libporolb_cuda.so must not be mapped in that process."""
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--config', 'C2', "
+            "'--steps', '2', '--warmup', '3', '--ref-budget', '1']\n"
+            "try:\n    runpy.run_path('bench.py', run_name='__main__')\n"
+            "except SystemExit:\n    pass\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "print('PRODUCT_LOADED' if 'libporolb_cuda' in maps else 'PRODUCT_ABSENT')\n"
+            "print('REF_LOADED' if 'libporolb_ref' in maps else 'REF_ABSENT')\n")
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert "PRODUCT_ABSENT" in res.stdout and "REF_LOADED" in res.stdout, res.stdout
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][0])
+    assert line["geometry"].startswith("sha256 == tests/golden/C2.json")
+    assert line["cpu_baseline"]["cores"] >= 1
+
+
+def test_both_arms_print_the_same_config(ref, pg):
+    """The config dict of --impl reference equals what our arm prints (same
+    keys and values), built here from the product workload definition."""
+    import bench
+    from paper_1507_06565_b200 import configs
+    d = _run("--impl", "reference", "--config", "C3", "--steps", "2", "--warmup", "3",
+             "--ref-budget", "1")
+    w = configs.ALL["C3"]()
+    g = w.geometry()
+    ours = bench.config_dict(w.name, g.fluid_cells, g.cells, g.n_links, w.scheme.name, 1, w.meta)
+    assert d["config"] == json.loads(json.dumps(ours))
+
+
 def test_unknown_config_is_rejected():
     res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "C9"],
                          capture_output=True, text=True, timeout=120, cwd=ROOT)
@@ -49,3 +82,9 @@ def test_ours_json_line_small(gpu):
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"]
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"]
+    assert d["math"] == "fast"
+    pc = d["per_config"]
+    assert set(pc) == {"C2", "C3", "C5"}
+    for v in pc.values():
+        assert v["value"] > 0 and 0 < v["frac"] and v["layout"] in ("dense", "fluid-only",
+                                                                       "dense-persistent")

@@ -279,3 +279,40 @@ def test_oracle_matches_golden_c1(orc, pg):
     assert _sha(o.get_pdfs()[:, fl]) == gold["state"]["pdf_sha256"]
     prof = o.planar_profile()
     assert [float(v).hex() for v in prof["u_superficial"]] == gold["state"]["profile_u_superficial"]
+
+
+@pytest.mark.parametrize("key", ["C1", "C2", "C3", "C5"])
+def test_ref_workloads_match_configs(orc, pg, key):
+    """oracle/ref_workloads.py (the reference arm's workloads, built without
+    the product) restates configs.py: same recipe, same sphere list, and a
+    geometry byte-identical to the reference-made golden fixture."""
+    from oracle import ref_workloads
+    from paper_1507_06565_b200 import configs
+    w = configs.ALL[key]()
+    rw, geom, meta = ref_workloads.build(key, orc)
+    assert meta.pop("geometry_checked").startswith("sha256 == tests/golden")
+    assert (rw.name, tuple(rw.dims), rw.scheme, rw.nu, tuple(rw.g), rw.steps) == \
+        (w.name, tuple(w.dims), w.scheme.name, w.nu, tuple(w.g), w.steps)
+    assert meta == w.meta
+    assert rw.glbm == (w.glbm is not None)
+    if w.pack is not None:
+        c, r, _ = orc.generate_spheres(**rw.spheres)
+        assert np.array_equal(c, w.pack.centers) and np.array_equal(r, w.pack.radii)
+    g = w.geometry()
+    assert np.array_equal(geom.flags, g.flags)
+    for f in ("link_fluid_cell", "link_second_fluid", "link_direction", "link_q", "porosity"):
+        assert np.array_equal(getattr(geom, f), getattr(g, f)), f
+
+
+def test_c4_recipe_matches_configs(orc, pg):
+    """C4's sphere list (Boolean model, 20 783 spheres) from the oracle
+    generator equals the product harness one (geometry: checked against the
+    golden hashes whenever the reference arm runs)."""
+    from oracle import ref_workloads
+    from paper_1507_06565_b200 import configs
+    rw = ref_workloads.WORKLOADS["C4"]
+    w = configs.c4()
+    c, r, por = orc.generate_spheres(**rw.spheres)
+    assert np.array_equal(c, w.pack.centers) and np.array_equal(r, w.pack.radii)
+    assert por == w.meta["boolean_bed_porosity"]
+    assert _sha(np.c_[c, r]) == json.loads((GOLDEN / "C4.json").read_text())["sphere_sha256"]
