@@ -120,6 +120,16 @@ typedef struct {
   const uint8_t* ghost_flags_hi;
 } pgpu_geometry;
 
+/* DriveMode / DriveSpec (boundary.hpp:24-34) */
+enum pgpu_drive_mode { PGPU_DRIVE_BODY_FORCE = 0, PGPU_DRIVE_PRESSURE_GRADIENT_AS_FORCE = 1 };
+typedef struct {
+  int32_t mode;
+  double magnitude[3];       /* body force, or Delta_p on the stream axis */
+  uint8_t periodic_axes[3];
+  int32_t stream_axis;
+  double channel_length;     /* required for PGPU_DRIVE_PRESSURE_GRADIENT_AS_FORCE */
+} pgpu_drive_spec;
+
 /* SteadyConfig (simulation.hpp:118-123) */
 typedef struct {
   double tolerance;
@@ -178,6 +188,13 @@ int pgpu_device_count(void);
 int pgpu_relaxation_from_magic(double nu, double lambda_magic, pgpu_fluid_params* out);
 int pgpu_equilibrium(double delta_rho, const double u[3], double rho0, double out[19]);
 int pgpu_trt_collide(const double f[19], const pgpu_fluid_params* p, double out[19]);
+/* glbm_equilibrium (simulation.hpp:45-48, simulation.cpp:68-78): quadratic
+ * terms scaled by 1/eps; ConfigError for eps <= 0. */
+int pgpu_glbm_equilibrium(double delta_rho, const double u[3], double eps, double rho0,
+                          double out[19]);
+/* resolve_drive (boundary.hpp:24-38, boundary.cpp:9-17): the body force fed
+ * to the collision for a body-force or pressure-gradient drive. */
+int pgpu_resolve_drive(const pgpu_drive_spec* spec, double g_out[3]);
 int pgpu_kozeny_carman(int32_t n, const double* eps, double grain_diameter,
                        double free_threshold, double* K_out);
 int pgpu_make_glbm_params(int32_t n, const double* eps, const double* K, double c_F,
@@ -196,6 +213,9 @@ int pgpu_voxelize_slab(const pgpu_sphere_pack* pack, const int32_t dims[3],
                        pgpu_voxel_geometry** out);
 int pgpu_make_box_geometry(const int32_t dims[3], const pgpu_voxelize_options* opt,
                            pgpu_voxel_geometry** out);
+/* porosity_profile (geometry.hpp:86-88, geometry.cpp:642-661): z[k] = k + 1/2,
+ * eps[k] = fluid fraction of plane k (nz entries each). */
+int pgpu_porosity_profile(const pgpu_geometry* geom, double* z, double* eps);
 /* voxelize() on the GPU: byte-identical output, computed
  * by sm_100a kernels (flags, per-cell link counts, scan, links with q). */
 int pgpu_voxelize_device(const pgpu_sphere_pack* pack, const int32_t dims[3],
@@ -306,6 +326,14 @@ int pgpu_step_part(pgpu_sim* sim, int32_t part);
  * on two streams; the caller orders them (dist.py DistTransport). */
 int pgpu_step_part_on(pgpu_sim* sim, int32_t part, void* stream);
 int pgpu_step_finish(pgpu_sim* sim);
+
+/* Free stream() (simulation.hpp:113-116, simulation.cpp:436-439) of a field
+ * given as host arrays (reference layout, 19*cells each): streaming over
+ * fluid-fluid pairs with periodic wrap, then the buffer swap -- on return
+ * `cur` holds the streamed populations and `next` the previous current ones.
+ * Boundary links are not applied (as in the reference). */
+int pgpu_stream_field(const int32_t dims[3], const uint8_t periodic[3], const uint8_t* flags,
+                      double* cur, double* next, int32_t device);
 
 /* ---- file formats (io.hpp; byte-identical to the reference's writers) ------ */
 /* "%.17g" of v, NUL-terminated (cap >= 25 always suffices). */

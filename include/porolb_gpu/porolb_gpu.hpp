@@ -175,6 +175,72 @@ inline VoxelGeometry make_box_geometry(Dims dims, const VoxelizeOptions& opt) {
   return VoxelGeometry(h);
 }
 
+// simulation.hpp:45-48: porosity-bearing equilibrium (quadratic terms / eps)
+inline std::array<double, kQ> glbm_equilibrium(double delta_rho, const Vec3& u, double eps,
+                                               double rho0 = 1.0) {
+  std::array<double, kQ> f;
+  check(pgpu_glbm_equilibrium(delta_rho, u.data(), eps, rho0, f.data()));
+  return f;
+}
+
+using PeriodicAxes = std::array<bool, 3>;  // field.hpp:25
+
+// DriveMode / DriveSpec / resolve_drive (boundary.hpp:24-38)
+enum class DriveMode : std::uint8_t { BodyForce, PressureGradientAsForce };
+struct DriveSpec {
+  DriveMode mode = DriveMode::BodyForce;
+  Vec3 magnitude{0.0, 0.0, 0.0};  // body force, or Delta_p on the stream axis
+  PeriodicAxes periodic_axes{true, true, false};
+  int stream_axis = 0;
+  double channel_length = 0.0;  // required for PressureGradientAsForce
+};
+inline Vec3 resolve_drive(const DriveSpec& spec) {
+  pgpu_drive_spec c{};
+  c.mode = spec.mode == DriveMode::BodyForce ? PGPU_DRIVE_BODY_FORCE
+                                             : PGPU_DRIVE_PRESSURE_GRADIENT_AS_FORCE;
+  for (int i = 0; i < 3; ++i) {
+    c.magnitude[i] = spec.magnitude[i];
+    c.periodic_axes[i] = spec.periodic_axes[i] ? 1 : 0;
+  }
+  c.stream_axis = spec.stream_axis;
+  c.channel_length = spec.channel_length;
+  Vec3 g;
+  check(pgpu_resolve_drive(&c, g.data()));
+  return g;
+}
+
+// LatticeField (field.hpp:30-68) as host storage, for the free stream() below.
+class LatticeField {
+ public:
+  LatticeField() = default;
+  LatticeField(Dims dims, std::vector<std::uint8_t> flags)
+      : dims_(dims), flags_(std::move(flags)),
+        cur_(static_cast<std::size_t>(kQ * dims.cells()), 0.0),
+        nxt_(static_cast<std::size_t>(kQ * dims.cells()), 0.0) {}
+  const Dims& dims() const { return dims_; }
+  std::int64_t cells() const { return dims_.cells(); }
+  const std::vector<std::uint8_t>& flags() const { return flags_; }
+  bool is_fluid(std::int64_t c) const { return flags_[static_cast<std::size_t>(c)] == 0; }
+  double* cur(int k) { return cur_.data() + static_cast<std::size_t>(k) * cells(); }
+  const double* cur(int k) const { return cur_.data() + static_cast<std::size_t>(k) * cells(); }
+  double* next(int k) { return nxt_.data() + static_cast<std::size_t>(k) * cells(); }
+  const double* next(int k) const { return nxt_.data() + static_cast<std::size_t>(k) * cells(); }
+  void swap_buffers() { cur_.swap(nxt_); }
+
+ private:
+  Dims dims_;
+  std::vector<std::uint8_t> flags_;
+  std::vector<double> cur_, nxt_;
+};
+
+// simulation.hpp:113-116: streaming over fluid-fluid pairs + buffer swap, on
+// the device (pgpu_stream_field; boundary links are not applied).
+inline void stream(LatticeField& field, const PeriodicAxes& periodic, int device = 0) {
+  const int32_t d[3] = {field.dims().nx, field.dims().ny, field.dims().nz};
+  const uint8_t per[3] = {periodic[0], periodic[1], periodic[2]};
+  check(pgpu_stream_field(d, per, field.flags().data(), field.cur(0), field.next(0), device));
+}
+
 struct GlbmPlaneParams {  // simulation.hpp:18-27
   std::vector<double> eps, permeability, omega_plus, omega_minus;
   double forchheimer_cf = 0.0;
@@ -209,6 +275,19 @@ struct ProfileData {  // profile.hpp:12-34
   int stream_axis = 0;
   std::size_t size() const { return z.size(); }
 };
+
+// geometry.hpp:86-88: per-plane porosity from the flags, zero velocity columns
+inline ProfileData porosity_profile(const VoxelGeometry& geom) {
+  const std::size_t nz = static_cast<std::size_t>(geom.dims().nz);
+  ProfileData p;
+  p.z.resize(nz);
+  p.epsilon.resize(nz);
+  p.u_superficial.assign(nz, 0.0);
+  p.u_intrinsic.assign(nz, 0.0);
+  p.u_normalized.assign(nz, 0.0);
+  check(pgpu_porosity_profile(&geom.c(), p.z.data(), p.epsilon.data()));
+  return p;
+}
 
 struct SteadyConfig {  // simulation.hpp:118-123
   double tolerance = 1e-8;

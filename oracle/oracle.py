@@ -128,6 +128,10 @@ class RefLib:
         L.ref_make_glbm_params.argtypes = [C.c_int, P(f64), P(f64), f64, f64, f64, C.c_int, f64,
                                            P(f64), P(f64)]
         L.ref_set_threads.argtypes = [C.c_int]
+        L.ref_glbm_equilibrium.argtypes = [f64, P(f64), f64, f64, P(f64)]
+        L.ref_resolve_drive.argtypes = [C.c_int, P(f64), C.c_int, f64, P(f64)]
+        L.ref_stream.argtypes = [P(C.c_int), P(C.c_int), P(u8), P(f64), P(f64)]
+        L.ref_porosity_profile.argtypes = [vp, P(f64), P(f64)]
         cs = C.c_char_p
         L.ref_format_double.argtypes = [f64, cs, C.c_int]
         L.ref_write_profile_csv.argtypes = [cs, C.c_int] + [P(f64)] * 4 + [C.c_int, P(f64), P(f64)]
@@ -172,6 +176,33 @@ class RefLib:
         self._check(self.lib.ref_apply_link(kind, _i3(dims), _p(c, f64), fluid_cell, second_fluid,
                                             direction, q, _v3(u_wall), rho0, C.byref(out)))
         return out.value
+
+    def glbm_equilibrium(self, drho, u, eps, rho0=1.0):
+        out = np.zeros(Q)
+        self._check(self.lib.ref_glbm_equilibrium(drho, _v3(u), eps, rho0, _p(out, f64)))
+        return out
+
+    def resolve_drive(self, mode, magnitude, stream_axis=0, channel_length=0.0):
+        g = np.zeros(3)
+        self._check(self.lib.ref_resolve_drive(int(mode), _v3(magnitude), int(stream_axis),
+                                               float(channel_length), _p(g, f64)))
+        return tuple(g)
+
+    def stream(self, cur, nxt, flags, periodic):
+        """free stream() in place on (19, nz, ny, nx) buffers (swap semantics)."""
+        dims = cur.shape[1:][::-1]
+        fl = np.ascontiguousarray(flags, dtype=np.uint8).reshape(-1)
+        self._check(self.lib.ref_stream(_i3(dims), _i3(periodic), _p(fl, u8), _p(cur, f64),
+                                        _p(nxt, f64)))
+
+    def porosity_profile(self, geom):
+        h = self.geometry_handle(geom)
+        z, eps = np.zeros(geom.dims[2]), np.zeros(geom.dims[2])
+        try:
+            self._check(self.lib.ref_porosity_profile(h, _p(z, f64), _p(eps, f64)))
+        finally:
+            self.lib.ref_geometry_free(h)
+        return z, eps
 
     def kozeny_carman(self, eps, d, threshold=0.999):
         e = np.ascontiguousarray(eps, dtype=np.float64)

@@ -143,7 +143,57 @@ int ref_apply_link(int kind, const int dims[3], const double* cur, int64_t fluid
   });
 }
 
+int ref_glbm_equilibrium(double drho, const double u[3], double eps, double rho0,
+                         double out[19]) {
+  return guard([&] {
+    const Populations f = glbm_equilibrium(drho, {u[0], u[1], u[2]}, eps, LatticeModel::d3q19(), rho0);
+    std::memcpy(out, f.data(), sizeof(double) * kQ);
+  });
+}
+
+int ref_resolve_drive(int mode, const double mag[3], int stream_axis, double length,
+                      double g[3]) {
+  return guard([&] {
+    DriveSpec spec;
+    spec.mode = mode == 0 ? DriveMode::BodyForce : DriveMode::PressureGradientAsForce;
+    spec.magnitude = {mag[0], mag[1], mag[2]};
+    spec.stream_axis = stream_axis;
+    spec.channel_length = length;
+    const Vec3 r = resolve_drive(spec);
+    for (int i = 0; i < 3; ++i) g[i] = r[i];
+  });
+}
+
+// free stream() on a field built from the caller's buffers; returns the
+// swapped buffers (cur = streamed, next = previous cur).
+int ref_stream(const int dims[3], const int periodic[3], const uint8_t* flags, double* cur,
+               double* next) {
+  return guard([&] {
+    const Dims d{dims[0], dims[1], dims[2]};
+    LatticeField field(d, std::vector<std::uint8_t>(flags, flags + d.cells()));
+    for (int k = 0; k < kQ; ++k) {
+      std::memcpy(field.cur(k), cur + k * d.cells(), sizeof(double) * d.cells());
+      std::memcpy(field.next(k), next + k * d.cells(), sizeof(double) * d.cells());
+    }
+    stream(field, {periodic[0] != 0, periodic[1] != 0, periodic[2] != 0});
+    for (int k = 0; k < kQ; ++k) {
+      std::memcpy(cur + k * d.cells(), field.cur(k), sizeof(double) * d.cells());
+      std::memcpy(next + k * d.cells(), field.next(k), sizeof(double) * d.cells());
+    }
+  });
+}
+
 // ---- geometry ----------------------------------------------------------------
+int ref_porosity_profile(void* h, double* z, double* eps) {
+  return guard([&] {
+    const ProfileData p = porosity_profile(*static_cast<VoxelGeometry*>(h));
+    for (size_t i = 0; i < p.z.size(); ++i) {
+      z[i] = p.z[i];
+      eps[i] = p.epsilon[i];
+    }
+  });
+}
+
 int ref_voxelize(int64_t n, const double* cx, const double* cy, const double* cz,
                  const double* r, const double box[3], double plate_z, const int dims[3],
                  const int periodic[3], int wall_lo, int wall_hi, double q_clamp_min,

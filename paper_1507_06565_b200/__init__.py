@@ -10,6 +10,8 @@ from .porolb import (  # noqa: F401
     VELOCITIES,
     WEIGHTS,
     ConfigError,
+    DriveMode,
+    DriveSpec,
     CudaError,
     FluidParams,
     GeometryError,
@@ -27,12 +29,16 @@ from .porolb import (  # noqa: F401
     device_count,
     equilibrium,
     generate_spheres,
+    glbm_equilibrium,
     glbm_force_and_velocity,
     kozeny_carman,
     make_box_geometry,
     make_glbm_params,
+    porosity_profile,
     relaxation_from_magic,
+    resolve_drive,
     run_to_steady,
+    stream,
     trt_collide,
     voxelize,
     voxelize_device,

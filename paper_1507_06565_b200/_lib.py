@@ -34,6 +34,11 @@ class Geometry(C.Structure):
                 ("ghost_flags_lo", P(u8)), ("ghost_flags_hi", P(u8))]
 
 
+class DriveSpec(C.Structure):
+    _fields_ = [("mode", i32), ("magnitude", f64 * 3), ("periodic_axes", u8 * 3),
+                ("stream_axis", i32), ("channel_length", f64)]
+
+
 class SteadyConfig(C.Structure):
     _fields_ = [("tolerance", f64), ("check_interval", i32), ("max_steps", i64),
                 ("max_speed", f64)]
@@ -89,6 +94,10 @@ SIGNATURES = {
     "pgpu_synchronize": (C.c_int, [vp]),
     "pgpu_get_params": (C.c_int, [vp, P(FluidParams)]),
     "pgpu_set_math_mode": (C.c_int, [vp, i32]),
+    "pgpu_glbm_equilibrium": (C.c_int, [f64, P(f64), f64, f64, P(f64)]),
+    "pgpu_resolve_drive": (C.c_int, [P(DriveSpec), P(f64)]),
+    "pgpu_porosity_profile": (C.c_int, [P(Geometry), P(f64), P(f64)]),
+    "pgpu_stream_field": (C.c_int, [P(i32), P(u8), P(u8), P(f64), P(f64), i32]),
     "pgpu_get_layout": (C.c_int, [vp, P(i32)]),
     "pgpu_get_math_mode": (C.c_int, [vp, P(i32)]),
     "pgpu_set_body_force": (C.c_int, [vp, P(f64)]),

@@ -121,6 +121,20 @@ def build_demo() -> Path:
     return DEMO_BIN
 
 
+DNS_SRC = ROOT / "tests" / "cpp" / "dns_dropin.cpp"
+DNS_BIN = ROOT / "tests" / "cpp" / "dns_dropin"
+
+
+def build_dns_dropin() -> Path:
+    """The reference's dns.cpp driver compiled unchanged (namespace alias only)
+    against the C++ mirror (tests/cpp/dns_dropin.cpp)."""
+    deps = [DNS_SRC, ROOT / "include" / "porolb_gpu" / "porolb_gpu.hpp", LIB]
+    if _stale(DNS_BIN, deps):
+        _run([CXX, "-std=c++17", "-O2", f"-I{ROOT / 'include'}", str(DNS_SRC), "-o", str(DNS_BIN),
+              f"-L{PKG}", "-lporolb_cuda", f"-Wl,-rpath,$ORIGIN/../../{PKG.name}", "-pthread"])
+    return DNS_BIN
+
+
 def build_oracle() -> None:
     """Test infrastructure: oracle/liboracle.so always, oracle/_ref when the
     reference sources are present (this container; the GPU box gets the
@@ -147,6 +161,7 @@ def main(argv: list[str]) -> int:
     lib = build_product(force="--force" in argv)
     print(lib)
     print(build_demo())
+    print(build_dns_dropin())
     if "--all" in argv:
         build_oracle()
     return 0

@@ -726,6 +726,38 @@ __global__ void k_max_speed2(const KParams p, const double* __restrict__ f,
   }
 }
 
+// Free stream() (simulation.cpp:278-321 stream_pass + swap, 436-439) in pull
+// form: fluid d gets cur_k(d - e_k) when that (wrapped) source is fluid; other
+// slots keep `next` (the reference writes only fluid-fluid pairs).
+__global__ void k_stream_field(const uint8_t* __restrict__ flags, int nx, int ny, int nz, int px,
+                               int py, int pz, const double* __restrict__ cur,
+                               double* __restrict__ next, int64_t cells) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells || flags[c] != 0) return;
+  const int x = (int)(c % nx), y = (int)((c / nx) % ny), z = (int)(c / ((int64_t)nx * ny));
+  next[c] = cur[c];
+#pragma unroll
+  for (int k = 1; k < 19; ++k) {
+    int xs = x - EX[k], ys = y - EY[k], zs = z - EZ[k];
+    if (xs < 0) xs = px ? nx - 1 : -1;
+    if (xs >= nx) xs = px ? 0 : -1;
+    if (ys < 0) ys = py ? ny - 1 : -1;
+    if (ys >= ny) ys = py ? 0 : -1;
+    if (zs < 0) zs = pz ? nz - 1 : -1;
+    if (zs >= nz) zs = pz ? 0 : -1;
+    if (xs < 0 || ys < 0 || zs < 0) continue;
+    const int64_t s = ((int64_t)zs * ny + ys) * nx + xs;
+    if (flags[s] == 0) next[(int64_t)k * cells + c] = cur[(int64_t)k * cells + s];
+  }
+}
+
+void launch_stream_field(const uint8_t* flags, const int dims[3], const int per[3],
+                         const double* cur, double* next, cudaStream_t s) {
+  const int64_t cells = (int64_t)dims[0] * dims[1] * dims[2];
+  k_stream_field<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
+      flags, dims[0], dims[1], dims[2], per[0], per[1], per[2], cur, next, cells);
+}
+
 __global__ void k_fill_equilibrium(const uint32_t* __restrict__ cw, int64_t cells,
                                    int64_t ks, double* f, const double* feq /*19*/) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -39,6 +39,9 @@ void launch_max_speed2(bool glbm, const KParams& p, const double* f,
                        unsigned long long* vmax2_bits, int* nonfinite, int* err,
                        cudaStream_t s);
 void preload_kernels();
+// free stream() over a reference-layout field (plane stride = cells)
+void launch_stream_field(const uint8_t* flags, const int dims[3], const int per[3],
+                         const double* cur, double* next, cudaStream_t s);
 void launch_fill_equilibrium(const KParams& p, int64_t cells, double* f, const double* feq,
                              cudaStream_t s);
 

@@ -43,6 +43,16 @@ void equilibrium(double drho, const double u[3], double rho0, double out[19]) {
   }
 }
 
+// simulation.cpp:68-78 (glbm_equilibrium): quadratic terms scaled by 1/eps
+void glbm_equilibrium(double drho, const double u[3], double eps, double rho0, double out[19]) {
+  if (!(eps > 0.0)) throw ConfigError("porosity must be positive");
+  const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];  // lattice.hpp:13 dot
+  for (int k = 0; k < 19; ++k) {
+    const double eu = kE[k][0] * u[0] + kE[k][1] * u[1] + kE[k][2] * u[2];
+    out[k] = weight(k) * (drho + rho0 * (3.0 * eu + (4.5 * eu * eu - 1.5 * uu) / eps));
+  }
+}
+
 // lattice.cpp:88-101
 void moments(const double f[19], double rho0, double& drho, double u[3]) {
   drho = 0.0;
@@ -109,6 +119,53 @@ int pgpu_equilibrium(double delta_rho, const double u[3], double rho0, double ou
   return guard([&] {
     if (!u || !out) throw std::invalid_argument("null pointer");
     equilibrium(delta_rho, u, rho0, out);
+  });
+}
+
+// simulation.hpp:45-48, simulation.cpp:68-78
+int pgpu_glbm_equilibrium(double delta_rho, const double u[3], double eps, double rho0,
+                          double out[19]) {
+  return guard([&] {
+    if (!u || !out) throw std::invalid_argument("null pointer");
+    glbm_equilibrium(delta_rho, u, eps, rho0, out);
+  });
+}
+
+// boundary.hpp:24-38, boundary.cpp:9-17.  One tightening: a stream axis
+// outside 0..2 (the reference would index past the vector) is a ConfigError.
+int pgpu_resolve_drive(const pgpu_drive_spec* spec, double g_out[3]) {
+  return guard([&] {
+    if (!spec || !g_out) throw std::invalid_argument("null pointer");
+    if (spec->mode == PGPU_DRIVE_BODY_FORCE) {
+      for (int i = 0; i < 3; ++i) g_out[i] = spec->magnitude[i];
+      return;
+    }
+    if (spec->mode != PGPU_DRIVE_PRESSURE_GRADIENT_AS_FORCE) throw ConfigError("unknown drive mode");
+    if (!(spec->channel_length > 0.0))
+      throw ConfigError("pressure drive requires a positive channel length");
+    if (spec->stream_axis < 0 || spec->stream_axis > 2) throw ConfigError("stream axis must be 0, 1 or 2");
+    double g[3] = {0.0, 0.0, 0.0};
+    g[spec->stream_axis] = spec->magnitude[spec->stream_axis] / spec->channel_length;
+    for (int i = 0; i < 3; ++i) g_out[i] = g[i];
+  });
+}
+
+// geometry.hpp:86-88, geometry.cpp:642-661: per-plane porosity recounted from
+// the flags (z at cell centres); the velocity columns of the reference's
+// ProfileData are zero and are filled by the C++/Python mirrors.
+int pgpu_porosity_profile(const pgpu_geometry* g, double* z_out, double* eps_out) {
+  return guard([&] {
+    if (!g || !g->flags || !z_out || !eps_out) throw std::invalid_argument("null pointer");
+    const int nx = g->dims[0], ny = g->dims[1], nz = g->dims[2];
+    if (nx <= 0 || ny <= 0 || nz <= 0) throw ConfigError("voxel dims must be positive");
+    const int64_t plane = (int64_t)nx * ny;
+    for (int z = 0; z < nz; ++z) {
+      const uint8_t* f = g->flags + plane * z;
+      int64_t fluid = 0;
+      for (int64_t i = 0; i < plane; ++i) fluid += f[i] == 0;
+      z_out[z] = z + 0.5;
+      eps_out[z] = static_cast<double>(fluid) / (static_cast<double>(nx) * ny);
+    }
   });
 }
 

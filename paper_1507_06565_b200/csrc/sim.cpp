@@ -686,6 +686,40 @@ void device_setup(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors, Lap&& 
 
 extern "C" {
 
+// simulation.hpp:113-116, simulation.cpp:436-439: streaming of a field's
+// current buffer into the next one, then the swap.  The field is the caller's
+// host arrays (reference layout); on return `cur` holds the streamed state
+// (the reference's field.cur() after the swap) and `next` the previous one.
+int pgpu_stream_field(const int32_t dims[3], const uint8_t periodic[3], const uint8_t* flags,
+                      double* cur, double* next, int32_t device) {
+  return guard([&] {
+    if (!dims || !periodic || !flags || !cur || !next) throw std::invalid_argument("null pointer");
+    if (dims[0] <= 0 || dims[1] <= 0 || dims[2] <= 0) throw ConfigError("voxel dims must be positive");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw CudaError("no CUDA device available: the B200 path has no CPU fallback");
+    }
+    if (device < 0 || device >= ndev) throw CudaError("device index out of range");
+    CK(cudaSetDevice(device));
+    const int64_t cells = (int64_t)dims[0] * dims[1] * dims[2];
+    const size_t bytes = sizeof(double) * 19 * (size_t)cells;
+    DevBuf df, dc, dn;
+    CK(cudaMalloc(&df.p, (size_t)cells));
+    CK(cudaMalloc(&dc.p, bytes));
+    CK(cudaMalloc(&dn.p, bytes));
+    CK(cudaMemcpy(df.p, flags, (size_t)cells, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dc.p, cur, bytes, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dn.p, next, bytes, cudaMemcpyHostToDevice));
+    const int d[3] = {dims[0], dims[1], dims[2]};
+    const int per[3] = {periodic[0] != 0, periodic[1] != 0, periodic[2] != 0};
+    launch_stream_field(df.as<uint8_t>(), d, per, dc.as<double>(), dn.as<double>(), 0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(next, dc.p, bytes, cudaMemcpyDeviceToHost));  // swap: old cur
+    CK(cudaMemcpy(cur, dn.p, bytes, cudaMemcpyDeviceToHost));   // streamed
+  });
+}
+
 int pgpu_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {

@@ -124,6 +124,40 @@ def equilibrium(delta_rho: float, u, rho0: float = 1.0) -> np.ndarray:
     return out
 
 
+def glbm_equilibrium(delta_rho: float, u, eps: float, rho0: float = 1.0) -> np.ndarray:
+    """simulation.cpp:68-78 (bindings.cpp:92-97)."""
+    out = np.zeros(Q)
+    _check(lib.pgpu_glbm_equilibrium(float(delta_rho), _vec3(u), float(eps), float(rho0),
+                                     _p(out, C.c_double)))
+    return out
+
+
+class DriveMode(enum.IntEnum):
+    """boundary.hpp:24"""
+    BodyForce = 0
+    PressureGradientAsForce = 1
+
+
+@dataclass
+class DriveSpec:
+    """boundary.hpp:28-34"""
+    mode: DriveMode = DriveMode.BodyForce
+    magnitude: tuple = (0.0, 0.0, 0.0)
+    periodic_axes: tuple = (True, True, False)
+    stream_axis: int = 0
+    channel_length: float = 0.0
+
+
+def resolve_drive(spec: DriveSpec) -> tuple:
+    """boundary.cpp:9-17: the body force G for the collision."""
+    c = _lib.DriveSpec(int(spec.mode), (C.c_double * 3)(*[float(v) for v in spec.magnitude]),
+                       (C.c_uint8 * 3)(*[int(bool(v)) for v in spec.periodic_axes]),
+                       int(spec.stream_axis), float(spec.channel_length))
+    g = (C.c_double * 3)()
+    _check(lib.pgpu_resolve_drive(C.byref(c), g))
+    return tuple(g)
+
+
 def trt_collide(f, params: FluidParams) -> np.ndarray:
     fi = np.ascontiguousarray(f, dtype=np.float64)
     if fi.size != Q:
@@ -408,6 +442,36 @@ class RunStats:
     converged: bool = False
     residual: float = 0.0
     cli_fallbacks: int = 0
+
+
+def porosity_profile(geometry: "VoxelGeometry") -> ProfileData:
+    """geometry.cpp:642-661: per-plane porosity from the flags, zero velocities."""
+    g, keep = geometry.to_c()
+    nz = int(geometry.dims[2])
+    z, eps = np.zeros(nz), np.zeros(nz)
+    _check(lib.pgpu_porosity_profile(C.byref(g), _p(z, C.c_double), _p(eps, C.c_double)))
+    del keep
+    return ProfileData(z=z, u_superficial=np.zeros(nz), u_intrinsic=np.zeros(nz), epsilon=eps,
+                       u_normalized=np.zeros(nz))
+
+
+def stream(cur: np.ndarray, nxt: np.ndarray, flags: np.ndarray, periodic, device: int = 0) -> None:
+    """Free stream() (simulation.cpp:436-439) of a field given as its two
+    population buffers (19, nz, ny, nx), in place: afterwards `cur` holds the
+    streamed populations and `nxt` the previous ones (the buffer swap)."""
+    if cur.shape != nxt.shape or cur.ndim != 4 or cur.shape[0] != Q:
+        raise ConfigError("populations must be (19, nz, ny, nx) arrays of equal shape")
+    for a in (cur, nxt):
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise ConfigError("populations must be C-contiguous float64")
+    nz, ny, nx = cur.shape[1:]
+    fl = np.ascontiguousarray(flags, dtype=np.uint8).reshape(-1)
+    if fl.size != nx * ny * nz:
+        raise ConfigError("flags do not match the field")
+    dims = (C.c_int32 * 3)(nx, ny, nz)
+    per = (C.c_uint8 * 3)(*[int(bool(p)) for p in periodic])
+    _check(lib.pgpu_stream_field(dims, per, _p(fl, C.c_uint8), _p(cur, C.c_double),
+                                 _p(nxt, C.c_double), int(device)))
 
 
 def _profile(bufs, meta: _lib.ProfileMeta) -> ProfileData:

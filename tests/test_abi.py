@@ -115,3 +115,67 @@ def test_status_codes_and_last_error(pg):
     assert _lib.lib.pgpu_relaxation_from_magic(-1.0, 0.25, C.byref(out)) == 1
     assert b"viscosity" in _lib.lib.pgpu_last_error()
     assert _lib.lib.pgpu_relaxation_from_magic(0.1, 0.25, None) == 5
+
+
+def test_glbm_equilibrium_bitwise_vs_reference(pg, ref):
+    """simulation.cpp:68-78 (bindings.cpp:92-97); ConfigError for eps <= 0."""
+    rng = np.random.default_rng(8)
+    for _ in range(200):
+        drho = 0.02 * rng.standard_normal()
+        u = 0.05 * rng.standard_normal(3)
+        eps = rng.uniform(0.05, 1.0)
+        rho0 = rng.choice([1.0, 1.3])
+        assert np.array_equal(pg.glbm_equilibrium(drho, u, eps, rho0),
+                              ref.glbm_equilibrium(drho, u, eps, rho0))
+    # eps = 1: the standard equilibrium (to rounding: the reference groups the
+    # quadratic terms differently, simulation.cpp:76 vs lattice.cpp:84)
+    u = (0.01, -0.002, 0.003)
+    assert np.array_equal(pg.glbm_equilibrium(0.0, u, 1.0), ref.glbm_equilibrium(0.0, u, 1.0))
+    np.testing.assert_allclose(pg.glbm_equilibrium(0.0, u, 1.0), ref.equilibrium(0.0, u, 1.0),
+                               rtol=1e-14, atol=1e-20)
+    for bad in (0.0, -0.5, float("nan")):
+        with pytest.raises(pg.ConfigError):
+            pg.glbm_equilibrium(0.0, u, bad)
+
+
+def test_resolve_drive_vs_reference(pg, ref):
+    """boundary.cpp:9-17 (dns.cpp:13 calls it)."""
+    D = pg.DriveSpec
+    spec = D(pg.DriveMode.BodyForce, (1e-6, 2e-7, -3e-8))
+    assert pg.resolve_drive(spec) == ref.resolve_drive(0, (1e-6, 2e-7, -3e-8))
+    for axis in (0, 1, 2):
+        spec = D(pg.DriveMode.PressureGradientAsForce, (3e-5, 7e-6, 1e-6), stream_axis=axis,
+                 channel_length=97.0)
+        assert pg.resolve_drive(spec) == ref.resolve_drive(1, (3e-5, 7e-6, 1e-6), axis, 97.0)
+    for length in (0.0, -1.0):
+        with pytest.raises(pg.ConfigError, match="positive channel length"):
+            pg.resolve_drive(D(pg.DriveMode.PressureGradientAsForce, (1e-5, 0, 0),
+                               channel_length=length))
+    with pytest.raises(pg.ConfigError):
+        pg.resolve_drive(D(pg.DriveMode.PressureGradientAsForce, (1e-5, 0, 0), stream_axis=3,
+                           channel_length=10.0))
+
+
+def test_porosity_profile_vs_reference(pg, ref):
+    """geometry.cpp:642-661 on a sphere bed (plate and walls included)."""
+    rng = np.random.default_rng(4)
+    dims = (30, 20, 26)
+    c = np.c_[rng.uniform(0, 30, 7), rng.uniform(0, 20, 7), rng.uniform(2, 20, 7)]
+    pack = pg.SpherePack(c, rng.uniform(2, 5, 7), (30.0, 20.0, 26.0), 3.2)
+    g = pg.voxelize(pack, dims, (True, True, False), True, True)
+    prof = pg.porosity_profile(g)
+    z, eps = ref.porosity_profile(g)
+    assert np.array_equal(prof.z, z) and np.array_equal(prof.epsilon, eps)
+    assert not prof.u_superficial.any() and prof.u_normalized.size == dims[2]
+    np.testing.assert_array_equal(prof.epsilon, g.porosity)  # voxelize's own porosity
+
+
+def test_dns_driver_compiles_unchanged(pg):
+    """the reference's dns.cpp make_simulation (with
+    resolve_drive(cfg.drive)) compiles and links against the C++ mirror."""
+    import subprocess
+    root = Path(__file__).resolve().parent.parent
+    res = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", f"-I{root / 'include'}",
+                          str(root / "tests" / "cpp" / "dns_dropin.cpp")],
+                         capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr

@@ -21,3 +21,23 @@ def test_cpp_demo_acceptance(gpu):
     assert out["cli_over_sbb"] >= 0.75
     assert out["bench_cells"] == 128 ** 3
     assert out["io_round_trip"]  # profile/sphere CSV + voxel file through the io.hpp mirror
+
+
+def test_dns_dropin_resolve_drive(gpu, ref):
+    """The reference's make_simulation/run_to_steady (dns.cpp:11-22) compiled
+    unchanged against the C++ mirror: a pressure-gradient drive resolved by
+    resolve_drive() runs to the same steady state as the reference."""
+    exe = Path(__file__).resolve().parent / "cpp" / "dns_dropin"
+    assert exe.exists(), "build with python paper_1507_06565_b200/build.py"
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr
+    got = dict(kv.split("=") for kv in res.stdout.split())
+    g = ref.resolve_drive(1, (4e-8, 0.0, 0.0), 0, 4.0)
+    assert float(got["g"]) == g[0] == 1e-8
+    geom = ref.make_box_geometry((4, 4, 18), (True, True, False), True, True)
+    wp, wm = ref.relaxation_from_magic(1.0 / 6.0, 3.0 / 16.0)
+    r = ref.simulation(geom, 1.0 / 6.0, wp, wm, 3.0 / 16.0, g, 0)
+    st = r.run_to_steady_state(1e-10, 500, 20000)
+    assert int(got["steps"]) == st["steps"] and int(got["converged"]) == int(st["converged"])
+    assert float(got["u_max"]) == r.planar_profile()["u_max"]
+    assert float(got["eps_wall"]) == 0.0 and float(got["eps_mid"]) == 1.0

@@ -329,3 +329,28 @@ def test_inconsistent_links_rejected(gpu):
     bad.link_moving = geom.link_moving[1:]
     with pytest.raises(pg.ConfigError):
         pg.Simulation(bad, 0.1, 3.0 / 16.0, (0, 0, 0), pg.WallScheme.SBB)
+
+
+@pytest.mark.parametrize("periodic", [(1, 1, 1), (1, 0, 1), (0, 1, 0)])
+def test_free_stream_matches_reference(gpu, ref, periodic):
+    """Free stream() (simulation.cpp:436-439) on a sphere bed with random
+    populations in both buffers (slots the pass does not write keep `next`),
+    and test_simulation.cpp:26-42's periodic advection."""
+    pg = gpu
+    rng = np.random.default_rng(3)
+    flags = np.where(rng.random(16 * 12 * 20) < 0.2, 1, 0).astype(np.uint8)
+    cur = rng.standard_normal((19, 16, 12, 20))
+    nxt = rng.standard_normal((19, 16, 12, 20))
+    a, b = cur.copy(), nxt.copy()
+    pg.stream(a, b, flags, periodic)
+    c, d = cur.copy(), nxt.copy()
+    ref.stream(c, d, flags, periodic)
+    assert np.array_equal(a, c) and np.array_equal(b, d)
+    # periodic advection: a lone population moves one cell per call
+    if all(periodic):
+        box = pg.make_box_geometry((5, 4, 3), (True, True, True))
+        f = np.zeros((19, 3, 4, 5))
+        f[7, 1, 2, 4] = 1.0  # e_7 = (1, 1, 0)
+        g = np.zeros_like(f)
+        pg.stream(f, g, box.flags, (1, 1, 1))
+        assert f[7, 1, 3, 0] == 1.0 and f.sum() == 1.0
