@@ -320,6 +320,11 @@ def run_ours(args):
     # simulation stays alive meanwhile (52 GB of 180 GB on C4): reallocating
     # the 26 GB it would free right away made cudaMalloc take up to 0.7 s in
     # some runs (tools/e2e_probe.py), a driver effect unrelated to the path.
+    parity = None
+    if (world > 1 or args.force_slab) and args.verify:
+        parity = verify_slabs(w, sim_obj, args.warmup + args.steps, rank, world, local, dist,
+                              args.scaling)
+
     e2e = None
     if world == 1 and not args.no_e2e and not args.force_slab:
         e2e = e2e_run(pg, configs, w, geom, args.steps, local)
@@ -375,10 +380,53 @@ def run_ours(args):
             "total_cell_mlups": int(np.prod(w.dims)) * args.steps / (ms * 1e-3) / 1e6,
             "per_config": per_config,
         }
+        if parity is not None:
+            line["parity"] = parity
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def verify_slabs(w, sim_obj, total_steps, rank, world, device, dist, scaling):
+    """--verify: after the timed region every rank hashes its slab's fluid
+    populations f(n); rank 0 reruns the whole domain single-GPU for the same
+    number of steps and hashes the same column ranges.  parity_ok = every
+    slab bit-identical (strong scaling: the global domain fits one GPU)."""
+    import hashlib
+
+    import torch
+
+    from paper_1507_06565_b200 import configs
+    from paper_1507_06565_b200.dist import slab_ranges
+
+    def fluid_hash(pdfs, flags):
+        return hashlib.sha256(np.ascontiguousarray(pdfs[:, flags == 0]).tobytes()).hexdigest()
+
+    g = sim_obj.me.geometry
+    mine = fluid_hash(sim_obj.sim.get_pdfs(), g.flags.reshape(g.dims[::-1]))
+    hashes = [None] * world
+    if dist is not None:
+        dist.all_gather_object(hashes, mine)
+    else:
+        hashes = [mine]
+    if rank != 0:
+        return None
+    if scaling != "strong" and world > 1:
+        return {"parity_ok": None, "why": "weak scaling: the global domain does not fit one GPU",
+                "slab_sha256": hashes}
+    full = w.geometry()
+    sim = configs.make_simulation(w, full, device=device)
+    sim.step(total_steps)
+    f = sim.get_pdfs()
+    del sim
+    torch.cuda.empty_cache()
+    flags = full.flags.reshape(w.dims[::-1])
+    ok = []
+    for r, (x0, x1) in enumerate(slab_ranges(w.dims[0], world)):
+        ok.append(fluid_hash(np.ascontiguousarray(f[..., x0:x1]), flags[..., x0:x1]) == hashes[r])
+    return {"parity_ok": all(ok), "steps": total_steps, "slabs_equal": ok,
+            "what": "sha256 of every slab's fluid f(n) vs the single-GPU run of the same steps"}
 
 
 def per_config_run(pg, configs, skip, device, peak):
@@ -505,6 +553,9 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=20.0,
                     help="seconds of reference steps per --impl reference run (after >= 3 warm-ups)")
     ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--verify", action="store_true",
+                    help="N>1 / --force-slab: check the slabs' f(n) bitwise against a "
+                         "single-GPU run of the same steps (strong scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-slab", action="store_true",

@@ -327,6 +327,34 @@ int pgpu_step_part(pgpu_sim* sim, int32_t part);
 int pgpu_step_part_on(pgpu_sim* sim, int32_t part, void* stream);
 int pgpu_step_finish(pgpu_sim* sim);
 
+/* ---- multi-GPU x-slab driver (dist.cpp) ----------------------
+ * One handle drives the slabs of an x-slab decomposition: per step the edge
+ * columns (high-priority stream) -> 5-PDF ghost exchange, concurrently with
+ * the interior columns on the simulation's stream; the exchange is NCCL
+ * (one rank per process; libnccl resolved at run time) or peer copies (all
+ * slabs in this process).  Each simulation must come from a slab geometry
+ * (pgpu_voxelize_slab) and must not have halo buffers of its own in use: the
+ * driver owns them.  Observables are global (all ranks).  No reference
+ * analogue (the reference is single-node OpenMP); the exchange rebuilds the
+ * paper's communication-reducing ghost layer. */
+typedef struct pgpu_dist pgpu_dist;
+/* NCCL unique id (128 bytes): made by rank 0, distributed by the caller. */
+int pgpu_dist_nccl_unique_id(uint8_t id[128]);
+int pgpu_dist_create_nccl(pgpu_sim* sim, const uint8_t id[128], int32_t rank, int32_t world,
+                          pgpu_dist** out);
+/* sims[r] = slab r of `world` (any devices; same device is allowed). */
+int pgpu_dist_create_local(pgpu_sim* const* sims, int32_t world, pgpu_dist** out);
+/* NCCL mode replays a CUDA graph of two steps (default on; PGPU_DIST_GRAPHS=0). */
+int pgpu_dist_set_graphs(pgpu_dist* d, int32_t enable);
+int pgpu_dist_step(pgpu_dist* d, int64_t n);
+int pgpu_dist_synchronize(pgpu_dist* d);
+int pgpu_dist_plane_sums(pgpu_dist* d, int32_t stream_axis, double* sums_nz);
+int pgpu_dist_max_speed2(pgpu_dist* d, double* vmax2, int32_t* finite);
+int pgpu_dist_planar_profile(pgpu_dist* d, int32_t stream_axis, double* z, double* u_superficial,
+                             double* u_intrinsic, double* epsilon, double* u_normalized,
+                             pgpu_profile_meta* meta);
+int pgpu_dist_destroy(pgpu_dist* d);
+
 /* Free stream() (simulation.hpp:113-116, simulation.cpp:436-439) of a field
  * given as host arrays (reference layout, 19*cells each): streaming over
  * fluid-fluid pairs with periodic wrap, then the buffer swap -- on return

@@ -7,6 +7,8 @@
 #pragma once
 
 #include <array>
+#include <cmath>
+#include <limits>
 #include <cstdint>
 #include <limits>
 #include <memory>
@@ -172,6 +174,19 @@ inline VoxelGeometry make_box_geometry(Dims dims, const VoxelizeOptions& opt) {
   const pgpu_voxelize_options o = detail::opts(opt);
   pgpu_voxel_geometry* h = nullptr;
   check(pgpu_make_box_geometry(d, &o, &h));
+  return VoxelGeometry(h);
+}
+
+// Local x-slab [x0, x1) of voxelize(pack, dims, opt) plus the ghost-column
+// flags (multi-GPU runs, DistSimulation below); byte-identical to the
+// corresponding columns of the single-domain geometry.
+inline VoxelGeometry voxelize_slab(const SpherePack& pack, Dims dims, const VoxelizeOptions& opt,
+                                   int x0, int x1) {
+  detail::PackArrays pa(pack);
+  const int32_t d[3] = {dims.nx, dims.ny, dims.nz};
+  const pgpu_voxelize_options o = detail::opts(opt);
+  pgpu_voxel_geometry* h = nullptr;
+  check(pgpu_voxelize_slab(&pa.c, d, &o, x0, x1, &h));
   return VoxelGeometry(h);
 }
 
@@ -421,6 +436,58 @@ class Simulation {
   std::unique_ptr<pgpu_sim, Del> h_;
   Dims dims_;
   bool porous_ = false;
+};
+
+// porolb::Simulation over P GPUs (x slabs, 5-PDF ghost exchange; dist.cpp).
+// Local: every slab's Simulation lives in this process (devices may differ,
+// exchange by peer copies).  NCCL: one slab per process; rank 0 makes the id
+// with nccl_unique_id() and the caller distributes it (MPI, a file, ...).
+class DistSimulation {
+ public:
+  explicit DistSimulation(const std::vector<Simulation*>& slabs) {
+    std::vector<pgpu_sim*> h;
+    for (Simulation* s : slabs) h.push_back(s->handle());
+    pgpu_dist* d = nullptr;
+    check(pgpu_dist_create_local(h.data(), static_cast<int32_t>(h.size()), &d));
+    d_.reset(d);
+    nz_ = slabs.front()->dims().nz;
+  }
+  DistSimulation(Simulation& slab, const std::array<std::uint8_t, 128>& nccl_id, int rank,
+                 int world) {
+    pgpu_dist* d = nullptr;
+    check(pgpu_dist_create_nccl(slab.handle(), nccl_id.data(), rank, world, &d));
+    d_.reset(d);
+    nz_ = slab.dims().nz;
+  }
+  static std::array<std::uint8_t, 128> nccl_unique_id() {
+    std::array<std::uint8_t, 128> id;
+    check(pgpu_dist_nccl_unique_id(id.data()));
+    return id;
+  }
+  void step(long n = 1) { check(pgpu_dist_step(d_.get(), n)); }
+  void synchronize() const { check(pgpu_dist_synchronize(d_.get())); }
+  // global observables (simulation.cpp:371-434 over all slabs)
+  ProfileData planar_profile(int stream_axis = 0) const {
+    std::vector<double> b[5];
+    for (auto& v : b) v.resize(static_cast<std::size_t>(nz_));
+    pgpu_profile_meta m;
+    check(pgpu_dist_planar_profile(d_.get(), stream_axis, b[0].data(), b[1].data(), b[2].data(),
+                                   b[3].data(), b[4].data(), &m));
+    return detail::profile_from(b, m);
+  }
+  double max_speed() const {
+    double v2;
+    int32_t fin;
+    check(pgpu_dist_max_speed2(d_.get(), &v2, &fin));
+    return fin ? std::sqrt(v2) : std::numeric_limits<double>::quiet_NaN();
+  }
+
+ private:
+  struct Del {
+    void operator()(pgpu_dist* d) const { pgpu_dist_destroy(d); }
+  };
+  std::unique_ptr<pgpu_dist, Del> d_;
+  int nz_ = 0;
 };
 
 // simulation.hpp:134-138

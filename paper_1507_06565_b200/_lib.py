@@ -94,6 +94,17 @@ SIGNATURES = {
     "pgpu_synchronize": (C.c_int, [vp]),
     "pgpu_get_params": (C.c_int, [vp, P(FluidParams)]),
     "pgpu_set_math_mode": (C.c_int, [vp, i32]),
+    "pgpu_dist_nccl_unique_id": (C.c_int, [P(u8)]),
+    "pgpu_dist_create_nccl": (C.c_int, [vp, P(u8), i32, i32, P(vp)]),
+    "pgpu_dist_create_local": (C.c_int, [P(vp), i32, P(vp)]),
+    "pgpu_dist_set_graphs": (C.c_int, [vp, i32]),
+    "pgpu_dist_step": (C.c_int, [vp, i64]),
+    "pgpu_dist_synchronize": (C.c_int, [vp]),
+    "pgpu_dist_plane_sums": (C.c_int, [vp, i32, P(f64)]),
+    "pgpu_dist_max_speed2": (C.c_int, [vp, P(f64), P(i32)]),
+    "pgpu_dist_planar_profile": (C.c_int, [vp, i32, P(f64), P(f64), P(f64), P(f64), P(f64),
+                                           P(ProfileMeta)]),
+    "pgpu_dist_destroy": (C.c_int, [vp]),
     "pgpu_glbm_equilibrium": (C.c_int, [f64, P(f64), f64, f64, P(f64)]),
     "pgpu_resolve_drive": (C.c_int, [P(DriveSpec), P(f64)]),
     "pgpu_porosity_profile": (C.c_int, [P(Geometry), P(f64), P(f64)]),

@@ -31,8 +31,9 @@ CUDA_INC = "/usr/local/cuda/include"
 CXX = shutil.which("g++") or "g++"
 
 CU_SOURCES = ["kernels.cu", "sweep_compact.cu", "voxelize_device.cu", "setup.cu"]
-CPP_SOURCES = ["params.cpp", "voxelize.cpp", "synth.cpp", "sim.cpp", "io.cpp"]
-HEADERS = ["kparams.h", "kernels.h", "lattice.cuh", "host_common.h", "voxel_geometry.h", "setup.h", "staging.h"]
+CPP_SOURCES = ["params.cpp", "voxelize.cpp", "synth.cpp", "sim.cpp", "io.cpp", "dist.cpp"]
+HEADERS = ["kparams.h", "kernels.h", "lattice.cuh", "host_common.h", "voxel_geometry.h", "setup.h", "staging.h",
+           "sim_impl.h"]
 
 
 def _run(cmd: list[str]) -> None:
@@ -103,7 +104,7 @@ def build_product(force: bool = False, defines: tuple = (), lib: Path = LIB,
     stamp.write_text(khash)
     if force or jobs or _stale(LIB, objs):
         _run([NVCC, *GENCODE, "-shared", "-cudart", "static", "-o", str(LIB),
-              *[str(o) for o in objs], "-Xcompiler", "-pthread"])
+              *[str(o) for o in objs], "-Xcompiler", "-pthread", "-ldl"])
     return LIB
 
 
@@ -135,6 +136,19 @@ def build_dns_dropin() -> Path:
     return DNS_BIN
 
 
+DIST_SRC = ROOT / "tests" / "cpp" / "dist_demo.cpp"
+DIST_BIN = ROOT / "tests" / "cpp" / "dist_demo"
+
+
+def build_dist_demo() -> Path:
+    """The C++ multi-GPU host path demo (DistSimulation, local + NCCL)."""
+    deps = [DIST_SRC, ROOT / "include" / "porolb_gpu" / "porolb_gpu.hpp", LIB]
+    if _stale(DIST_BIN, deps):
+        _run([CXX, "-std=c++17", "-O2", f"-I{ROOT / 'include'}", str(DIST_SRC), "-o", str(DIST_BIN),
+              f"-L{PKG}", "-lporolb_cuda", f"-Wl,-rpath,$ORIGIN/../../{PKG.name}", "-pthread"])
+    return DIST_BIN
+
+
 def build_oracle() -> None:
     """Test infrastructure: oracle/liboracle.so always, oracle/_ref when the
     reference sources are present (this container; the GPU box gets the
@@ -162,6 +176,7 @@ def main(argv: list[str]) -> int:
     print(lib)
     print(build_demo())
     print(build_dns_dropin())
+    print(build_dist_demo())
     if "--all" in argv:
         build_oracle()
     return 0

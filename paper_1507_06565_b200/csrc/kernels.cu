@@ -551,12 +551,12 @@ template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(128) k_sweep_edges(const KParams p,
                                                      const double* __restrict__ src,
                                                      double* __restrict__ dst) {
-  // grid (2 faces, ceil(ny/4), nz); each warp one row's band
+  // grid (2 faces, ceil(ny * band / 128), nz); threads walk (y, column) pairs
   const int w = edge_band(p.nx);
-  const int xx = threadIdx.x & 31;
-  const int y = blockIdx.y * 4 + (threadIdx.x >> 5);
+  const int t = blockIdx.y * blockDim.x + threadIdx.x;
+  const int xx = t % w, y = t / w;
   const int z = blockIdx.z;
-  if (xx >= w || y >= p.ny) return;
+  if (y >= p.ny) return;
   const int x = blockIdx.x ? p.nx - w + xx : xx;
   if (blockIdx.x && x < w) return;  // the bands overlap when nx < 2w
   const CellWord cw = ld_cw(p, ((int64_t)z * p.ny + y) * p.nx + x);
@@ -805,7 +805,7 @@ void launch_sweep_t(const KParams& p, const double* src, double* dst, int part,
                     cudaStream_t s) {
   if (part == PART_EDGES) {
     k_sweep_edges<CM, GLBM, RECORDS, SLAB, OP>
-        <<<dim3(2, (p.ny + 3) / 4, p.nz), 128, 0, s>>>(p, src, dst);
+        <<<dim3(2, (p.ny * edge_band(p.nx) + 127) / 128, p.nz), 128, 0, s>>>(p, src, dst);
   } else if (g_sweep_mode <= 1) {
     const int zper = pipe_zper(p);
     const dim3 grid((p.nx + kPipeBX - 1) / kPipeBX, p.ny, (p.nz + zper - 1) / zper);

@@ -31,12 +31,14 @@ __device__ __forceinline__ constexpr double pair_w(int p) { return p < 3 ? 1.0 /
 enum SweepOp { OP_STREAM_COLLIDE = 0, OP_STREAM_ONLY = 1 };
 enum SweepPart { PART_ALL = 0, PART_EDGES = 1, PART_INTERIOR = 2 };
 
-// x-slab split: the edge part sweeps one warp-aligned band of columns at each
-// x face (x < w or x >= nx - w; it alone reads ghosts and fills the send
-// buffers), the interior part the rest.  Bands of 32 keep the edge rows
-// coalesced, so the edge part streams like the interior instead of touching
-// one 8-byte slot per DRAM line.
-__host__ __device__ __forceinline__ int edge_band(int nx) { return nx < 64 ? (nx + 1) / 2 : 32; }
+// x-slab split: the edge part sweeps a band of columns at each x face
+// (x < w or x >= nx - w; it alone reads ghosts and fills the send buffers),
+// the interior part the rest.  Slabs of >= 96 columns use warp-aligned bands
+// of 32 (coalesced edge rows); narrower slabs (64 columns = C4 strong scaling
+// at 8 GPUs) use the single face columns, so the interior part -- which the
+// halo exchange overlaps -- is not empty (the edge part then reads one slot
+// per row and 32-byte sector, but for only 2 of the slab's columns).
+__host__ __device__ __forceinline__ int edge_band(int nx) { return nx >= 96 ? 32 : 1; }
 __device__ __forceinline__ bool in_edge_band(int x, int nx) {
   const int w = edge_band(nx);
   return x < w || x >= nx - w;

@@ -84,7 +84,7 @@ __host__ __device__ constexpr int row_of(int j) {
 // x-slab split: each edge band (edge_band() = 32 columns) is exactly the first
 // / last 32-cell chunk of a row.
 __host__ __device__ __forceinline__ bool edge_chunks(const KParams& p) {
-  return p.nx % 32 == 0 && p.nx >= 64;
+  return p.nx % 32 == 0 && edge_band(p.nx) == 32;
 }
 
 // Periodic wrap of a row coordinate; false if it leaves a non-periodic axis.
@@ -286,16 +286,17 @@ __global__ void __launch_bounds__(128) k_csweep_cells(const KParams p,
   if (part == PART_INTERIOR && in_edge_band(x, p.nx)) return;
   csweep_cell<CM, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, blockIdx.y, blockIdx.z);
 }
-// ... or of the two x edge bands (slab split; grid (2, ceil(ny/4), nz)).
+// ... or of the two x edge bands (slab split; threads walk the band's
+// (y, column) pairs, grid (2, ceil(ny * band / 128), nz)).
 template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(128) k_csweep_edges(const KParams p,
                                                       const double* __restrict__ src,
                                                       double* __restrict__ dst) {
   const int w = edge_band(p.nx);
-  const int xx = threadIdx.x & 31;
-  const int y = blockIdx.y * 4 + (threadIdx.x >> 5);
+  const int t = blockIdx.y * blockDim.x + threadIdx.x;
+  const int xx = t % w, y = t / w;
   const int z = blockIdx.z;
-  if (xx >= w || y >= p.ny) return;
+  if (y >= p.ny) return;
   const int x = blockIdx.x ? p.nx - w + xx : xx;
   if (blockIdx.x && x < w) return;
   csweep_cell<CM, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z);
@@ -877,7 +878,7 @@ void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* sr
   // the pipelined kernel sweeps the slab edge bands when each band is one chunk
   if (cfg.part == PART_EDGES && (!edge_chunks(p) || g_plain_sweep())) {
     k_csweep_edges<CM, GLBM, RECORDS, SLAB, OP>
-        <<<dim3(2, (p.ny + 3) / 4, p.nz), 128, 0, s>>>(p, src, dst);
+        <<<dim3(2, (p.ny * edge_band(p.nx) + 127) / 128, p.nz), 128, 0, s>>>(p, src, dst);
   } else if (g_plain_sweep()) {
     k_csweep_cells<CM, GLBM, RECORDS, SLAB, OP><<<ccell_grid(p), ccell_block(p), 0, s>>>(
         p, src, dst, cfg.part);
@@ -888,7 +889,7 @@ void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* sr
     if (cfg.part == PART_EDGES) grid = dim3(1, (p.ny + kCW / 2 - 1) / (kCW / 2), zg);
     if (cfg.part == PART_INTERIOR && edge_chunks(p))
       grid = dim3((unsigned)(((int64_t)p.ny * (p.nchunk - 2) + kCW - 1) / kCW), 1, zg);
-    if (grid.x == 0) return;  // nx == 64 slab: everything is edge band
+    if (grid.x == 0) return;
     constexpr int smem = (int)sizeof(CSmem<RECORDS, RECORDS && CM == CM_FAST_FOLD>) + PGPU_SMEM_PAD;  // pad: L1-capacity experiment
     static bool attr = [] {
       cudaFuncSetAttribute(k_sweep_cpipe<CM, GLBM, RECORDS, SLAB, OP>,

@@ -1,29 +1,25 @@
-"""x-slab domain decomposition across GPUs (DESIGN.md §6; SURVEY §8e).
+"""x-slab domain decomposition across GPUs (DESIGN.md §8; SURVEY §8e).
 
 The global domain is cut along the flow axis x into P contiguous slabs, one
-per rank (one process per GPU).  In pull form a cell at a slab face needs,
-from the neighbouring slab, only the post-collision populations whose
-velocity points into the receiving slab: directions {1,7,9,11,13} (e_x=+1)
-from the left neighbour and {2,8,10,12,14} (e_x=-1) from the right one; a CLI
-link's second fluid cell x_f1 - e_k lies in the ghost column only for those
-same directions.  So each face carries exactly 5 PDFs per (y, z): the
-paper's communication-reducing ghost-layer exchange.
+per rank.  In pull form a cell at a slab face needs, from the neighbouring
+slab, only the post-collision populations whose velocity points into the
+receiving slab: directions {1,7,9,11,13} (e_x=+1) from the left neighbour and
+{2,8,10,12,14} (e_x=-1) from the right one; a CLI link's second fluid cell
+x_f1 - e_k lies in the ghost column only for those same directions.  So each
+face carries exactly 5 PDFs per (y, z): the paper's communication-reducing
+ghost-layer exchange.
 
-Per step and rank (DistTransport), on two CUDA streams:
-  1. edge stream: step_part(0) pulls/collides the edge columns x=0 and
-     x=nx-1 and writes their 5 outgoing PDFs to the send buffers, then the
-     exchange (NCCL send/recv through torch.distributed) fills the
-     neighbours' ghost buffers of the next parity;
-  2. compute stream: step_part(1), the interior columns, concurrently;
-  3. step_finish(): buffer swap, parity flip.
-Interior cells never read ghosts, so the only cross-stream orderings are the
-column dependencies between consecutive steps: the edge part of step n+1
-waits for the interior of step n (and for the exchange of step n, in stream
-order), the interior of step n+1 waits for the edge part of step n.
-The exchange is the only data-path collective; observables combine per-rank
-partial sums with all_reduce.  LocalTransport runs all slabs in one process on
-one device (sequentially, no kernel ever waits on another), which is how the
-decomposition is verified bit-for-bit on a single GPU.
+On the GPU the per-step schedule runs natively in libporolb_cuda.so
+(csrc/dist.cpp, `pgpu_dist_*`): edge columns on a high-priority stream, then
+the exchange, overlapped with the interior columns on the simulation's
+stream; NCCL between processes (one rank per GPU, `SlabSimulation`) or peer
+copies between the slabs of one process (`LocalTransport`).  NCCL mode
+replays the steady-state schedule as a CUDA graph.  This module only builds
+the slab simulations and hands them to that driver.
+
+`DistTransport` keeps the same schedule in Python over torch.distributed for
+CPU engines (the oracle slab engine), which is how the host-side logic of the
+decomposition is tested with gloo at world size 2 without GPUs.
 """
 from __future__ import annotations
 
@@ -39,8 +35,10 @@ TO_LEFT = (2, 8, 10, 12, 14)   # e_x = -1: leave through x = 0
 
 
 def slab_ranges(nx: int, world: int) -> List[tuple]:
-    """Equal contiguous x ranges; every slab keeps a multiple of 32 cells
-    when possible so rows stay warp-aligned."""
+    """Equal contiguous x ranges of nx / world columns (ConfigError if world
+    does not divide nx).  Widths need not be multiples of 32: slabs of >= 96
+    columns sweep 32-column edge bands, narrower ones the face columns
+    (csrc/lattice.cuh edge_band)."""
     if nx % world:
         raise P.ConfigError(f"nx={nx} is not divisible by {world} ranks")
     w = nx // world
@@ -72,20 +70,20 @@ class SlabRank:
         self.x0, self.x1 = slab_ranges(workload.dims[0], world)[rank]
         self.geometry = geometry if geometry is not None else workload.geometry_slab(self.x0, self.x1)
         if engine is None:
+            # CUDA slab: the native driver (pgpu_dist) owns its halo buffers
             self.sim = P.Simulation.from_params(self.geometry, workload.params(), workload.scheme,
                                                 int(device))
             gp = workload.glbm_params()
             if gp is not None:
                 self.sim.set_porous(gp)
             tdev = torch.device("cuda", int(device))
-            # kernels, halo copies and NCCL calls are ordered on one torch stream
+            # the slab's interior sweeps and observables run on this torch stream
             self.stream = stream if stream is not None else torch.cuda.Stream(device=tdev)
             self.sim.set_stream(self.stream.cuda_stream)
-        else:
-            self.sim = engine(self.geometry, workload)
-            tdev = torch.device("cpu")
+            return
+        self.sim = engine(self.geometry, workload)
         n = self.sim.halo_elems
-        mk = lambda: torch.zeros(n, dtype=torch.float64, device=tdev)  # noqa: E731
+        mk = lambda: torch.zeros(n, dtype=torch.float64)  # noqa: E731
         self.send_lo, self.send_hi = mk(), mk()
         self.recv_lo = [mk(), mk()]
         self.recv_hi = [mk(), mk()]
@@ -93,8 +91,101 @@ class SlabRank:
                                   self.recv_hi[0], self.recv_hi[1])
 
 
+def _profile_meta(prof: P.ProfileData, params: P.FluidParams, geometry, nz: int) -> None:
+    """ProfileData metadata exactly as simulation.cpp:386-397 fills it."""
+    prof.nu = params.nu
+    prof.body_force = tuple(params.body_force)
+    lo, hi = geometry.wall_plane_lo, geometry.wall_plane_hi
+    if lo is not None and hi is not None:
+        prof.z0, prof.height = float(lo), float(hi) - float(lo)
+    else:
+        prof.z0, prof.height = 0.0, float(nz)
+
+
+class NativeDist:
+    """The native x-slab driver (csrc/dist.cpp) over slab simulations.
+
+    local mode: `sims` are all slabs of the decomposition in this process
+    (peer copies); nccl mode: `sims` is this process's one slab and
+    `nccl_id`/`rank`/`world` describe the communicator."""
+
+    def __init__(self, sims, nccl_id: Optional[bytes] = None, rank: int = 0,
+                 world: Optional[int] = None):
+        import ctypes as C
+
+        from . import _lib
+        self._C, self._lib = C, _lib
+        self.sims = list(sims)
+        self.world = int(world if world is not None else len(self.sims))
+        self._h = C.c_void_p()
+        if nccl_id is None:
+            arr = (C.c_void_p * len(self.sims))(*[s._h.value for s in self.sims])
+            P._check(_lib.lib.pgpu_dist_create_local(arr, len(self.sims), C.byref(self._h)))
+        else:
+            buf = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+            P._check(_lib.lib.pgpu_dist_create_nccl(self.sims[0]._h, buf, int(rank), self.world,
+                                                    C.byref(self._h)))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        import ctypes as C
+
+        from . import _lib
+        buf = (C.c_uint8 * 128)()
+        P._check(_lib.lib.pgpu_dist_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def step(self, n: int = 1) -> None:
+        P._check(self._lib.lib.pgpu_dist_step(self._h, int(n)))
+
+    def set_graphs(self, enable: bool) -> None:
+        P._check(self._lib.lib.pgpu_dist_set_graphs(self._h, int(bool(enable))))
+
+    def synchronize(self) -> None:
+        P._check(self._lib.lib.pgpu_dist_synchronize(self._h))
+
+    def plane_sums(self, stream_axis: int = 0) -> np.ndarray:
+        out = np.zeros(self.sims[0].nz)
+        P._check(self._lib.lib.pgpu_dist_plane_sums(self._h, int(stream_axis),
+                                                    P._p(out, self._C.c_double)))
+        return out
+
+    def max_speed2(self):
+        v2, fin = self._C.c_double(), self._C.c_int32()
+        P._check(self._lib.lib.pgpu_dist_max_speed2(self._h, self._C.byref(v2),
+                                                    self._C.byref(fin)))
+        return v2.value, bool(fin.value)
+
+    def max_speed(self) -> float:
+        v2, fin = self.max_speed2()
+        return float(np.sqrt(v2)) if fin else float("nan")
+
+    def planar_profile(self, stream_axis: int = 0) -> P.ProfileData:
+        """simulation.cpp:371-417 over the whole domain (per-rank plane sums
+        added across ranks: equal to the reference within rounding)."""
+        nz = self.sims[0].nz
+        bufs = [np.zeros(nz) for _ in range(5)]
+        meta = self._lib.ProfileMeta()
+        P._check(self._lib.lib.pgpu_dist_planar_profile(
+            self._h, int(stream_axis), *[P._p(b, self._C.c_double) for b in bufs],
+            self._C.byref(meta)))
+        return P._profile(bufs, meta)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.lib.pgpu_dist_destroy(self._h)
+            self._h = self._C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class DistTransport:
-    """One rank per process; neighbours over torch.distributed (NCCL / gloo)."""
+    """CPU engines: the native schedule restated over torch.distributed
+    (gloo), one rank per process (host-logic tests of the decomposition)."""
 
     def __init__(self, rank: SlabRank, group=None):
         import torch.distributed as dist
@@ -105,12 +196,6 @@ class DistTransport:
         self.left = (rank.rank - 1) % rank.world
         self.right = (rank.rank + 1) % rank.world
 
-    def step(self, n: int = 1) -> None:
-        if self.me.stream is None:  # CPU engine: one ordered sequence
-            self._step_serial(n)
-            return
-        self._step_two_streams(n)
-
     def _exchange(self):
         me, dist = self.me, self.dist
         p = me.sim.halo_parity
@@ -118,13 +203,14 @@ class DistTransport:
             me.recv_hi[p].copy_(me.send_lo)
             me.recv_lo[p].copy_(me.send_hi)
             return []
+        # same per-peer order as csrc/dist.cpp (matching does not rely on tags)
         ops = [dist.P2POp(dist.isend, me.send_lo, self.left, self.group, tag=0),
                dist.P2POp(dist.isend, me.send_hi, self.right, self.group, tag=1),
                dist.P2POp(dist.irecv, me.recv_hi[p], self.right, self.group, tag=0),
                dist.P2POp(dist.irecv, me.recv_lo[p], self.left, self.group, tag=1)]
         return dist.batch_isend_irecv(ops)
 
-    def _step_serial(self, n: int) -> None:
+    def step(self, n: int = 1) -> None:
         me = self.me
         for _ in range(int(n)):
             me.sim.step_part(0)  # edge columns -> send buffers
@@ -134,45 +220,16 @@ class DistTransport:
             for req in reqs:  # the next step's edge part reads the new ghosts
                 req.wait()
 
-    def _step_two_streams(self, n: int) -> None:
-        import torch
-
-        me = self.me
-        main = me.stream
-        if getattr(self, "_edge_stream", None) is None:
-            # high priority: the edge part (and the exchange ordered after it)
-            # is dispatched ahead of the interior sweep's remaining blocks
-            self._edge_stream = torch.cuda.Stream(device=main.device, priority=-1)
-        edge = self._edge_stream
-        edge.wait_stream(main)  # everything issued before step() on the main stream
-        prev_edge = None
-        for _ in range(int(n)):
-            ev_main = torch.cuda.Event()
-            ev_main.record(main)  # interior of the previous step
-            with torch.cuda.stream(edge):
-                edge.wait_event(ev_main)
-                me.sim.step_part(0, edge.cuda_stream)  # edge columns -> send buffers
-                ev_edge = torch.cuda.Event()
-                ev_edge.record(edge)
-                for req in self._exchange():  # in edge-stream order
-                    req.wait()
-            if prev_edge is not None:  # the interior reads/overwrites the previous
-                main.wait_event(prev_edge)  # step's edge columns
-            me.sim.step_part(1, main.cuda_stream)  # interior, concurrent with edge + exchange
-            me.sim.step_finish()
-            prev_edge = ev_edge
-        main.wait_stream(edge)  # step() returns with all work ordered on the main stream
-
     # -- collective observables ---------------------------------------------
     def _allreduce(self, values, op="sum"):
         import torch
 
-        t = torch.tensor(np.asarray(values, dtype=np.float64), device=self.me.send_lo.device)
+        t = torch.tensor(np.asarray(values, dtype=np.float64))
         if self.me.world > 1:
             rop = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX,
                    "min": self.dist.ReduceOp.MIN}[op]
             self.dist.all_reduce(t, op=rop, group=self.group)
-        return t.cpu().numpy()
+        return t.numpy()
 
     def fluid_cells(self) -> int:
         return int(self._allreduce([self.me.sim.fluid_cells])[0])
@@ -184,23 +241,27 @@ class DistTransport:
         g = me.geometry
         nx_loc, ny, nz = g.dims
         sums = self._allreduce(me.sim.plane_sums(stream_axis))
-        counts = self._allreduce(np.asarray(g.porosity) * nx_loc * ny)
+        counts = self._allreduce(np.round(np.asarray(g.porosity) * nx_loc * ny))
         plane = float(me.workload.dims[0] * ny)
-        nzp = [z for z in range(nz) if round(counts[z]) > 0]
         prof = P.ProfileData()
+        prof.stream_axis = stream_axis
+        _profile_meta(prof, me.workload.params(), g, nz)
+        nzp = [z for z in range(nz) if counts[z] > 0]
         if not nzp:
             return prof
         zl, zh = nzp[0], nzp[-1]
         zs = np.arange(zl, zh + 1)
         prof.z = zs + 0.5
         prof.u_superficial = sums[zl:zh + 1] / plane
-        cnt = np.round(counts[zl:zh + 1])
+        cnt = counts[zl:zh + 1]
         prof.u_intrinsic = np.where(cnt > 0, sums[zl:zh + 1] / np.maximum(cnt, 1), 0.0)
         prof.epsilon = cnt / plane
-        i = int(np.argmax(np.abs(prof.u_superficial)))
-        prof.u_max = float(prof.u_superficial[i])
-        prof.u_normalized = prof.u_superficial / prof.u_max if prof.u_max else 0 * prof.z
-        prof.stream_axis = stream_axis
+        u_max = 0.0
+        for v in prof.u_superficial:  # profile.cpp:10-19 (first largest |u|)
+            if abs(v) > abs(u_max):
+                u_max = float(v)
+        prof.u_max = u_max
+        prof.u_normalized = prof.u_superficial / u_max if u_max != 0.0 else 0 * prof.z
         return prof
 
     def max_speed(self) -> float:
@@ -210,38 +271,78 @@ class DistTransport:
         return float(np.sqrt(v2)) if fin > 0 else float("nan")
 
 
-class SlabSimulation(DistTransport):
-    """The rank-local handle bench.py uses: SlabSimulation(workload, rank, world)."""
+class SlabSimulation:
+    """One rank's slab (the handle bench.py uses): SlabSimulation(workload,
+    rank, world).  CUDA: the native driver in NCCL mode (the unique id travels
+    over torch.distributed when it is initialised); CPU engines: DistTransport."""
 
     def __init__(self, workload, rank: int, world: int, device=0, group=None, engine=None,
                  geometry=None):
-        super().__init__(SlabRank(workload, rank, world, device, engine, geometry=geometry), group)
+        self.me = SlabRank(workload, rank, world, device, engine, geometry=geometry)
         self.sim = self.me.sim
+        self.workload = workload
+        self._cpu = None
+        self.native = None
+        if engine is not None:
+            self._cpu = DistTransport(self.me, group)
+            return
+        nid = None
+        import torch.distributed as tdist
+        if world > 1 and tdist.is_available() and tdist.is_initialized():
+            obj = [NativeDist.nccl_unique_id() if rank == 0 else None]
+            tdist.broadcast_object_list(obj, src=0, group=group)
+            nid = obj[0]
+        elif world == 1:
+            nid = NativeDist.nccl_unique_id()
+        else:
+            raise P.ConfigError("world > 1 needs torch.distributed initialised (NCCL id exchange)")
+        self.native = NativeDist([self.sim], nccl_id=nid, rank=rank, world=world)
 
-    def set_stream(self, stream) -> None:
-        self.me.stream = stream
-        self.sim.set_stream(stream.cuda_stream)
+    def step(self, n: int = 1) -> None:
+        (self._cpu or self.native).step(n)
+
+    def planar_profile(self, stream_axis: int = 0) -> P.ProfileData:
+        return (self._cpu or self.native).planar_profile(stream_axis)
+
+    def max_speed(self) -> float:
+        return (self._cpu or self.native).max_speed()
+
+    def fluid_cells(self) -> int:
+        if self._cpu is not None:
+            return self._cpu.fluid_cells()
+        return int(self.workload_fluid_total())
+
+    def workload_fluid_total(self) -> int:
+        counts = np.round(np.asarray(self.me.geometry.porosity) * self.me.geometry.dims[0]
+                          * self.me.geometry.dims[1])
+        import torch.distributed as tdist
+        if self.me.world > 1 and tdist.is_initialized():
+            import torch
+            t = torch.tensor([counts.sum()], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(t)
+            return int(t.item())
+        return int(counts.sum())
+
+    def close(self) -> None:
+        if self.native is not None:
+            self.native.close()
 
 
 class LocalTransport:
-    """All slabs of a decomposition in ONE process on one device.  Each step
-    runs every slab's edge part, then the exchanges (device copies), then the
-    interior parts -- sequentially, so no kernel waits on another.  Used to
-    verify the decomposition bit-for-bit on one GPU (and on CPU engines)."""
+    """All slabs of a decomposition in ONE process: on the GPU the native
+    driver in local mode (peer copies; edge and interior parts on two streams
+    per slab), for CPU engines the same steps in order.  Verifies the
+    decomposition bit for bit against the single domain on one device."""
 
     def __init__(self, workload, world: int, device=0, engine=None):
-        import torch
-
-        self.stream = None if engine is not None else torch.cuda.Stream(device=int(device))
-        self.ranks = [SlabRank(workload, r, world, device, engine, self.stream)
-                      for r in range(world)]
         self.world = world
+        self.ranks = [SlabRank(workload, r, world, device, engine) for r in range(world)]
+        self.native = None if engine is not None else NativeDist([r.sim for r in self.ranks])
 
     def step(self, n: int = 1) -> None:
-        with _on(self.stream):
-            self._step(n)
-
-    def _step(self, n: int) -> None:
+        if self.native is not None:
+            self.native.step(n)
+            return
         R, W = self.ranks, self.world
         for _ in range(int(n)):
             for r in R:
@@ -255,6 +356,12 @@ class LocalTransport:
                 r.sim.step_part(1)
             for r in R:
                 r.sim.step_finish()
+
+    def planar_profile(self, stream_axis: int = 0) -> P.ProfileData:
+        return self.native.planar_profile(stream_axis)
+
+    def max_speed(self) -> float:
+        return self.native.max_speed()
 
     def gather_pdfs(self) -> np.ndarray:
         """Global f(n) (19, nz, ny, nx) assembled from the slabs."""

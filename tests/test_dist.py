@@ -64,9 +64,10 @@ def _worker(rank, world, port, scheme, q):
         s = SlabSimulation(w, rank, world, engine=OracleSlabSim)
         s.step(w.steps)
         prof = s.planar_profile()
-        q.put((rank, s.sim.get_pdfs(), prof.u_superficial, s.max_speed(), s.fluid_cells()))
+        meta = (prof.height, prof.z0, prof.nu, tuple(prof.body_force), prof.u_max)
+        q.put((rank, s.sim.get_pdfs(), prof.u_superficial, s.max_speed(), s.fluid_cells(), meta))
       except Exception as exc:  # report instead of hanging the parent
-        q.put((rank, repr(exc), None, None, None))
+        q.put((rank, repr(exc), None, None, None, None))
         raise
     finally:
         dist.destroy_process_group()
@@ -98,7 +99,13 @@ def test_gloo_two_ranks(scheme):
     o = OracleLib().simulation(g, p.nu, p.omega_plus, p.omega_minus, p.body_force, int(w.scheme))
     o.step(w.steps)
     ref = o.planar_profile()["u_superficial"]
+    oprof = o.planar_profile()
     for r in res:
         np.testing.assert_allclose(r[2], ref, rtol=1e-12, atol=1e-300)
+        # ProfileData metadata as simulation.cpp:386-397 fills it
+        height, z0, nu, g_, u_max = r[5]
+        assert (height, z0, nu) == (oprof["height"], oprof["z0"], p.nu)
+        assert g_ == tuple(p.body_force)
+        assert u_max == pytest.approx(oprof["u_max"], rel=1e-12)
         assert r[3] == pytest.approx(o.max_speed(), rel=1e-12)
         assert r[4] == g.fluid_cells

@@ -41,3 +41,18 @@ def test_dns_dropin_resolve_drive(gpu, ref):
     assert int(got["steps"]) == st["steps"] and int(got["converged"]) == int(st["converged"])
     assert float(got["u_max"]) == r.planar_profile()["u_max"]
     assert float(got["eps_wall"]) == 0.0 and float(got["eps_mid"]) == 1.0
+
+
+def test_dist_demo_cpp_multi_gpu_host_path(gpu):
+    """DistSimulation (C++ over csrc/dist.cpp): 2 and 3 slabs through the local
+    transport, and the NCCL transport at world size 1 (periodic self-exchange,
+    CUDA-graph replay) -- both bit-identical to the single domain."""
+    exe = Path(__file__).resolve().parent / "cpp" / "dist_demo"
+    assert exe.exists(), "build with python paper_1507_06565_b200/build.py"
+    for args in (["256", "64", "96", "2", "23"], ["192", "40", "64", "3", "16"]):
+        res = subprocess.run([str(exe), *args], capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stdout + res.stderr
+        out = json.loads(res.stdout)
+        assert out["local_bitwise"] and out["local_profile"] and out["local_vmax_equal"], out
+        assert out["nccl_error"] == "", out["nccl_error"]
+        assert out["nccl_bitwise"] and out["nccl_profile"] and out["nccl_vmax_equal"], out

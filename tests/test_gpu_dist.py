@@ -36,6 +36,32 @@ def bed_workload(pg, scheme, nx=128, glbm=False):
     return w
 
 
+@pytest.mark.parametrize("nx,world", [(200, 2), (96, 2), (96, 3)])
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_slabs_not_warp_multiples(gpu, nx, world, scheme):
+    """Slab widths that are not multiples of 32 (100: 32-column per-cell edge
+    bands + masked interior chunks; 48 and 32: face-column edge bands), the
+    native local transport against the single domain, bit for bit, plus the
+    global profile (metadata exact, values within 1e-12) and max speed."""
+    pg = gpu
+    from paper_1507_06565_b200 import configs
+    from paper_1507_06565_b200.dist import LocalTransport
+    w = bed_workload(pg, scheme, nx=nx)
+    lt = LocalTransport(w, world, device=0)
+    lt.step(w.steps)
+    g = w.geometry()
+    sim = configs.make_simulation(w, g)
+    sim.step(w.steps)
+    fl = g.flags.reshape(w.dims[::-1]) == 0
+    assert np.array_equal(lt.gather_pdfs()[:, fl], sim.get_pdfs()[:, fl])
+    a, b = lt.planar_profile(), sim.planar_profile()
+    assert np.array_equal(a.z, b.z) and np.array_equal(a.epsilon, b.epsilon)
+    assert (a.height, a.z0, a.nu, tuple(a.body_force), a.stream_axis) == \
+        (b.height, b.z0, b.nu, tuple(b.body_force), b.stream_axis)
+    assert np.abs(a.u_superficial - b.u_superficial).max() <= 1e-12 * abs(b.u_max)
+    assert lt.max_speed() == sim.max_speed()
+
+
 @pytest.mark.parametrize("world", [1, 2, 4])
 @pytest.mark.parametrize("scheme", [0, 1])
 def test_slabs_match_single_domain(gpu, orc, world, scheme):
@@ -75,10 +101,11 @@ def test_slabs_glbm(gpu):
 
 @pytest.mark.parametrize("scheme", [0, 1])
 def test_dist_transport_two_streams_single_rank(gpu, scheme):
-    """DistTransport's two-stream schedule (edge part + exchange on one stream,
-    interior on another, cross-step events only) at world size 1, where the
-    exchange is the periodic self-copy: bit-identical to the single domain,
-    also when observables and more steps interleave."""
+    """SlabSimulation at world size 1: the native NCCL driver (edge part +
+    exchange on the high-priority stream, interior on the simulation's stream,
+    two-step CUDA-graph replays) with the periodic exchange going through
+    ncclSend/ncclRecv to self: bit-identical to the single domain, also when
+    observables and more steps interleave."""
     pg = gpu
     from paper_1507_06565_b200 import configs
     from paper_1507_06565_b200.dist import SlabSimulation
@@ -93,6 +120,10 @@ def test_dist_transport_two_streams_single_rank(gpu, scheme):
         got = ss.sim.get_pdfs()
         assert np.array_equal(got[:, fl], sim.get_pdfs()[:, fl]), n
     assert ss.max_speed() == sim.max_speed()
+    a, b = ss.planar_profile(), sim.planar_profile()
+    assert (a.height, a.z0, a.nu, tuple(a.body_force)) == (b.height, b.z0, b.nu,
+                                                           tuple(b.body_force))
+    ss.close()
 
 
 @pytest.mark.parametrize("scheme", [0, 1])
