@@ -152,13 +152,14 @@ def ncu_traffic(config_name: str, math: str, kernel_hash: str):
         return None
 
 
-def config_dict(name, fluid, cells, links, scheme, world, meta):
+def config_dict(name, fluid, cells, links, scheme, world, meta, slab=None):
     """The `config` of the JSON line, identical in both arms."""
+    slab = world > 1 if slab is None else slab
     return {"workload": name, "fluid_cells": int(fluid), "cells": int(cells),
             "links": int(links), "scheme": scheme,
             "l2": "inputs larger than L2 (2 x 19 x cells x 8 B > 126 MB)"
             if 2 * 19 * 8 * cells > 126e6 else "state L2-resident",
-            "parallelism": f"x-slab{world}" if world > 1 else "single", **meta}
+            "parallelism": f"x-slab{world}" if slab else "single", **meta}
 
 
 # ---------------------------------------------------------------------------
@@ -370,7 +371,7 @@ def run_ours(args):
             "data": "synthetic",
             "config": config_dict(w.name, fluid_total, int(np.prod(w.dims)) if world == 1
                                   else int(np.prod(w.dims)), links_total, w.scheme.name,
-                                  world if (world > 1 or not args.force_slab) else 1, w.meta),
+                                  world, w.meta, slab=world > 1 or args.force_slab),
             "math": args.math,
             "roofline": roofline,
             "cpu_baseline": cpu,

@@ -115,12 +115,24 @@ struct pgpu_dist {
   int64_t halo_n = 0;
   double* d_red = nullptr;  // NCCL reductions (nz + 2 doubles)
   bool graphs = true;
-  cudaGraphExec_t gexec = nullptr;
+  // two-step graphs keyed by the state they were captured in (sweep buffer
+  // parity `cur`, ghost parity): the kernels' pointers are baked in, and an
+  // observable or an odd number of eager steps changes the parities
+  cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   cudaStream_t gstream = nullptr;
   int64_t glaunches = 0;  // kernels per graph replay (two steps)
 
+  void drop_graphs() {
+    for (auto& row : gexec)
+      for (auto& g : row)
+        if (g) {
+          cudaGraphExecDestroy(g);
+          g = nullptr;
+        }
+  }
+
   ~pgpu_dist() {
-    if (gexec) cudaGraphExecDestroy(gexec);
+    drop_graphs();
     for (auto& r : ranks) {
       cudaSetDevice(r.sim->device);
       cudaStreamSynchronize(r.edge);
@@ -243,6 +255,7 @@ struct pgpu_dist {
   void capture() {  // NCCL mode, post state: a graph of two steps
     DistRank& r = ranks[0];
     pgpu_sim* s = r.sim;
+    cudaGraphExec_t& gexec = this->gexec[s->cur][s->ghost_cur];
     join();
     r.have_prev = false;  // consecutive replays are ordered by the stream
     const int64_t l0 = s->launches;
@@ -278,10 +291,8 @@ struct pgpu_dist {
       DistRank& r0 = ranks[0];
       const bool graphable = use_nccl && graphs && r0.sim->post && n - i >= 2;
       if (graphable) {
-        if (gexec && gstream != r0.sim->stream) {
-          cudaGraphExecDestroy(gexec);
-          gexec = nullptr;
-        }
+        if (gstream != r0.sim->stream) drop_graphs();  // pgpu_set_stream since the capture
+        cudaGraphExec_t gexec = this->gexec[r0.sim->cur][r0.sim->ghost_cur];
         if (!gexec) {
           capture();
           i += 2;

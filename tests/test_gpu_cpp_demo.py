@@ -52,7 +52,8 @@ def test_dist_demo_cpp_multi_gpu_host_path(gpu):
     for args in (["256", "64", "96", "2", "23"], ["192", "40", "64", "3", "16"]):
         res = subprocess.run([str(exe), *args], capture_output=True, text=True, timeout=600)
         assert res.returncode == 0, res.stdout + res.stderr
-        out = json.loads(res.stdout)
+        # (NCCL may print its version banner on stdout first)
+        out = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
         assert out["local_bitwise"] and out["local_profile"] and out["local_vmax_equal"], out
         assert out["nccl_error"] == "", out["nccl_error"]
         assert out["nccl_bitwise"] and out["nccl_profile"] and out["nccl_vmax_equal"], out
