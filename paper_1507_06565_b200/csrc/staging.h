@@ -111,16 +111,24 @@ class StagedUpload {
       return e != cudaSuccess ? e : cudaStreamSynchronize(st);
     }
     std::lock_guard<std::mutex> lock(mu_);
-    if (!stage_[0]) {
-      for (auto& b : stage_) {
-        cudaError_t e = cudaHostAlloc(&b, chunk_, cudaHostAllocPortable);
-        if (e != cudaSuccess) return e;
+    if (!stage_[0]) {  // all slots or none: a failed allocation leaves no partial set
+      void* got[kSlots] = {nullptr, nullptr, nullptr, nullptr};
+      for (int k = 0; k < kSlots; ++k) {
+        const cudaError_t e = cudaHostAlloc(&got[k], chunk_, cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+          for (int j = 0; j < k; ++j) cudaFreeHost(got[j]);
+          return e;
+        }
       }
+      for (int k = 0; k < kSlots; ++k) stage_[k] = got[k];
     }
     cudaEvent_t ev[kSlots];
-    for (auto& e : ev) {
-      cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      if (r != cudaSuccess) return r;
+    for (int k = 0; k < kSlots; ++k) {
+      const cudaError_t r = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+      if (r != cudaSuccess) {
+        for (int j = 0; j < k; ++j) cudaEventDestroy(ev[j]);
+        return r;
+      }
     }
     cudaError_t err = cudaSuccess;
     const char* s = static_cast<const char*>(src);
