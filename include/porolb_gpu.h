@@ -255,6 +255,8 @@ int pgpu_set_math_mode(pgpu_sim* sim, int32_t mode);
 /* PDF layout chosen at creation (PGPU_LAYOUT overrides). */
 enum pgpu_layout { PGPU_LAYOUT_DENSE = 0, PGPU_LAYOUT_FLUID_ONLY = 1, PGPU_LAYOUT_DENSE_PERSISTENT = 2 };
 int pgpu_get_layout(pgpu_sim* sim, int32_t* layout);
+/* Device memory held by the simulation (PDF buffers, cell words, link data). */
+int pgpu_device_bytes(pgpu_sim* sim, int64_t* bytes);
 int pgpu_get_math_mode(pgpu_sim* sim, int32_t* mode);
 int pgpu_set_body_force(pgpu_sim* sim, const double g[3]);
 int pgpu_set_lid_velocity(pgpu_sim* sim, const double u[3]);

@@ -110,6 +110,7 @@ SIGNATURES = {
     "pgpu_porosity_profile": (C.c_int, [P(Geometry), P(f64), P(f64)]),
     "pgpu_stream_field": (C.c_int, [P(i32), P(u8), P(u8), P(f64), P(f64), i32]),
     "pgpu_get_layout": (C.c_int, [vp, P(i32)]),
+    "pgpu_device_bytes": (C.c_int, [vp, P(i64)]),
     "pgpu_get_math_mode": (C.c_int, [vp, P(i32)]),
     "pgpu_set_body_force": (C.c_int, [vp, P(f64)]),
     "pgpu_set_lid_velocity": (C.c_int, [vp, P(f64)]),

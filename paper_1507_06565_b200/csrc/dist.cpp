@@ -203,6 +203,7 @@ struct pgpu_dist {
       CK(cudaEventRecord(r.ev_edge[r.parity], r.edge));
     }
     // exchange: fill the ghost parity the next step reads
+    Nvtx nv("halo exchange (5 PDFs per face)");
     if (use_nccl) {
       DistRank& r = ranks[0];
       const int p = 1 - r.sim->ghost_cur;

@@ -600,14 +600,17 @@ __global__ void __launch_bounds__(128) k_collide_inplace(const KParams p, double
 // ---------------------------------------------------------------------------
 // Observables from a pre-collision state f (simulation.cpp:354-434).
 // ---------------------------------------------------------------------------
-// moments(): lattice.cpp:88-101, literal order over k = 0..18.
+// moments(): lattice.cpp:88-101, literal order over k = 0..18.  `slot` and
+// `stride`: the cell's element and the plane stride of the state's layout
+// (dense: cell index / ksd; fluid-only: compact slot / ks).
 template <bool GLBM>
 __device__ __forceinline__ bool macro_cell(const KParams& p, const double* __restrict__ f,
-                                           int64_t c, int z, double& drho, double (&u)[3]) {
+                                           int64_t slot, int64_t stride, int z, double& drho,
+                                           double (&u)[3]) {
   double d = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0;
 #pragma unroll
   for (int k = 0; k < 19; ++k) {
-    const double fk = f[(int64_t)k * p.ksd + c];
+    const double fk = f[(int64_t)k * stride + slot];
     d = DADD(d, fk);
     v0 = DADD(v0, DMUL((double)EX[k], fk));
     v1 = DADD(v1, DMUL((double)EY[k], fk));
@@ -637,7 +640,7 @@ __device__ __forceinline__ bool macro_cell(const KParams& p, const double* __res
   return !(disc < 0.0);
 }
 
-template <bool GLBM>
+template <bool GLBM, bool COMPACT>
 __global__ void k_macro_fields(const KParams p, const double* __restrict__ f, double* drho,
                                double* ux, double* uy, double* uz, int* err) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -652,7 +655,8 @@ __global__ void k_macro_fields(const KParams p, const double* __restrict__ f, do
     return;
   }
   double d, u[3];
-  if (!macro_cell<GLBM>(p, f, c, z, d, u)) atomicOr(err, 1);
+  const int64_t slot = COMPACT ? compact_slot(p, x, y, z) : c;
+  if (!macro_cell<GLBM>(p, f, slot, COMPACT ? p.ks : p.ksd, z, d, u)) atomicOr(err, 1);
   if (drho) drho[c] = d;
   if (ux) ux[c] = u[0];
   if (uy) uy[c] = u[1];
@@ -695,7 +699,7 @@ __global__ void __launch_bounds__(256) k_plane_sums(const double* __restrict__ u
 }
 
 // max |u|^2 and finiteness over fluid cells (simulation.cpp:419-434).
-template <bool GLBM>
+template <bool GLBM, bool COMPACT>
 __global__ void k_max_speed2(const KParams p, const double* __restrict__ f,
                              unsigned long long* vmax2_bits, int* nonfinite, int* err) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -706,7 +710,8 @@ __global__ void k_max_speed2(const KParams p, const double* __restrict__ f,
     const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
     if (!(p.cellw[c] & kNonFluid)) {
       double d, u[3];
-      if (!macro_cell<GLBM>(p, f, c, z, d, u)) atomicOr(err, 1);
+      const int64_t slot = COMPACT ? compact_slot(p, x, y, z) : c;
+      if (!macro_cell<GLBM>(p, f, slot, COMPACT ? p.ks : p.ksd, z, d, u)) atomicOr(err, 1);
       m2 = DADD(DADD(DMUL(u[0], u[0]), DMUL(u[1], u[1])), DMUL(u[2], u[2]));
       bad = !(isfinite(m2) && isfinite(d));
       if (!(m2 > 0.0)) m2 = 0.0;  // std::max(vmax2, m2) ignores NaN and keeps 0
@@ -936,10 +941,14 @@ void launch_collide_inplace(bool glbm, bool slab, const KParams& p, double* buf,
 
 void launch_macro_fields(bool glbm, const KParams& p, const double* f, double* drho,
                          double* ux, double* uy, double* uz, int* err, cudaStream_t s) {
-  if (glbm)
-    k_macro_fields<true><<<cell_grid2(p), cell_block(p), 0, s>>>(p, f, drho, ux, uy, uz, err);
-  else
-    k_macro_fields<false><<<cell_grid2(p), cell_block(p), 0, s>>>(p, f, drho, ux, uy, uz, err);
+  const dim3 g = cell_grid2(p), b = cell_block(p);
+  if (p.ctab) {
+    if (glbm) k_macro_fields<true, true><<<g, b, 0, s>>>(p, f, drho, ux, uy, uz, err);
+    else k_macro_fields<false, true><<<g, b, 0, s>>>(p, f, drho, ux, uy, uz, err);
+  } else {
+    if (glbm) k_macro_fields<true, false><<<g, b, 0, s>>>(p, f, drho, ux, uy, uz, err);
+    else k_macro_fields<false, false><<<g, b, 0, s>>>(p, f, drho, ux, uy, uz, err);
+  }
 }
 
 void launch_plane_sums(const KParams& p, const double* u, double* sums, cudaStream_t s) {
@@ -950,11 +959,14 @@ void launch_plane_sums(const KParams& p, const double* u, double* sums, cudaStre
 void launch_max_speed2(bool glbm, const KParams& p, const double* f,
                        unsigned long long* vmax2_bits, int* nonfinite, int* err,
                        cudaStream_t s) {
-  if (glbm)
-    k_max_speed2<true><<<cell_grid2(p), cell_block(p), 0, s>>>(p, f, vmax2_bits, nonfinite, err);
-  else
-    k_max_speed2<false><<<cell_grid2(p), cell_block(p), 0, s>>>(p, f, vmax2_bits, nonfinite,
-                                                                err);
+  const dim3 g = cell_grid2(p), b = cell_block(p);
+  if (p.ctab) {
+    if (glbm) k_max_speed2<true, true><<<g, b, 0, s>>>(p, f, vmax2_bits, nonfinite, err);
+    else k_max_speed2<false, true><<<g, b, 0, s>>>(p, f, vmax2_bits, nonfinite, err);
+  } else {
+    if (glbm) k_max_speed2<true, false><<<g, b, 0, s>>>(p, f, vmax2_bits, nonfinite, err);
+    else k_max_speed2<false, false><<<g, b, 0, s>>>(p, f, vmax2_bits, nonfinite, err);
+  }
 }
 
 void launch_fill_equilibrium(const KParams& p, int64_t cells, double* f, const double* feq,
@@ -967,11 +979,15 @@ void launch_fill_equilibrium(const KParams& p, int64_t cells, double* f, const d
 // lazily at first launch, ~10 ms on the first observable otherwise).
 void preload_kernels() {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, k_macro_fields<true>);
-  cudaFuncGetAttributes(&a, k_macro_fields<false>);
+  cudaFuncGetAttributes(&a, k_macro_fields<true, false>);
+  cudaFuncGetAttributes(&a, k_macro_fields<false, false>);
+  cudaFuncGetAttributes(&a, k_macro_fields<true, true>);
+  cudaFuncGetAttributes(&a, k_macro_fields<false, true>);
   cudaFuncGetAttributes(&a, k_plane_sums);
-  cudaFuncGetAttributes(&a, k_max_speed2<true>);
-  cudaFuncGetAttributes(&a, k_max_speed2<false>);
+  cudaFuncGetAttributes(&a, k_max_speed2<true, false>);
+  cudaFuncGetAttributes(&a, k_max_speed2<false, false>);
+  cudaFuncGetAttributes(&a, k_max_speed2<true, true>);
+  cudaFuncGetAttributes(&a, k_max_speed2<false, true>);
   cudaFuncGetAttributes(&a, k_fill_equilibrium);
   cudaGetLastError();
 }

@@ -16,16 +16,23 @@ struct SweepConfig {
 };
 
 // Dense layout (kernels.cu) or, when p.ctab is set, the fluid-only layout
-// (sweep_compact.cu).  In the fluid-only layout op 1 (KP) writes the dense
-// observable buffer (plane stride p.ksd).
+// (sweep_compact.cu); op 1 (KP) writes f(n) into the other buffer of the
+// same layout.
 void launch_sweep(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
                   cudaStream_t s);
 void launch_sweep_compact(const SweepConfig& cfg, const KParams& p, const double* src,
                           double* dst, cudaStream_t s);
-// K0 of the fluid-only layout: dense pre-collision state -> compact post state
-// (with records in math mode fast: folded CLI slots, kparams.h KParams::fast).
-void launch_collide_to_compact(bool glbm, bool slab, bool records, const KParams& p,
-                               const double* dense, double* dst, cudaStream_t s);
+// K0 of the fluid-only layout: pre-collision f(n) -> post-collision g(n) in
+// place (with records in math mode fast + PGPU_FOLD: folded CLI slots).
+void launch_collide_compact(bool glbm, bool slab, bool records, const KParams& p, double* buf,
+                            cudaStream_t s);
+// Population I/O of the fluid-only layout through a reference-layout staging
+// buffer of the planes [z0, z0 + nzc): expand (compact -> dense) or pack.
+void launch_compact_io(bool expand, const KParams& p, double* f, double* dense, int z0, int nzc,
+                       cudaStream_t s);
+// initialize_equilibrium in the fluid-only layout (every fluid slot = feq)
+void launch_fill_compact(const KParams& p, int64_t nfluid, double* f, const double* feq,
+                         cudaStream_t s);
 // One cooperative launch running nsteps K1 sweeps (a -> b -> a ...); returns 0
 // on success, -1 if the cooperative launch is not possible.
 int launch_sweep_persistent(const SweepConfig& cfg, const KParams& p, double* a, double* b,

@@ -86,7 +86,8 @@ struct KParams {
   int64_t ks;          // element stride between the 19 direction planes of the sweep buffers
   int64_t ksd;         // plane stride of the dense (observable) layout, cells rounded to 32
   const ChunkEnt* ctab;  // compact layout: [rows][nchunk] chunk entries (null: dense layout)
-  int32_t poff[19];      // compact layout: j * ks (19 * ks < 2^31 is checked at creation)
+  uint32_t poff[19];     // compact layout: j * ks; slot offsets are 32-bit unsigned
+                         // (19 * ks < 2^32, i.e. up to 226 M fluid cells per GPU)
   const uint32_t* cellw;     // per-cell word (kNonFluid / bounce bits / kFillSector)
   const int32_t* cellbase;   // per-cell first link record (per-cell kernels)
   const int32_t* chunkbase;  // first link record of each 32-cell chunk of a row

@@ -44,6 +44,12 @@ __device__ __forceinline__ bool in_edge_band(int x, int nx) {
   return x < w || x >= nx - w;
 }
 
+// Fluid-only layout: slot of fluid cell (x, y, z) from its row chunk entry.
+__device__ __forceinline__ int64_t compact_slot(const KParams& p, int x, int y, int z) {
+  const ChunkEnt e = p.ctab[((int64_t)z * p.ny + y) * p.nchunk + (x >> 5)];
+  return (int64_t)e.rank + __popc(e.mask & ((1u << (x & 31)) - 1u));
+}
+
 // ---------------------------------------------------------------------------
 // Collision: simulation.cpp:150-196 (core) and :198-274 (GLBM), literal order.
 // ---------------------------------------------------------------------------

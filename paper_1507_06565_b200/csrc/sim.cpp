@@ -318,22 +318,18 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
         CK(cudaMalloc(&s->d_ctab, sizeof(ChunkEnt) * rows * s->kp.nchunk));
         const int64_t nf = build_ctab(s->d_cellw, s->nx, rows, s->kp.nchunk, s->d_ctab, s->stream);
         const int64_t ksc = std::max<int64_t>(32, (nf + 31) / 32 * 32);
-        // 32-bit slot offsets must reach all 19 planes
-        s->compact = 19 * ksc < (int64_t)std::numeric_limits<int32_t>::max() &&
+        // unsigned 32-bit slot offsets must reach all 19 planes (226 M fluid cells)
+        s->compact = 19 * ksc <= (int64_t)std::numeric_limits<uint32_t>::max() &&
                      (e || (double)nf < 0.97 * (double)s->cells);
         if (s->compact) {
           sweep_ks = ksc;
+          s->nfluid_slots = nf;
           s->persistent = false;
         } else {
           CK(cudaFree(s->d_ctab));
           s->d_ctab = nullptr;
         }
       }
-    }
-    if (s->compact) {
-      const size_t pbytes = sizeof(double) * 19 * (size_t)s->ks;
-      CK(cudaMalloc(&s->pre, pbytes));
-      CK(cudaMemsetAsync(s->pre, 0, pbytes, s->stream));
     }
     // device buffers: two PDF grids, zero-filled like the reference
     const size_t fbytes = sizeof(double) * 19 * (size_t)sweep_ks;
@@ -355,7 +351,7 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     kp.ks = sweep_ks;
     kp.ksd = s->ks;
     kp.ctab = s->d_ctab;
-    for (int j = 0; j < 19; ++j) kp.poff[j] = s->compact ? (int32_t)(j * sweep_ks) : 0;
+    for (int j = 0; j < 19; ++j) kp.poff[j] = s->compact ? (uint32_t)(j * sweep_ks) : 0u;
     for (int j = 0; j < 19; ++j) {
       const int64_t d = kE[j][0] + (int64_t)kE[j][1] * s->nx + (int64_t)kE[j][2] * s->nx * s->ny;
       kp.pull_off[j] = (int64_t)j * s->ks - d;
@@ -427,6 +423,13 @@ int pgpu_set_math_mode(pgpu_sim* sim, int32_t mode) {
     sim->fast = want;
     sim->refresh_params();
     sim->sync();
+  });
+}
+
+int pgpu_device_bytes(pgpu_sim* sim, int64_t* bytes) {
+  return guard([&] {
+    SIM_CHECK();
+    *bytes = sim->device_bytes();
   });
 }
 
@@ -515,11 +518,14 @@ int pgpu_initialize_equilibrium(pgpu_sim* sim, double delta_rho, const double u[
     double feq[19];
     equilibrium(delta_rho, u, sim->params.rho0, feq);
     if (sim->post) {  // the dead buffer becomes the pre-collision state
-      if (!sim->compact) sim->cur = 1 - sim->cur;
+      sim->cur = 1 - sim->cur;
       sim->post = false;
     }
     CK(cudaMemcpyAsync(sim->d_feq, feq, sizeof(feq), cudaMemcpyHostToDevice, sim->stream));
-    launch_fill_equilibrium(sim->kp, sim->cells, sim->pre_buf(), sim->d_feq, sim->stream);
+    if (sim->compact)
+      launch_fill_compact(sim->kp, sim->nfluid_slots, sim->pre_buf(), sim->d_feq, sim->stream);
+    else
+      launch_fill_equilibrium(sim->kp, sim->cells, sim->pre_buf(), sim->d_feq, sim->stream);
     sim->check_launch();
     ++sim->launches;
     sim->sync();
@@ -581,9 +587,25 @@ int pgpu_get_pdfs(pgpu_sim* sim, double* out) {
     SIM_CHECK();
     if (!out) throw std::invalid_argument("null output");
     sim->ensure_pre();
-    CK(cudaMemcpy2DAsync(out, sim->cells * sizeof(double), sim->pre_buf(),
-                         sim->ks * sizeof(double), sim->cells * sizeof(double), 19,
-                         cudaMemcpyDeviceToHost, sim->stream));
+    if (!sim->compact) {
+      CK(cudaMemcpy2DAsync(out, sim->cells * sizeof(double), sim->pre_buf(),
+                           sim->ks * sizeof(double), sim->cells * sizeof(double), 19,
+                           cudaMemcpyDeviceToHost, sim->stream));
+    } else {  // expand z-chunks into the dead sweep buffer, then copy each out
+      Nvtx r("get_pdfs expand");
+      const int64_t plane = (int64_t)sim->nx * sim->ny;
+      double* stage = sim->f[1 - sim->cur];
+      for (int z0 = 0; z0 < sim->nz; z0 += sim->io_planes()) {
+        const int nzc = std::min(sim->io_planes(), sim->nz - z0);
+        if (z0) CK(cudaStreamSynchronize(sim->stream));  // staging reused
+        launch_compact_io(true, sim->kp, sim->pre_buf(), stage, z0, nzc, sim->stream);
+        sim->check_launch();
+        ++sim->launches;
+        const size_t w = sizeof(double) * (size_t)(nzc * plane);
+        CK(cudaMemcpy2DAsync(out + z0 * plane, sim->cells * sizeof(double), stage, w, w, 19,
+                             cudaMemcpyDeviceToHost, sim->stream));
+      }
+    }
     sim->sync();
   });
 }
@@ -594,11 +616,25 @@ int pgpu_set_pdfs(pgpu_sim* sim, const double* in) {
     if (!in) throw std::invalid_argument("null input");
     if (sim->slab && sim->pending) throw ConfigError("split step in progress");
     sim->sync();
-    if (sim->post && !sim->compact) sim->cur = 1 - sim->cur;
+    if (sim->post) sim->cur = 1 - sim->cur;
     sim->post = false;
-    CK(cudaMemcpy2DAsync(sim->pre_buf(), sim->ks * sizeof(double), in,
-                         sim->cells * sizeof(double), sim->cells * sizeof(double), 19,
-                         cudaMemcpyHostToDevice, sim->stream));
+    if (!sim->compact) {
+      CK(cudaMemcpy2DAsync(sim->pre_buf(), sim->ks * sizeof(double), in,
+                           sim->cells * sizeof(double), sim->cells * sizeof(double), 19,
+                           cudaMemcpyHostToDevice, sim->stream));
+    } else {  // z-chunks through the dead sweep buffer, packed into fluid slots
+      const int64_t plane = (int64_t)sim->nx * sim->ny;
+      double* stage = sim->f[1 - sim->cur];
+      for (int z0 = 0; z0 < sim->nz; z0 += sim->io_planes()) {
+        const int nzc = std::min(sim->io_planes(), sim->nz - z0);
+        const size_t w = sizeof(double) * (size_t)(nzc * plane);
+        CK(cudaMemcpy2DAsync(stage, w, in + z0 * plane, sim->cells * sizeof(double), w, 19,
+                             cudaMemcpyHostToDevice, sim->stream));
+        launch_compact_io(false, sim->kp, sim->pre_buf(), stage, z0, nzc, sim->stream);
+        sim->check_launch();
+        ++sim->launches;
+      }
+    }
     sim->sync();
   });
 }
@@ -615,7 +651,14 @@ int pgpu_set_cell_populations(pgpu_sim* sim, int64_t cell, const double in[19]) 
     SIM_CHECK();
     if (cell < 0 || cell >= sim->cells) throw ConfigError("cell index out of range");
     sim->ensure_pre();
-    CK(cudaMemcpy2DAsync(sim->pre_buf() + cell, sim->ks * sizeof(double), in, sizeof(double),
+    int64_t slot = cell, stride = sim->ks;
+    if (sim->compact) {
+      sim->sync();
+      slot = sim->compact_slot_of(cell);
+      stride = sim->kp.ks;
+      if (slot < 0) return;  // non-fluid cells hold no populations in this layout
+    }
+    CK(cudaMemcpy2DAsync(sim->pre_buf() + slot, stride * sizeof(double), in, sizeof(double),
                          sizeof(double), 19, cudaMemcpyHostToDevice, sim->stream));
     sim->sync();
   });

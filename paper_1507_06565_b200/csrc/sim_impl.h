@@ -16,6 +16,18 @@
 #include "kernels.h"
 #include "kparams.h"
 #include "setup.h"
+#include <nvtx3/nvToolsExt.h>  // header-only; no cost without a profiler attached
+
+namespace pgpu {
+// NVTX range for the host-side issue of a phase (K0, K1 parts, KP, halo
+// exchange): visible in nsys / ncu --nvtx timelines next to the kernels.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
+}  // namespace pgpu
 
 namespace pgpu {
 void moments(const double f[19], double rho0, double& drho, double u[3]);
@@ -67,13 +79,13 @@ struct pgpu_sim {
   std::vector<double> eps, K, gwp, gwm;
   double cf = 0.0;
   bool eps_in_eq = true;
-  // device memory.  Dense layout: f[0]/f[1] hold both the pre-collision and
-  // the post-collision states.  Fluid-only ("compact") layout: f[0]/f[1] are
-  // the post-collision sweep buffers (plane stride kp.ks) and `pre` holds the
-  // pre-collision state in the reference's dense layout (plane stride ks).
+  // device memory: f[0]/f[1] hold the pre-collision state f(n) (in f[cur],
+  // "pre") or the post-collision state g(n-1) ("post"), in the dense layout
+  // (plane stride ks) or the fluid-only one (plane stride kp.ks); population
+  // I/O of the fluid-only layout stages through the dead buffer.
   double* f[2] = {nullptr, nullptr};
   bool compact = false;
-  double* pre = nullptr;
+  int64_t nfluid_slots = 0;  // fluid-only layout: fluid cells (slots 0..n-1 of every plane)
   ChunkEnt* d_ctab = nullptr;
   double* d_scratch = nullptr;  // compact layout: observable scratch when f[1-cur] is too small
   int64_t scratch_n = 0;
@@ -116,7 +128,6 @@ struct pgpu_sim {
       if (g) cudaGraphExecDestroy(g);
     cudaSetDevice(device);
     for (double* p : f) cudaFree(p);
-    cudaFree(pre);
     cudaFree(d_ctab);
     cudaFree(d_scratch);
     cudaFree(d_cellw);
@@ -305,8 +316,40 @@ struct pgpu_sim {
 
   void check_launch() { CK(cudaGetLastError()); }
 
-  // buffer holding the pre-collision state (valid when !post)
-  double* pre_buf() const { return compact ? pre : f[cur]; }
+  // device memory held by this simulation (its resident allocations)
+  int64_t device_bytes() const {
+    const int64_t rows = (int64_t)ny * nz, nch = kp.nchunk;
+    int64_t b = 2 * 19 * (int64_t)sizeof(double) * kp.ks;  // the two PDF buffers
+    b += cells * (int64_t)(sizeof(uint32_t) + sizeof(int32_t));  // cell words + record bases
+    b += (rows * nch + 1) * (int64_t)sizeof(int32_t);             // chunk record bases
+    if (d_ctab) b += rows * nch * (int64_t)sizeof(ChunkEnt);
+    if (d_recs) b += n_links * (int64_t)sizeof(LinkRec);
+    if (d_recs_fold) b += n_links * (int64_t)sizeof(LinkRec);
+    if (d_linkdesc) b += (n_links + 2) * (int64_t)sizeof(uint16_t);
+    if (d_planes) b += nz * (int64_t)sizeof(PlaneCoef);
+    if (d_scratch) b += scratch_n * (int64_t)sizeof(double);
+    b += (19 + 2 + 1 + nz) * 8;  // feq, flags, vmax, plane sums
+    return b;
+  }
+
+  // buffer holding the pre-collision state (valid when !post), in the
+  // simulation's layout (fluid-only: compact slots, plane stride kp.ks)
+  double* pre_buf() const { return f[cur]; }
+  // fluid-only layout: compact slot of a cell (-1: not fluid)
+  int64_t compact_slot_of(int64_t cell) {
+    const int x = (int)(cell % nx), y = (int)((cell / nx) % ny), z = (int)(cell / ((int64_t)nx * ny));
+    ChunkEnt e;
+    CK(cudaMemcpy(&e, d_ctab + ((int64_t)z * ny + y) * kp.nchunk + (x >> 5), sizeof(e),
+                  cudaMemcpyDeviceToHost));
+    if (!((e.mask >> (x & 31)) & 1u)) return -1;
+    return (int64_t)e.rank + __builtin_popcount(e.mask & ((1u << (x & 31)) - 1u));
+  }
+  // fluid-only layout: planes per staging chunk of the population I/O (the
+  // dead sweep buffer, 19 * kp.ks doubles, holds 19 dense planes of them)
+  int io_planes() const {
+    const int64_t plane = (int64_t)nx * ny;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(nz, kp.ks / plane));
+  }
   // n doubles of device scratch that do not alias the pre-collision state
   double* scratch(int64_t n) {
     if (19 * kp.ks >= n) return f[1 - cur];  // dead in the pre state
@@ -322,16 +365,17 @@ struct pgpu_sim {
 
   // ---- state transitions -----------------------------------------------------
   void k0() {
+    Nvtx r("K0 collide");
     set_ghost_ptrs();
     if (compact)
-      launch_collide_to_compact(glbm_active, slab, sweep_cfg(0, 0).records, kp, pre, f[cur],
-                                stream);
+      launch_collide_compact(glbm_active, slab, sweep_cfg(0, 0).records, kp, f[cur], stream);
     else
       launch_collide_inplace(glbm_active, slab, kp, f[cur], stream);
     check_launch();
     ++launches;
   }
   void k1(int part) {
+    Nvtx r(part == 0 ? "K1 sweep" : (part == 1 ? "K1 edge columns" : "K1 interior columns"));
     set_ghost_ptrs();
     launch_sweep(sweep_cfg(0, part), kp, f[cur], f[1 - cur], stream);
     check_launch();
@@ -342,11 +386,12 @@ struct pgpu_sim {
     // of a split step (slab mode) no buffer holds a consistent f(n)
     if (slab && pending) throw ConfigError("observable requested in the middle of a split step");
     if (!post) return;
+    Nvtx r("KP materialise f(n)");
     set_ghost_ptrs();
-    launch_sweep(sweep_cfg(1, 0), kp, f[cur], compact ? pre : f[1 - cur], stream);
+    launch_sweep(sweep_cfg(1, 0), kp, f[cur], f[1 - cur], stream);
     check_launch();
     ++launches;
-    if (!compact) cur = 1 - cur;
+    cur = 1 - cur;
     post = false;
   }
 
@@ -504,8 +549,18 @@ struct pgpu_sim {
   void get_cell(int64_t cell, double out[19]) {
     if (cell < 0 || cell >= cells) throw ConfigError("cell index out of range");
     ensure_pre();
-    CK(cudaMemcpy2DAsync(out, sizeof(double), pre_buf() + cell, ks * sizeof(double), sizeof(double),
-                         19, cudaMemcpyDeviceToHost, stream));
+    int64_t slot = cell, stride = ks;
+    if (compact) {
+      sync();
+      slot = compact_slot_of(cell);
+      stride = kp.ks;
+      if (slot < 0) {  // non-fluid cells hold no populations in this layout
+        for (int k = 0; k < 19; ++k) out[k] = 0.0;
+        return;
+      }
+    }
+    CK(cudaMemcpy2DAsync(out, sizeof(double), pre_buf() + slot, stride * sizeof(double),
+                         sizeof(double), 19, cudaMemcpyDeviceToHost, stream));
     sync();
   }
 

@@ -58,8 +58,7 @@ __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_gro
 // Compact index helpers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int64_t fidx(const KParams& p, int x, int y, int z) {
-  const ChunkEnt e = p.ctab[((int64_t)z * p.ny + y) * p.nchunk + (x >> 5)];
-  return (int64_t)e.rank + __popc(e.mask & ((1u << (x & 31)) - 1u));
+  return compact_slot(p, x, y, z);
 }
 
 // Source rows: row r holds the directions with (e_y, e_z) = (row_ey(r), row_ez(r)); their
@@ -270,9 +269,9 @@ __device__ __forceinline__ void csweep_cell(const KParams& p, const double* __re
 #pragma unroll
     for (int j = 0; j < 19; ++j) __stcs(dst + (int64_t)j * p.ks + fc, f[j]);
     write_sends<SLAB>(p, x, y, z, f);
-  } else {  // KP: dense observable buffer
+  } else {  // KP: f(n) into the other compact buffer
 #pragma unroll
-    for (int j = 0; j < 19; ++j) dst[(int64_t)j * p.ksd + c] = f[j];
+    for (int j = 0; j < 19; ++j) dst[(int64_t)j * p.ks + fc] = f[j];
   }
 }
 
@@ -302,29 +301,57 @@ __global__ void __launch_bounds__(128) k_csweep_edges(const KParams p,
   csweep_cell<CM, GLBM, RECORDS, SLAB, OP>(p, src, dst, x, y, z);
 }
 
-// K0: dense pre-collision f -> compact post-collision g (simulation.cpp:150-274).
+// K0: pre-collision f(n) -> post-collision g(n) in place on the compact
+// buffer (simulation.cpp:150-274).
 template <int CM, bool GLBM, bool SLAB, bool FOLD>
-__global__ void __launch_bounds__(128) k_collide_to_compact(const KParams p,
-                                                            const double* __restrict__ f0,
-                                                            double* __restrict__ dst) {
+__global__ void __launch_bounds__(128) k_collide_compact(const KParams p, double* buf) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= p.nx) return;
   const int64_t c = ((int64_t)z * p.ny + y) * p.nx + x;
   const uint32_t w = __ldg(p.cellw + c);
   if (w & kNonFluid) return;
+  const int64_t fc = fidx(p, x, y, z);
   double f[19];
 #pragma unroll
-  for (int j = 0; j < 19; ++j) f[j] = __ldg(f0 + (int64_t)j * p.ksd + c);
+  for (int j = 0; j < 19; ++j) f[j] = buf[(int64_t)j * p.ks + fc];
   collide<CM, GLBM>(f, p, z);
   if (FOLD && (w & kBounceMask)) {
     const int32_t base = __ldg(p.cellbase + c);
     fold_epilogue(f, w & kBounceMask, p, [&](int i) { return __ldg(p.links + base + i); });
   }
-  const int64_t fc = fidx(p, x, y, z);
 #pragma unroll
-  for (int j = 0; j < 19; ++j) dst[(int64_t)j * p.ks + fc] = f[j];
+  for (int j = 0; j < 19; ++j) buf[(int64_t)j * p.ks + fc] = f[j];
   write_sends<SLAB>(p, x, y, z, f);
+}
+
+// Reference-layout staging of a z-range [z0, z0 + nzc) for population I/O:
+// expand (compact -> dense, zeros in non-fluid cells) or pack (dense ->
+// compact).  `dense` holds 19 planes of nzc * nx * ny cells.
+template <bool EXPAND>
+__global__ void k_compact_io(const KParams p, double* __restrict__ f, double* __restrict__ dense,
+                             int z0, int nzc) {
+  const int64_t chunk = (int64_t)nzc * p.ny * p.nx;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= chunk) return;
+  const int x = (int)(i % p.nx), y = (int)((i / p.nx) % p.ny), z = z0 + (int)(i / ((int64_t)p.nx * p.ny));
+  const bool fluid = !(__ldg(p.cellw + ((int64_t)z * p.ny + y) * p.nx + x) & kNonFluid);
+  const int64_t fc = fluid ? fidx(p, x, y, z) : 0;
+#pragma unroll
+  for (int j = 0; j < 19; ++j) {
+    if (EXPAND)
+      dense[(int64_t)j * chunk + i] = fluid ? f[(int64_t)j * p.ks + fc] : 0.0;
+    else if (fluid)
+      f[(int64_t)j * p.ks + fc] = dense[(int64_t)j * chunk + i];
+  }
+}
+
+__global__ void k_fill_compact(const KParams p, int64_t nfluid, double* __restrict__ f,
+                               const double* __restrict__ feq) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nfluid) return;
+#pragma unroll
+  for (int j = 0; j < 19; ++j) f[(int64_t)j * p.ks + i] = feq[j];
 }
 
 // Warp-exclusive prefix sum of n; the warp total in *total.
@@ -378,7 +405,7 @@ __device__ __forceinline__ const double* wrap_src(const KParams& p, const double
 // once at setup) ride in the meta ring, the 32 lanes copy each link's record
 // and g_j(x) into a per-warp pool with the plane's populations, and close the
 // links cooperatively in shared memory before the collision.  Addresses are
-// 32-bit slot offsets from the buffer base (plane j at p.poff[j]); only lanes
+// unsigned 32-bit slot offsets from the buffer base (plane j at p.poff[j]); only lanes
 // on the periodic x faces take the general path (partner chunk / slab ghosts).
 // ---------------------------------------------------------------------------
 #ifndef PGPU_CW
@@ -439,7 +466,7 @@ __device__ __forceinline__ void bounds_ok(bool ok) {
   if (PGPU_BOUNDS && !ok) __trap();
 }
 // slot `idx` lies in direction plane `plane` of a compact buffer
-__device__ __forceinline__ bool in_plane(const KParams& p, int idx, int plane) {
+__device__ __forceinline__ bool in_plane(const KParams& p, uint32_t idx, int plane) {
   return idx >= p.poff[plane] && (int64_t)idx < (int64_t)p.poff[plane] + p.ks;
 }
 // address lies in a sweep buffer or a ghost column buffer
@@ -605,7 +632,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
       if (!(x == 0 || x == p.nx - 1)) {
 #pragma unroll
         for (int j = 0; j < 19; ++j) {
-          int idx;
+          uint32_t idx;  // unsigned: 19 * ks may exceed 2^31
           if (j == 0) {
             idx = fc;
           } else if ((cw >> j) & 1u) {
@@ -631,7 +658,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
             a = wrap_src<SLAB>(p, src, E[9 + row_of(j)], j, x, y, z);
           } else {
             const int r = row_of(j);
-            int idx = q[r] + p.poff[j];
+            uint32_t idx = q[r] + p.poff[j];
             if (EX[j] == 1) idx -= 1;
             if (EX[j] == -1) idx += (bits >> r) & 1u;
             a = src + (uint32_t)idx;
@@ -841,10 +868,9 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
             dst[(uint32_t)(li.fc + p.poff[j])] = f[j];
         }
         write_sends<SLAB>(p, x, y, z, f);
-      } else {  // KP into the dense observable buffer
-        double* const d = dst + ((int64_t)z * p.ny + y) * p.nx + x;
+      } else {  // KP: f(n) into the other compact buffer
 #pragma unroll
-        for (int j = 0; j < 19; ++j) d[(int64_t)j * p.ksd] = f[j];
+        for (int j = 0; j < 19; ++j) dst[(uint32_t)(li.fc + p.poff[j])] = f[j];
       }
     }
     cnt_cur = cnt_next;
@@ -930,15 +956,14 @@ void cdispatch_cm(const SweepConfig& cfg, const KParams& p, const double* src, d
 }
 
 template <int CM, bool FOLD>
-void collide_to_compact_cm(bool glbm, bool slab, const KParams& p, const double* dense,
-                           double* dst, cudaStream_t s) {
+void collide_compact_cm(bool glbm, bool slab, const KParams& p, double* buf, cudaStream_t s) {
   const dim3 g = ccell_grid(p), b = ccell_block(p);
   if (glbm) {
-    if (slab) k_collide_to_compact<CM, true, true, FOLD><<<g, b, 0, s>>>(p, dense, dst);
-    else k_collide_to_compact<CM, true, false, FOLD><<<g, b, 0, s>>>(p, dense, dst);
+    if (slab) k_collide_compact<CM, true, true, FOLD><<<g, b, 0, s>>>(p, buf);
+    else k_collide_compact<CM, true, false, FOLD><<<g, b, 0, s>>>(p, buf);
   } else {
-    if (slab) k_collide_to_compact<CM, false, true, FOLD><<<g, b, 0, s>>>(p, dense, dst);
-    else k_collide_to_compact<CM, false, false, FOLD><<<g, b, 0, s>>>(p, dense, dst);
+    if (slab) k_collide_compact<CM, false, true, FOLD><<<g, b, 0, s>>>(p, buf);
+    else k_collide_compact<CM, false, false, FOLD><<<g, b, 0, s>>>(p, buf);
   }
 }
 
@@ -954,17 +979,31 @@ void launch_sweep_compact(const SweepConfig& cfg, const KParams& p, const double
   }
 }
 
-void launch_collide_to_compact(bool glbm, bool slab, bool records, const KParams& p,
-                               const double* dense, double* dst, cudaStream_t s) {
+void launch_collide_compact(bool glbm, bool slab, bool records, const KParams& p, double* buf,
+                            cudaStream_t s) {
   switch (collide_mode(p)) {
-    case CM_FAST: collide_to_compact_cm<CM_FAST, false>(glbm, slab, p, dense, dst, s); break;
+    case CM_FAST: collide_compact_cm<CM_FAST, false>(glbm, slab, p, buf, s); break;
     case CM_FAST_FOLD:
-      if (records) collide_to_compact_cm<CM_FAST_FOLD, true>(glbm, slab, p, dense, dst, s);
-      else collide_to_compact_cm<CM_FAST, false>(glbm, slab, p, dense, dst, s);
+      if (records) collide_compact_cm<CM_FAST_FOLD, true>(glbm, slab, p, buf, s);
+      else collide_compact_cm<CM_FAST, false>(glbm, slab, p, buf, s);
       break;
-    case CM_EXACT_RHO1: collide_to_compact_cm<CM_EXACT_RHO1, false>(glbm, slab, p, dense, dst, s); break;
-    default: collide_to_compact_cm<CM_EXACT, false>(glbm, slab, p, dense, dst, s);
+    case CM_EXACT_RHO1: collide_compact_cm<CM_EXACT_RHO1, false>(glbm, slab, p, buf, s); break;
+    default: collide_compact_cm<CM_EXACT, false>(glbm, slab, p, buf, s);
   }
+}
+
+void launch_compact_io(bool expand, const KParams& p, double* f, double* dense, int z0, int nzc,
+                       cudaStream_t s) {
+  const int64_t n = (int64_t)nzc * p.ny * p.nx;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  if (expand) k_compact_io<true><<<blocks, 256, 0, s>>>(p, f, dense, z0, nzc);
+  else k_compact_io<false><<<blocks, 256, 0, s>>>(p, f, dense, z0, nzc);
+}
+
+void launch_fill_compact(const KParams& p, int64_t nfluid, double* f, const double* feq,
+                         cudaStream_t s) {
+  if (nfluid == 0) return;
+  k_fill_compact<<<(unsigned)((nfluid + 255) / 256), 256, 0, s>>>(p, nfluid, f, feq);
 }
 
 }  // namespace pgpu

@@ -539,6 +539,13 @@ class Simulation:
         _check(lib.pgpu_set_body_force(self._h, _vec3(g)))
 
     @property
+    def device_bytes(self) -> int:
+        """Device memory held by the simulation (pgpu_device_bytes)."""
+        n = C.c_int64()
+        _check(lib.pgpu_device_bytes(self._h, C.byref(n)))
+        return n.value
+
+    @property
     def layout(self) -> str:
         """"dense", "fluid-only" or "dense-persistent" (pgpu_get_layout)."""
         m = C.c_int32()

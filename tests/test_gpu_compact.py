@@ -141,3 +141,48 @@ for scheme in (0, 1):
         o.step(9)
         got = np.load(tmp_path / f"plain_{scheme}.npy")
         assert np.array_equal(got[:, m], o.get_pdfs()[:, m])
+
+
+def test_fluid_only_footprint_has_no_dense_state(gpu, monkeypatch):
+    """The fluid-only layout keeps no dense copy of the populations: the
+    pre-collision state lives in the compact buffers and population I/O
+    stages through the dead one (C4: 16.5 GB instead of 26.7 GB)."""
+    pg = gpu
+    monkeypatch.setenv("PGPU_LAYOUT", "compact")
+    geom = geometry(pg, (96, 64, 80), 40, 3.0, 6.0, 5)
+    sim = pg.Simulation(geom, 0.08, 3.0 / 16.0, (1e-6, 0, 0), pg.WallScheme.CLI)
+    assert sim.layout == "fluid-only"
+    fluid, cells, links = geom.fluid_cells, geom.cells, geom.n_links
+    sweep = 2 * 19 * 8 * ((fluid + 31) // 32 * 32)
+    b = sim.device_bytes
+    assert sweep < b < sweep + 12 * cells + 20 * links + (1 << 20), (b, sweep)
+    # observables and population I/O work without it (and leave it that way)
+    sim.step(5)
+    f = sim.get_pdfs()
+    sim.set_pdfs(f)
+    sim.step(3)
+    sim.planar_profile()
+    assert sim.device_bytes <= b
+
+
+def test_more_than_113m_fluid_cells_stay_fluid_only(gpu, monkeypatch):
+    """A 512x512x460 walled box (120 M fluid cells: 19 planes need unsigned
+    32-bit slot offsets) runs in the fluid-only layout and steps bit for bit
+    like the dense layout (profile, single-cell populations, max speed)."""
+    pg = gpu
+    geom = pg.make_box_geometry((512, 512, 460), (True, True, False), True, True)
+    assert geom.fluid_cells > 113_000_000
+    runs = {}
+    for layout in ("compact", "dense"):
+        monkeypatch.setenv("PGPU_LAYOUT", layout)
+        sim = pg.Simulation(geom, 0.1, 3.0 / 16.0, (1e-6, 2e-7, 0), pg.WallScheme.SBB)
+        assert sim.layout == ("fluid-only" if layout == "compact" else "dense")
+        sim.step(6)
+        cells = [512 * 512 * 1 + 7, 512 * 512 * 230 + 300 * 512 + 11, 512 * 512 * 458 + 511]
+        runs[layout] = (sim.planar_profile().u_superficial, [sim.cell_populations(c) for c in cells],
+                        sim.max_speed())
+        del sim
+    a, b = runs["compact"], runs["dense"]
+    assert np.array_equal(a[0], b[0]) and a[2] == b[2]
+    for x, y in zip(a[1], b[1]):
+        assert np.array_equal(x, y)
