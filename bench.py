@@ -282,6 +282,7 @@ def run_ours(args):
         fluid_total, links_total = int(t[0].item()), int(t[1].item())
         dist.barrier()
 
+    device_bytes = sim.device_bytes
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = sim.launch_count
@@ -373,6 +374,7 @@ def run_ours(args):
                                   else int(np.prod(w.dims)), links_total, w.scheme.name,
                                   world, w.meta, slab=world > 1 or args.force_slab),
             "math": args.math,
+            "device_bytes_per_gpu": device_bytes,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -1,5 +1,6 @@
-# round 2: GPU suite (not slow), default bench, reference arm
+# round 2: GPU suite incl. slow (C4 at 1000 steps, exact + fast), default bench, reference arm
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -q -m "gpu and not slow" -x > gpurun_out/gpu_tests.log 2>&1; echo "gpu tests rc=$?"; tail -4 gpurun_out/gpu_tests.log
-timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"; cat gpurun_out/bench_default.json | head -c 4000; echo
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json | head -c 2000; echo
+timeout 2400 python -m pytest tests -q -m "gpu" > gpurun_out/gpu_tests.log 2>&1; echo "gpu tests rc=$?"; grep -E "passed|failed|FAILED" gpurun_out/gpu_tests.log | tail -8
+timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"; python -c "
+import json; d=json.load(open('gpurun_out/bench_default.json')); print(round(d['value']), round(d['roofline']['frac'],3), d['device_bytes_per_gpu']/1e9, round(d['e2e']['value']), d['cpu_baseline']['value'], d['clocks'], {k: (round(v['value']), round(v['frac'],3)) for k,v in d['per_config'].items()})"
+bash tools/zper_sweep.sh "C2 C3" "1 2 3"
