@@ -255,6 +255,13 @@ int pgpu_set_math_mode(pgpu_sim* sim, int32_t mode);
 /* PDF layout chosen at creation (PGPU_LAYOUT overrides). */
 enum pgpu_layout { PGPU_LAYOUT_DENSE = 0, PGPU_LAYOUT_FLUID_ONLY = 1, PGPU_LAYOUT_DENSE_PERSISTENT = 2 };
 int pgpu_get_layout(pgpu_sim* sim, int32_t* layout);
+/* K1 kernel of the fluid-only layout (no reference analogue,
+ * results are bit-identical): AUTO (the library's choice), CPIPE (per-thread
+ * asynchronous copies, k_sweep_cpipe) or TMA (warp-specialised bulk-copy
+ * pipeline, k_sweep_tma).  PGPU_SWEEP=cpipe|tma sets the default at creation. */
+enum pgpu_sweep_kernel { PGPU_SWEEP_AUTO = 0, PGPU_SWEEP_CPIPE = 1, PGPU_SWEEP_TMA = 2 };
+int pgpu_set_sweep_kernel(pgpu_sim* sim, int32_t kind);
+int pgpu_get_sweep_kernel(pgpu_sim* sim, int32_t* kind);
 /* Device memory held by the simulation (PDF buffers, cell words, link data). */
 int pgpu_device_bytes(pgpu_sim* sim, int64_t* bytes);
 int pgpu_get_math_mode(pgpu_sim* sim, int32_t* mode);

@@ -94,6 +94,8 @@ SIGNATURES = {
     "pgpu_synchronize": (C.c_int, [vp]),
     "pgpu_get_params": (C.c_int, [vp, P(FluidParams)]),
     "pgpu_set_math_mode": (C.c_int, [vp, i32]),
+    "pgpu_set_sweep_kernel": (C.c_int, [vp, i32]),
+    "pgpu_get_sweep_kernel": (C.c_int, [vp, P(i32)]),
     "pgpu_dist_nccl_unique_id": (C.c_int, [P(u8)]),
     "pgpu_dist_create_nccl": (C.c_int, [vp, P(u8), i32, i32, P(vp)]),
     "pgpu_dist_create_local": (C.c_int, [P(vp), i32, P(vp)]),

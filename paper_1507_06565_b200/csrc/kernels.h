@@ -22,6 +22,11 @@ void launch_sweep(const SweepConfig& cfg, const KParams& p, const double* src, d
                   cudaStream_t s);
 void launch_sweep_compact(const SweepConfig& cfg, const KParams& p, const double* src,
                           double* dst, cudaStream_t s);
+// K1 of the fluid-only layout as a warp-specialised TMA pipeline (sweep_tma.cu):
+// whole-domain stream+collide, no slab, no folded links, nx % 4 == 0.
+bool tma_sweep_supported(const SweepConfig& cfg, const KParams& p);
+bool launch_sweep_tma(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+                      cudaStream_t s);
 // K0 of the fluid-only layout: pre-collision f(n) -> post-collision g(n) in
 // place (with records in math mode fast + PGPU_FOLD: folded CLI slots).
 void launch_collide_compact(bool glbm, bool slab, bool records, const KParams& p, double* buf,

@@ -131,7 +131,7 @@ void device_setup(pgpu_sim* s, const pgpu_geometry* g, bool fill_sectors, Lap&& 
 
   // records: CLI coefficients / SBB / moving wall; validation in the same pass
   const bool cli = s->scheme == PGPU_CLI;
-  if (L > 0 && (cli || g->link_moving)) CK(cudaMalloc(&s->d_recs, sizeof(LinkRec) * L));
+  if (L > 0 && (cli || g->link_moving)) CK(cudaMalloc(&s->d_recs, sizeof(LinkRec) * (L + 2)));
   const int64_t words = (L + 31) / 32;
   if (words) {
     CK(cudaMalloc(&seen.p, sizeof(uint32_t) * words));
@@ -341,6 +341,8 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     CK(cudaMalloc(&s->d_flags, sizeof(int) * 2));
     CK(cudaMalloc(&s->d_vmax, sizeof(unsigned long long)));
     CK(cudaMalloc(&s->d_sums, sizeof(double) * s->nz));
+    CK(cudaMalloc(&s->d_tickets, sizeof(uint32_t) * 2));
+    CK(cudaMemsetAsync(s->d_tickets, 0, sizeof(uint32_t) * 2, s->stream));
     KParams& kp = s->kp;
     kp.nx = s->nx;
     kp.ny = s->ny;
@@ -361,6 +363,13 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     kp.cellw = s->d_cellw;
     kp.cellbase = s->d_cellbase;
     kp.chunkbase = s->d_chunkbase;
+    // fluid-only K1 kernel (PGPU_SWEEP=tma|cpipe overrides the default); the
+    // TMA sweep addresses the link sources of every scheme through the
+    // per-record descriptors
+    if (s->compact) s->ensure_linkdesc();
+    kp.tickets = s->d_tickets;
+    if (const char* e = std::getenv("PGPU_SWEEP"))
+      kp.sweep = e[0] == 't' ? PGPU_SWEEP_TMA : (e[0] == 'c' ? PGPU_SWEEP_CPIPE : PGPU_SWEEP_AUTO);
     lap("alloc pdfs");
     s->refresh_params();
     CK(cudaStreamSynchronize(s->stream));
@@ -423,6 +432,27 @@ int pgpu_set_math_mode(pgpu_sim* sim, int32_t mode) {
     sim->fast = want;
     sim->refresh_params();
     sim->sync();
+  });
+}
+
+// K1 kernel of the fluid-only layout (not in the reference: a schedule choice,
+// results are bit-identical between them).
+int pgpu_set_sweep_kernel(pgpu_sim* sim, int32_t kind) {
+  return guard([&] {
+    SIM_CHECK();
+    if (kind != PGPU_SWEEP_AUTO && kind != PGPU_SWEEP_CPIPE && kind != PGPU_SWEEP_TMA)
+      throw ConfigError("unknown sweep kernel");
+    if (kind == sim->kp.sweep) return;
+    sim->sync();
+    sim->kp.sweep = kind;
+    sim->drop_graphs();  // graphs hold the kernel parameters by value
+  });
+}
+
+int pgpu_get_sweep_kernel(pgpu_sim* sim, int32_t* kind) {
+  return guard([&] {
+    SIM_CHECK();
+    *kind = sim->resolved_sweep();
   });
 }
 

@@ -104,6 +104,7 @@ struct pgpu_sim {
   int* d_flags = nullptr;  // [0] err, [1] nonfinite
   unsigned long long* d_vmax = nullptr;
   double* d_sums = nullptr;
+  uint32_t* d_tickets = nullptr;  // TMA sweep work counter (KParams::tickets)
   // state
   int cur = 0;
   bool post = false;
@@ -141,6 +142,7 @@ struct pgpu_sim {
     cudaFree(d_flags);
     cudaFree(d_vmax);
     cudaFree(d_sums);
+    cudaFree(d_tickets);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 
@@ -279,7 +281,7 @@ struct pgpu_sim {
   // a later set_lid_velocity on an SBB simulation starts from all-SBB (NaN).
   void ensure_records() {
     if (d_recs || n_links == 0) return;
-    CK(cudaMalloc(&d_recs, sizeof(LinkRec) * n_links));
+    CK(cudaMalloc(&d_recs, sizeof(LinkRec) * (n_links + 2)));  // + 2: even-rounded bulk copies
     fill_records_nan(d_recs, n_links, stream);
     ensure_linkdesc();
     update_links();
@@ -287,13 +289,21 @@ struct pgpu_sim {
     drop_graphs();
   }
 
-  // per-record link descriptors for the compact CLI sweep (+ 2: pair copies)
+  // per-record link descriptors for the compact sweeps (+ 16: pair / 16-byte bulk copies)
   void ensure_linkdesc() {
     if (d_linkdesc || n_links == 0) return;
-    CK(cudaMalloc(&d_linkdesc, sizeof(uint16_t) * (n_links + 2)));
-    CK(cudaMemsetAsync(d_linkdesc, 0, sizeof(uint16_t) * (n_links + 2), stream));
+    CK(cudaMalloc(&d_linkdesc, sizeof(uint16_t) * (n_links + 16)));
+    CK(cudaMemsetAsync(d_linkdesc, 0, sizeof(uint16_t) * (n_links + 16), stream));
     build_linkdesc(d_cellw, d_cellbase, nx, cells, d_linkdesc, stream);
     kp.linkdesc = d_linkdesc;
+  }
+
+  // the K1 kernel the whole-domain step runs (pgpu_sweep_kernel; AUTO for the
+  // dense layout, which has one)
+  int resolved_sweep() const {
+    if (!compact) return PGPU_SWEEP_AUTO;
+    if (kp.sweep == PGPU_SWEEP_TMA && tma_sweep_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_TMA;
+    return PGPU_SWEEP_CPIPE;
   }
 
   SweepConfig sweep_cfg(int op, int part) const {
@@ -323,9 +333,9 @@ struct pgpu_sim {
     b += cells * (int64_t)(sizeof(uint32_t) + sizeof(int32_t));  // cell words + record bases
     b += (rows * nch + 1) * (int64_t)sizeof(int32_t);             // chunk record bases
     if (d_ctab) b += rows * nch * (int64_t)sizeof(ChunkEnt);
-    if (d_recs) b += n_links * (int64_t)sizeof(LinkRec);
+    if (d_recs) b += (n_links + 2) * (int64_t)sizeof(LinkRec);
     if (d_recs_fold) b += n_links * (int64_t)sizeof(LinkRec);
-    if (d_linkdesc) b += (n_links + 2) * (int64_t)sizeof(uint16_t);
+    if (d_linkdesc) b += (n_links + 16) * (int64_t)sizeof(uint16_t);
     if (d_planes) b += nz * (int64_t)sizeof(PlaneCoef);
     if (d_scratch) b += scratch_n * (int64_t)sizeof(double);
     b += (19 + 2 + 1 + nz) * 8;  // feq, flags, vmax, plane sums

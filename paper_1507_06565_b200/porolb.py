@@ -73,6 +73,10 @@ class MathMode(enum.IntEnum):
     FAST = 1
 
 
+# pgpu_sweep_kernel (include/porolb_gpu.h), by value
+SWEEP_KERNELS = ("auto", "cpipe", "tma")
+
+
 class GlbmViscosity(enum.IntEnum):
     Plain = 0
     Rescaled = 1
@@ -561,6 +565,17 @@ class Simulation:
     @math_mode.setter
     def math_mode(self, mode) -> None:
         _check(lib.pgpu_set_math_mode(self._h, int(mode)))
+
+    @property
+    def sweep_kernel(self) -> str:
+        """Fluid-only K1 kernel: "auto", "cpipe" or "tma" (pgpu_get_sweep_kernel)."""
+        m = C.c_int32()
+        _check(lib.pgpu_get_sweep_kernel(self._h, C.byref(m)))
+        return SWEEP_KERNELS[m.value]
+
+    @sweep_kernel.setter
+    def sweep_kernel(self, kind: str) -> None:
+        _check(lib.pgpu_set_sweep_kernel(self._h, SWEEP_KERNELS.index(kind)))
 
     def set_lid_velocity(self, u) -> None:
         _check(lib.pgpu_set_lid_velocity(self._h, _vec3(u)))
