@@ -272,6 +272,8 @@ def run_ours(args):
         sim.set_stream(stream.cuda_stream)
     with torch.cuda.stream(stream):
         stepper(args.warmup)
+        if not (world > 1 or args.force_slab):
+            sim.prepare()  # the step's CUDA graphs exist before the timed region (no steps taken)
     torch.cuda.synchronize()
     fluid_total = fluid_local
     links_local = geom.n_links if geom is not None else sim_obj.me.geometry.n_links
@@ -450,6 +452,7 @@ def per_config_run(pg, configs, skip, device, peak):
         stream = torch.cuda.Stream(device=device)
         sim.set_stream(stream.cuda_stream)
         sim.step(20)
+        sim.prepare()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         steps = 200

@@ -261,6 +261,9 @@ int pgpu_get_layout(pgpu_sim* sim, int32_t* layout);
  * pipeline, k_sweep_tma).  PGPU_SWEEP=cpipe|tma sets the default at creation. */
 enum pgpu_sweep_kernel { PGPU_SWEEP_AUTO = 0, PGPU_SWEEP_CPIPE = 1, PGPU_SWEEP_TMA = 2 };
 int pgpu_set_sweep_kernel(pgpu_sim* sim, int32_t kind);
+/* Instantiate the step's CUDA graphs now (no time step is taken; no reference
+ * analogue): a later step() does not pay their capture.  Optional. */
+int pgpu_prepare(pgpu_sim* sim);
 int pgpu_get_sweep_kernel(pgpu_sim* sim, int32_t* kind);
 /* Device memory held by the simulation (PDF buffers, cell words, link data). */
 int pgpu_device_bytes(pgpu_sim* sim, int64_t* bytes);

@@ -119,6 +119,7 @@ SIGNATURES = {
     "pgpu_set_porous": (C.c_int, [vp, i32, P(f64), P(f64), P(f64), P(f64), f64, i32]),
     "pgpu_initialize_equilibrium": (C.c_int, [vp, f64, P(f64)]),
     "pgpu_step": (C.c_int, [vp, i64]),
+    "pgpu_prepare": (C.c_int, [vp]),
     "pgpu_steps_done": (C.c_int, [vp, P(i64)]),
     "pgpu_cli_fallback_count": (C.c_int, [vp, P(i32)]),
     "pgpu_fluid_cells": (C.c_int, [vp, P(i64)]),

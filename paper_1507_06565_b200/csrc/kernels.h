@@ -13,6 +13,9 @@ struct SweepConfig {
   bool glbm = false;
   bool records = false;
   bool slab = false;
+  // visit the z-blocks in descending order: consecutive sweeps alternate, so
+  // each starts on the planes the previous one wrote last (still in L2)
+  bool zrev = false;
 };
 
 // Dense layout (kernels.cu) or, when p.ctab is set, the fluid-only layout

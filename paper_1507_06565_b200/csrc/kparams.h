@@ -107,6 +107,7 @@ struct KParams {
   int32_t moving;  // some link is a moving wall (records hold +inf for it)
   int32_t sweep;   // fluid-only K1 kernel: pgpu_sweep_kernel (0 auto, 1 cpipe, 2 tma)
   uint32_t* tickets;  // TMA sweep: [0] next work item, [1] finished blocks (zero between launches)
+  int32_t stream_stores;  // sweeps store the new state evict-first (domains far larger than L2)
   FastCoef fc;
   double fpop[9];   // core force term ((3*w)*rho0)*eg per pair (simulation.cpp:190)
   double wr3[9];    // (w*rho0)*3 per pair                      (simulation.cpp:185)

@@ -368,6 +368,15 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     // per-record descriptors
     if (s->compact) s->ensure_linkdesc();
     kp.tickets = s->d_tickets;
+    // evict-first stores only where the state dwarfs L2 (C4); smaller domains
+    // keep the new state in L2 for the next sweep (read first, zrev order)
+    {
+      const char* e = std::getenv("PGPU_STREAM_STORES");
+      const double buf_bytes = 19.0 * 8.0 * (double)sweep_ks;
+      kp.stream_stores = e ? (e[0] == '1') : (buf_bytes > 4.0 * 126e6);
+      const char* z = std::getenv("PGPU_ZREV");
+      s->zrev_on = !(z && z[0] == '0');
+    }
     if (const char* e = std::getenv("PGPU_SWEEP"))
       kp.sweep = e[0] == 't' ? PGPU_SWEEP_TMA : (e[0] == 'c' ? PGPU_SWEEP_CPIPE : PGPU_SWEEP_AUTO);
     lap("alloc pdfs");
@@ -567,6 +576,15 @@ int pgpu_step(pgpu_sim* sim, int64_t n) {
     SIM_CHECK();
     if (n < 0) throw ConfigError("step count must be non-negative");
     sim->step(n);
+  });
+}
+
+// Instantiate the multi-step CUDA graphs of both buffer parities now (no
+// time step is taken), so a timed step() does not pay their capture.
+int pgpu_prepare(pgpu_sim* sim) {
+  return guard([&] {
+    SIM_CHECK();
+    sim->prepare();
   });
 }
 

@@ -121,6 +121,7 @@ struct pgpu_sim {
   static constexpr int kGraphSteps = 16;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   bool persistent = false;  // L2-resident domain: cooperative multi-step sweep
+  bool zrev_on = true;      // alternate the z order of consecutive sweeps (PGPU_ZREV=0: off)
   cudaStream_t graph_stream = nullptr;
   KParams kp{};
 
@@ -387,7 +388,9 @@ struct pgpu_sim {
   void k1(int part) {
     Nvtx r(part == 0 ? "K1 sweep" : (part == 1 ? "K1 edge columns" : "K1 interior columns"));
     set_ghost_ptrs();
-    launch_sweep(sweep_cfg(0, part), kp, f[cur], f[1 - cur], stream);
+    SweepConfig c = sweep_cfg(0, part);
+    c.zrev = zrev_on && cur == 1;
+    launch_sweep(c, kp, f[cur], f[1 - cur], stream);
     check_launch();
     ++launches;
   }
@@ -411,7 +414,9 @@ struct pgpu_sim {
     CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     int c = start;
     for (int i = 0; i < kGraphSteps; ++i) {
-      launch_sweep(sweep_cfg(0, 0), kp, f[c], f[1 - c], cs);
+      SweepConfig sc = sweep_cfg(0, 0);
+      sc.zrev = zrev_on && c == 1;
+      launch_sweep(sc, kp, f[c], f[1 - c], cs);
       c = 1 - c;
     }
     cudaGraph_t g = nullptr;
@@ -420,6 +425,13 @@ struct pgpu_sim {
     CK(cudaGraphInstantiate(&graph[start], g, 0));
     cudaGraphDestroy(g);
     graph_stream = cs;
+  }
+
+  void prepare() {
+    if (slab || persistent) return;
+    if (graph_stream != stream) drop_graphs();
+    for (int c = 0; c < 2; ++c)
+      if (!graph[c]) build_graph(c);
   }
 
   void step(int64_t n) {

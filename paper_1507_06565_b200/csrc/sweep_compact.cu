@@ -536,7 +536,7 @@ __device__ __forceinline__ void cclose_link(double* stage, int owner, int j, dou
 template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
 __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
     k_sweep_cpipe(const KParams p, const double* __restrict__ src, double* __restrict__ dst,
-                  int part, int zper) {
+                  int part, int zper, int zrev) {
   constexpr bool FOLD = RECORDS && CM == CM_FAST_FOLD;
   using Sm = CSmem<RECORDS, FOLD>;
   constexpr int kS = Sm::S;
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
     y = blockIdx.y;
   }
   const int x = xc * 32 + lane;
-  const int z0 = blockIdx.z * zper;
+  const int z0 = (zrev ? gridDim.z - 1 - blockIdx.z : blockIdx.z) * zper;
   const int z1 = min(z0 + zper, p.nz);
   const bool wok = xc < p.nchunk && y < p.ny;
   const bool valid = wok && x < p.nx;
@@ -862,7 +862,7 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
 #pragma unroll
         for (int j = 0; j < 19; ++j) {
           bounds_ok(in_plane(p, li.fc + p.poff[j], j));
-          if (PGPU_STCS)
+          if (PGPU_STCS && p.stream_stores)
             __stcs(dst + (uint32_t)(li.fc + p.poff[j]), f[j]);
           else
             dst[(uint32_t)(li.fc + p.poff[j])] = f[j];
@@ -924,7 +924,7 @@ void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* sr
     }();
     (void)attr;
     k_sweep_cpipe<CM, GLBM, RECORDS, SLAB, OP><<<grid, kCBXp, smem, s>>>(p, src, dst, cfg.part,
-                                                                         zper);
+                                                                         zper, cfg.zrev ? 1 : 0);
   }
 }
 

@@ -604,6 +604,11 @@ class Simulation:
     def step(self, n: int = 1) -> None:
         _check(lib.pgpu_step(self._h, int(n)))
 
+    def prepare(self) -> None:
+        """Instantiate the step's CUDA graphs now (pgpu_prepare): a later
+        step() does not pay their capture.  No time step is taken."""
+        _check(lib.pgpu_prepare(self._h))
+
     @property
     def steps_done(self) -> int:
         v = C.c_int64()
