@@ -611,11 +611,13 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
   };
 
   // issue plane z (meta slot m) into stage s; returns the warp's link count
-  auto issue = [&](int z, int s, int m) -> int {
+  // what: 1 the populations, 2 the link extras (records, g_j(x)), 3 both
+  auto issue = [&](int z, int s, int m, int what = 3) -> int {
     const CMeta& M = S.meta[m];
     const uint32_t cw = M.cw[tx];
     const bool fl = !(cw & kNonFluid);
     const ChunkEnt* E = M.ent[warp];
+    if (what & 1) {
     int q[9];
     uint32_t bits = 0;  // bit r: the source row r has a fluid cell at this x (rows 0..4)
 #pragma unroll
@@ -668,7 +670,9 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
         }
       }
     }
+    }  // what & 1
     int total = 0;
+    if (!(what & 2)) return total;
     if (RECORDS && kStaticDesc) {
       // the chunk-plane's links are records [cb, cbn) with their (lane, j)
       // descriptors already in the meta slot: no prefix sum, no publish loop
@@ -731,14 +735,22 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
   cpa_commit();
   cpa_wait_all();
   __syncwarp();
+  int cnt_cur;
   if (kStaticDesc) {
+    // the descriptors (addressed by the chunk bases just landed) and the first
+    // plane's populations go in flight together; the link extras follow once
+    // the descriptors have landed
     desc_load(0);
     if (z0 + 1 < z1) desc_load(1);
     cpa_commit();
-    cpa_wait_all();
+    issue(z0, 0, 0, 1);
+    cpa_commit();
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // the descriptors (not the populations)
     __syncwarp();
+    cnt_cur = issue(z0, 0, 0, 2);
+  } else {
+    cnt_cur = issue(z0, 0, 0);
   }
-  int cnt_cur = issue(z0, 0, 0);
   __syncwarp();
   if (z0 + 2 < z1) meta_load(z0 + 2, 2);
   cpa_commit();
