@@ -331,7 +331,7 @@ def run_ours(args):
 
     e2e = None
     if world == 1 and not args.no_e2e and not args.force_slab:
-        e2e = e2e_run(pg, configs, w, geom, args.steps, local)
+        e2e = e2e_run(pg, configs, w, geom, args.steps, local, args.e2e_output)
     elif (world > 1 or args.force_slab) and not args.no_e2e:
         slab_geom = sim_obj.me.geometry
         e2e = e2e_run_dist(w, slab_geom, args.steps, rank, world, local, dist)
@@ -474,31 +474,42 @@ def per_config_run(pg, configs, skip, device, peak):
     return out
 
 
-def e2e_run(pg, configs, w, geom, steps, device):
-    """Timed: create from host geometry (H2D) + steps + f(N) and profile back (D2H)."""
+def e2e_run(pg, configs, w, geom, steps, device, output="fields"):
+    """Timed: create from host geometry (H2D) + steps + the result back (D2H):
+    the macroscopic density and velocity fields (the API's field output,
+    simulation.hpp macroscopic(); `output="pdfs"`: all of f(N)) into pinned
+    memory, and the planar profile."""
     import torch
 
     cells = geom.cells
-    pdf_host = torch.empty(19 * cells, dtype=torch.float64, pin_memory=True).numpy()
+    shape = geom.dims[::-1]
+    if output == "pdfs":
+        host = torch.empty(19 * cells, dtype=torch.float64, pin_memory=True).numpy()
+    else:
+        host = torch.empty(4 * cells, dtype=torch.float64, pin_memory=True).numpy()
     h2d = (geom.flags.nbytes + geom.n_links * (8 + 8 + 4 + 4 + 1) + geom.porosity.nbytes)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     sim = configs.make_simulation(w, geom, device=device)
     tc = time.perf_counter()
     sim.step(steps)
-    sim.get_pdfs(pdf_host.reshape(19, *geom.dims[::-1]))
+    if output == "pdfs":
+        sim.get_pdfs(host.reshape(19, *shape))
+    else:
+        sim.macroscopic_fields(out=[host[i * cells:(i + 1) * cells].reshape(shape) for i in range(4)])
     td = time.perf_counter()
     prof = sim.planar_profile()
     t1 = time.perf_counter()
-    d2h = pdf_host.nbytes + 5 * prof.z.nbytes
+    d2h = host.nbytes + 5 * prof.z.nbytes
     del sim
     torch.cuda.empty_cache()
+    what = ("pgpu_get_pdfs (pinned)" if output == "pdfs"
+            else "pgpu_macroscopic_fields (delta_rho, u; pinned)")
     return {"value": geom.fluid_cells * steps / (t1 - t0) / 1e6, "unit": "MLUPS",
             "h2d_bytes_per_step": h2d / steps, "d2h_bytes_per_step": d2h / steps,
-            "seconds": t1 - t0, "create_s": tc - t0, "steps_and_pdf_download_s": td - tc,
-            "profile_s": t1 - td,
-            "what": "pgpu_create from host geometry + K steps + pgpu_get_pdfs (pinned) + "
-                    "pgpu_planar_profile"}
+            "seconds": t1 - t0, "create_s": tc - t0, "steps_and_result_s": td - tc,
+            "profile_s": t1 - td, "output": output,
+            "what": f"pgpu_create from host geometry + K steps + {what} + pgpu_planar_profile"}
 
 
 def e2e_run_dist(w, geom, steps, rank, world, device, dist):
@@ -510,7 +521,8 @@ def e2e_run_dist(w, geom, steps, rank, world, device, dist):
     from paper_1507_06565_b200.dist import SlabSimulation
 
     cells = geom.cells
-    pdf_host = torch.empty(19 * cells, dtype=torch.float64, pin_memory=True).numpy()
+    shape = geom.dims[::-1]
+    host = torch.empty(4 * cells, dtype=torch.float64, pin_memory=True).numpy()
     h2d = (geom.flags.nbytes + geom.n_links * (8 + 8 + 4 + 4 + 1) + geom.porosity.nbytes
            + 2 * geom.ghost_flags_lo.nbytes)
     torch.cuda.synchronize()
@@ -520,7 +532,7 @@ def e2e_run_dist(w, geom, steps, rank, world, device, dist):
     ss = SlabSimulation(w, rank, world, device=device, geometry=geom)
     tc = time.perf_counter()
     ss.step(steps)
-    ss.sim.get_pdfs(pdf_host.reshape(19, *geom.dims[::-1]))
+    ss.sim.macroscopic_fields(out=[host[i * cells:(i + 1) * cells].reshape(shape) for i in range(4)])
     td = time.perf_counter()
     prof = ss.planar_profile()
     t1 = time.perf_counter()
@@ -530,14 +542,16 @@ def e2e_run_dist(w, geom, steps, rank, world, device, dist):
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
         dist.all_reduce(fl)
     tt, tcr, tst, tpr = (float(v) for v in loc.cpu())
-    d2h = pdf_host.nbytes + 5 * prof.z.nbytes
+    d2h = host.nbytes + 5 * prof.z.nbytes
     del ss
     torch.cuda.empty_cache()
     return {"value": float(fl.item()) * steps / tt / 1e6, "unit": "MLUPS",
             "h2d_bytes_per_step": world * h2d / steps, "d2h_bytes_per_step": world * d2h / steps,
-            "seconds": tt, "create_s": tcr, "steps_and_pdf_download_s": tst, "profile_s": tpr,
+            "seconds": tt, "create_s": tcr, "steps_and_result_s": tst, "profile_s": tpr,
+            "output": "fields",
             "what": "per rank: pgpu_create from its host slab geometry + K steps with the NCCL "
-                    "halo + pgpu_get_pdfs (pinned) + global planar profile; max over ranks"}
+                    "halo + pgpu_macroscopic_fields of its slab (pinned) + global planar "
+                    "profile; max over ranks"}
 
 
 def main():
@@ -564,6 +578,9 @@ def main():
                          "single-GPU run of the same steps (strong scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-output", default="fields", choices=["fields", "pdfs"],
+                    help="the result read back in the e2e leg: the macroscopic density/velocity "
+                         "fields (default) or all of f(N)")
     ap.add_argument("--force-slab", action="store_true",
                     help="diagnostic: run the multi-GPU slab path (edge/interior split, halo "
                          "exchange) even at N=1")

@@ -695,10 +695,18 @@ class Simulation:
         _check(lib.pgpu_get_flags(self._h, _p(out, C.c_uint8)))
         return out
 
-    def macroscopic_fields(self):
-        """(delta_rho, ux, uy, uz), each shaped (nz, ny, nx); 0 on non-fluid cells."""
+    def macroscopic_fields(self, out=None):
+        """(delta_rho, ux, uy, uz), each shaped (nz, ny, nx); 0 on non-fluid cells.
+        `out`: four C-contiguous float64 arrays of that shape to fill (e.g. in
+        pinned host memory), returned."""
         nx, ny, nz = self.geometry_dims
-        outs = [np.empty((nz, ny, nx)) for _ in range(4)]
+        if out is not None:
+            outs = list(out)
+            if len(outs) != 4 or any(o.dtype != np.float64 or o.size != nx * ny * nz
+                                     or not o.flags.c_contiguous for o in outs):
+                raise ValueError("out: four C-contiguous float64 arrays of nx*ny*nz cells")
+        else:
+            outs = [np.empty((nz, ny, nx)) for _ in range(4)]
         _check(lib.pgpu_macroscopic_fields(self._h, *[_p(o, C.c_double) for o in outs]))
         return tuple(outs)
 
