@@ -251,7 +251,7 @@ def run_ours(args):
 
         w = configs.c4(nx_scale=world) if (args.config == "C4" and args.scaling == "weak") \
             else configs.ALL[args.config]()
-        sim_obj = SlabSimulation(w, rank, world, device=local)
+        sim_obj = SlabSimulation(w, rank, world, device=local, transport=args.transport)
         sim = sim_obj.sim
         fluid_local = sim.fluid_cells
         stepper = sim_obj.step
@@ -334,7 +334,7 @@ def run_ours(args):
         e2e = e2e_run(pg, configs, w, geom, args.steps, local, args.e2e_output)
     elif (world > 1 or args.force_slab) and not args.no_e2e:
         slab_geom = sim_obj.me.geometry
-        e2e = e2e_run_dist(w, slab_geom, args.steps, rank, world, local, dist)
+        e2e = e2e_run_dist(w, slab_geom, args.steps, rank, world, local, dist, args.transport)
     del sim, stepper
     if world > 1 or args.force_slab:
         del sim_obj
@@ -385,6 +385,8 @@ def run_ours(args):
             "total_cell_mlups": int(np.prod(w.dims)) * args.steps / (ms * 1e-3) / 1e6,
             "per_config": per_config,
         }
+        if world > 1 or args.force_slab:
+            line["halo_transport"] = args.transport
         if parity is not None:
             line["parity"] = parity
         print(json.dumps(line), flush=True)
@@ -534,7 +536,7 @@ def e2e_run(pg, configs, w, geom, steps, device, output="fields"):
             "what": f"pgpu_create from host geometry + K steps + {what} + pgpu_planar_profile"}
 
 
-def e2e_run_dist(w, geom, steps, rank, world, device, dist):
+def e2e_run_dist(w, geom, steps, rank, world, device, dist, transport="nccl"):
     """N > 1: every rank creates its slab from its host slab geometry, steps
     through DistTransport (NCCL halo), downloads its f(N) into pinned memory
     and joins the global profile; time = max over ranks."""
@@ -552,7 +554,7 @@ def e2e_run_dist(w, geom, steps, rank, world, device, dist):
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
-    ss = SlabSimulation(w, rank, world, device=device, geometry=geom)
+    ss = SlabSimulation(w, rank, world, device=device, geometry=geom, transport=transport)
     tc = time.perf_counter()
     ss.step(steps)
     ss.sim.macroscopic_fields(out=[host[i * cells:(i + 1) * cells].reshape(shape) for i in range(4)])
@@ -601,6 +603,9 @@ def main():
                          "single-GPU run of the same steps (strong scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N > 1 halo exchange: NCCL send/recv, or IPC (the edge kernel stores "
+                         "the 5 PDFs per face straight into the neighbours' ghost buffers)")
     ap.add_argument("--e2e-output", default="fields", choices=["fields", "pdfs"],
                     help="the result read back in the e2e leg: the macroscopic density/velocity "
                          "fields (default) or all of f(N)")

@@ -356,6 +356,16 @@ int pgpu_dist_create_nccl(pgpu_sim* sim, const uint8_t id[128], int32_t rank, in
                           pgpu_dist** out);
 /* sims[r] = slab r of `world` (any devices; same device is allowed). */
 int pgpu_dist_create_local(pgpu_sim* const* sims, int32_t world, pgpu_dist** out);
+/* IPC transport (one rank per process, all on one node): the edge-column
+ * kernel stores its outgoing PDFs straight into the neighbours' ghost buffers
+ * (CUDA IPC mappings over NVLink), ordered by interprocess events and a host
+ * channel in POSIX shared memory.  Create on every rank, export this rank's
+ * blob (pgpu_dist_ipc_blob_size bytes), all-gather the blobs in rank order by
+ * any means (MPI, torch.distributed, files), then connect. */
+int pgpu_dist_create_ipc(pgpu_sim* sim, int32_t rank, int32_t world, pgpu_dist** out);
+int pgpu_dist_ipc_blob_size(int64_t* bytes);
+int pgpu_dist_ipc_export(pgpu_dist* d, void* blob);
+int pgpu_dist_ipc_connect(pgpu_dist* d, const void* blobs);
 /* NCCL mode replays a CUDA graph of two steps (default on; PGPU_DIST_GRAPHS=0). */
 int pgpu_dist_set_graphs(pgpu_dist* d, int32_t enable);
 int pgpu_dist_step(pgpu_dist* d, int64_t n);

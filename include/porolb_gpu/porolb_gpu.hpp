@@ -16,6 +16,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <functional>
 #include <vector>
 
 #include "../porolb_gpu.h"
@@ -459,6 +460,27 @@ class DistSimulation {
     d_.reset(d);
     nz_ = slab.dims().nz;
   }
+  // IPC transport (one rank per process on one node): the edge kernel stores
+  // into the neighbours' ghost buffers.  `allgather` receives this rank's
+  // blob and returns all ranks' blobs in rank order (MPI_Allgather, a file
+  // exchange, ...).
+  using Allgather = std::function<std::vector<std::uint8_t>(const std::vector<std::uint8_t>&)>;
+  static DistSimulation ipc(Simulation& slab, int rank, int world, const Allgather& allgather) {
+    DistSimulation ds;
+    pgpu_dist* d = nullptr;
+    check(pgpu_dist_create_ipc(slab.handle(), rank, world, &d));
+    ds.d_.reset(d);
+    ds.nz_ = slab.dims().nz;
+    int64_t n = 0;
+    check(pgpu_dist_ipc_blob_size(&n));
+    std::vector<std::uint8_t> blob(static_cast<std::size_t>(n));
+    check(pgpu_dist_ipc_export(d, blob.data()));
+    const std::vector<std::uint8_t> all = allgather(blob);
+    if (all.size() != blob.size() * static_cast<std::size_t>(world))
+      throw std::invalid_argument("allgather must return world blobs");
+    check(pgpu_dist_ipc_connect(d, all.data()));
+    return ds;
+  }
   static std::array<std::uint8_t, 128> nccl_unique_id() {
     std::array<std::uint8_t, 128> id;
     check(pgpu_dist_nccl_unique_id(id.data()));
@@ -483,6 +505,7 @@ class DistSimulation {
   }
 
  private:
+  DistSimulation() = default;
   struct Del {
     void operator()(pgpu_dist* d) const { pgpu_dist_destroy(d); }
   };

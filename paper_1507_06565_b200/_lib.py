@@ -99,6 +99,10 @@ SIGNATURES = {
     "pgpu_dist_nccl_unique_id": (C.c_int, [P(u8)]),
     "pgpu_dist_create_nccl": (C.c_int, [vp, P(u8), i32, i32, P(vp)]),
     "pgpu_dist_create_local": (C.c_int, [P(vp), i32, P(vp)]),
+    "pgpu_dist_create_ipc": (C.c_int, [vp, i32, i32, P(vp)]),
+    "pgpu_dist_ipc_blob_size": (C.c_int, [P(i64)]),
+    "pgpu_dist_ipc_export": (C.c_int, [vp, vp]),
+    "pgpu_dist_ipc_connect": (C.c_int, [vp, vp]),
     "pgpu_dist_set_graphs": (C.c_int, [vp, i32]),
     "pgpu_dist_step": (C.c_int, [vp, i64]),
     "pgpu_dist_synchronize": (C.c_int, [vp]),

@@ -104,7 +104,7 @@ def build_product(force: bool = False, defines: tuple = (), lib: Path = LIB,
     stamp.write_text(khash)
     if force or jobs or _stale(LIB, objs):
         _run([NVCC, *GENCODE, "-shared", "-cudart", "static", "-o", str(LIB),
-              *[str(o) for o in objs], "-Xcompiler", "-pthread", "-ldl"])
+              *[str(o) for o in objs], "-Xcompiler", "-pthread", "-ldl", "-lrt"])
     return LIB
 
 

@@ -5,12 +5,21 @@
 // whose velocity enters the neighbour ({1,7,9,11,13} to the right,
 // {2,8,10,12,14} to the left), double-buffered by step parity.
 //
-// Two transports behind one schedule:
+// Three transports behind one schedule:
 //   * NCCL, one rank per process (pgpu_dist_create_nccl).  libnccl is
 //     resolved with dlopen at run time, so the library has no link-time NCCL
 //     dependency and shares the copy torch.distributed already loaded.
 //   * local, every slab in this process (pgpu_dist_create_local), on any mix
 //     of devices, exchanged with peer copies (NVLink on a multi-GPU node).
+//   * IPC, one rank per process on one node (pgpu_dist_create_ipc): the
+//     ranks map each other's ghost buffers (CUDA IPC) and the edge-column
+//     kernel STORES its 5 outgoing PDFs per face straight into the
+//     neighbours' ghost buffers over NVLink -- the exchange is fused into the
+//     sweep, no copy or send/recv kernel.  Ordering across processes:
+//     interprocess CUDA events (stream waits, never a spinning kernel) plus a
+//     host handshake in POSIX shared memory that makes each wait see the
+//     right record; the global observables reduce through the same shared
+//     memory in rank order.
 // Per step and rank, on two streams (the simulation's own = "main", and a
 // high-priority "edge" stream):
 //   edge : wait(interior of step n-1) -> edge columns (pgpu part 0: they alone
@@ -22,12 +31,18 @@
 // CUDA graph and replayed, so no per-step host work remains on the path.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>  // types only: the entry points are resolved with dlopen
+#include <sys/mman.h>
+#include <unistd.h>
 
+#include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sim_impl.h"
@@ -89,6 +104,105 @@ void nck(ncclResult_t r, const char* what) {
   }
 }
 
+// ---- host channel of the IPC transport (POSIX shared memory, one node) -------
+constexpr int kMaxIpcRanks = 64;
+struct ShmHeader {
+  std::atomic<uint64_t> edges[kMaxIpcRanks];  // edge parts recorded by each rank
+  std::atomic<uint64_t> bar_count;
+  std::atomic<uint64_t> bar_gen;
+  std::atomic<uint64_t> attached;
+  int32_t world, slot_doubles;
+};
+static_assert(std::atomic<uint64_t>::is_always_lock_free, "process-shared atomics");
+
+struct ShmChannel {
+  std::string name;
+  bool owner = false;
+  int world = 0;
+  size_t bytes = 0;
+  ShmHeader* h = nullptr;
+  double* slots = nullptr;  // world x slot_doubles reduction slots
+
+  static size_t size_for(int world, int slot_doubles) {
+    return sizeof(ShmHeader) + sizeof(double) * (size_t)world * slot_doubles;
+  }
+  void create(const std::string& nm, int w, int slot_doubles) {
+    name = nm;
+    owner = true;
+    world = w;
+    bytes = size_for(w, slot_doubles);
+    shm_unlink(name.c_str());
+    const int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0) throw CudaError("shm_open(create) failed for " + name);
+    if (ftruncate(fd, (off_t)bytes) != 0) {
+      close(fd);
+      throw CudaError("ftruncate failed for " + name);
+    }
+    map(fd);
+    std::memset(static_cast<void*>(h), 0, bytes);
+    h->world = w;
+    h->slot_doubles = slot_doubles;
+  }
+  void open_existing(const std::string& nm, int w, int slot_doubles) {
+    name = nm;
+    world = w;
+    bytes = size_for(w, slot_doubles);
+    const int fd = shm_open(name.c_str(), O_RDWR, 0600);
+    if (fd < 0) throw CudaError("shm_open(attach) failed for " + name);
+    map(fd);
+  }
+  void map(int fd) {
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw CudaError("mmap of the IPC channel failed");
+    h = static_cast<ShmHeader*>(p);
+    slots = reinterpret_cast<double*>(static_cast<char*>(p) + sizeof(ShmHeader));
+  }
+  ~ShmChannel() {
+    if (h) munmap(static_cast<void*>(h), bytes);
+    if (owner) shm_unlink(name.c_str());
+  }
+  // host spin with yields (the waits are short: a neighbour issuing a step)
+  template <class Pred>
+  static void spin(Pred done) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; !done(); ++i) {
+      if (i > 64) std::this_thread::yield();
+      if ((i & 0xffff) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(600))
+        throw CudaError("IPC transport: a neighbour rank stopped issuing steps");
+    }
+  }
+  void wait_edges(int rank, uint64_t n) {
+    spin([&] { return h->edges[rank].load(std::memory_order_acquire) >= n; });
+  }
+  void barrier() {
+    const uint64_t g = h->bar_gen.load(std::memory_order_acquire);
+    if (h->bar_count.fetch_add(1, std::memory_order_acq_rel) + 1 == (uint64_t)world) {
+      h->bar_count.store(0, std::memory_order_relaxed);
+      h->bar_gen.store(g + 1, std::memory_order_release);
+    } else {
+      spin([&] { return h->bar_gen.load(std::memory_order_acquire) != g; });
+    }
+  }
+};
+
+// what one rank publishes to the others (pgpu_dist_ipc_export)
+struct IpcBlob {
+  cudaIpcMemHandle_t halo;
+  cudaIpcEventHandle_t ev[2];
+  int32_t rank, world, device;
+  int64_t halo_n;
+  char shm[64];
+};
+
+struct DistPeer {  // a neighbour's ghost buffers and edge events as mapped here
+  double* base = nullptr;  // opened IPC allocation (nullptr: this rank itself)
+  double* recv_lo[2] = {nullptr, nullptr};
+  double* recv_hi[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool own = false;  // events/pointers are this process's (world 1, or the same peer twice)
+};
+
 struct DistRank {
   pgpu_sim* sim = nullptr;
   int rank = 0;
@@ -110,6 +224,12 @@ struct DistRank {
 struct pgpu_dist {
   int world = 1;
   bool use_nccl = false;
+  bool use_ipc = false;
+  // IPC transport
+  std::unique_ptr<ShmChannel> shm;
+  DistPeer peer_l, peer_r;
+  bool connected = false;
+  uint64_t nedge = 0;  // edge parts issued by this rank
   std::vector<DistRank> ranks;  // NCCL: this process's rank only
   ncclComm_t comm = nullptr;
   int64_t halo_n = 0;
@@ -133,6 +253,16 @@ struct pgpu_dist {
 
   ~pgpu_dist() {
     drop_graphs();
+    for (DistPeer* pr : {&peer_l, &peer_r}) {
+      if (pr->own) continue;
+      for (cudaEvent_t& e : pr->ev)
+        if (e) {
+          cudaEventDestroy(e);
+          e = nullptr;
+        }
+      if (pr->base && !(pr == &peer_r && peer_r.base == peer_l.base)) cudaIpcCloseMemHandle(pr->base);
+      pr->base = nullptr;
+    }
     for (auto& r : ranks) {
       cudaSetDevice(r.sim->device);
       cudaStreamSynchronize(r.edge);
@@ -185,7 +315,46 @@ struct pgpu_dist {
     ++s->steps;
   }
 
+  // IPC: the edge part stores straight into the neighbours' ghost buffers
+  void issue_step_ipc() {
+    DistRank& r = ranks[0];
+    pgpu_sim* s = r.sim;
+    CK(cudaSetDevice(s->device));
+    const int W = world;
+    const int left = (r.rank + W - 1) % W, right = (r.rank + 1) % W;
+    const int pn = 1 - s->ghost_cur;  // the ghost parity the next step reads
+    CK(cudaEventRecord(r.ev_main, s->stream));
+    CK(cudaStreamWaitEvent(r.edge, r.ev_main, 0));
+    if (nedge > 0) {
+      // the neighbours' edge parts of the previous step: they wrote the ghosts
+      // this step reads, and finished reading the ghost parity we overwrite
+      Nvtx nv("IPC wait for the neighbours' previous edge parts");
+      shm->wait_edges(left, nedge);
+      shm->wait_edges(right, nedge);
+      const int pp = (int)((nedge - 1) & 1);
+      CK(cudaStreamWaitEvent(r.edge, peer_l.ev[pp], 0));
+      if (peer_r.ev[pp] != peer_l.ev[pp]) CK(cudaStreamWaitEvent(r.edge, peer_r.ev[pp], 0));
+    }
+    // my x = 0 face feeds the left neighbour's x = nx ghost, x = nx-1 the right's x = -1
+    s->send_lo = peer_l.recv_hi[pn];
+    s->send_hi = peer_r.recv_lo[pn];
+    part(r, 0, r.edge);
+    CK(cudaEventRecord(r.ev_edge[nedge & 1], r.edge));
+    ++nedge;
+    shm->h->edges[r.rank].store(nedge, std::memory_order_release);
+    // interior columns (after the previous step's edge columns)
+    if (r.have_prev) CK(cudaStreamWaitEvent(s->stream, r.ev_edge[(nedge - 2) & 1], 0));
+    part(r, 1, s->stream);
+    finish(r);
+    r.have_prev = true;
+    r.parity = (int)(nedge & 1);
+  }
+
   void issue_step() {
+    if (use_ipc) {
+      issue_step_ipc();
+      return;
+    }
     const int W = world;
     const size_t bytes = sizeof(double) * (size_t)halo_n;
     // edge columns (after the previous interior; local mode: after the
@@ -311,6 +480,20 @@ struct pgpu_dist {
       ++i;
     }
     join();
+    if (use_ipc && nedge > 0) ipc_join();
+  }
+
+  // IPC: the simulation's stream also waits for the neighbours' last edge
+  // parts -- they wrote the ghosts an observable (KP) or the next step reads
+  void ipc_join() {
+    DistRank& r = ranks[0];
+    const int W = world;
+    shm->wait_edges((r.rank + W - 1) % W, nedge);
+    shm->wait_edges((r.rank + 1) % W, nedge);
+    const int pp = (int)((nedge - 1) & 1);
+    CK(cudaSetDevice(r.sim->device));
+    CK(cudaStreamWaitEvent(r.sim->stream, peer_l.ev[pp], 0));
+    if (peer_r.ev[pp] != peer_l.ev[pp]) CK(cudaStreamWaitEvent(r.sim->stream, peer_r.ev[pp], 0));
   }
 
   // ---- observables over the whole domain ---------------------------------------
@@ -342,6 +525,22 @@ struct pgpu_dist {
       allreduce(sums.data(), nz, ncclSum);
       allreduce(counts.data(), nz, ncclSum);
     }
+    if (use_ipc && world > 1) {  // rank-order sums through the shared channel
+      const int me = ranks[0].rank;
+      double* slot = shm->slots + (size_t)me * (2 * nz + 2);
+      std::memcpy(slot, sums.data(), sizeof(double) * nz);
+      std::memcpy(slot + nz, counts.data(), sizeof(double) * nz);
+      shm->barrier();
+      for (int z = 0; z < nz; ++z) sums[z] = counts[z] = 0.0;
+      for (int q = 0; q < world; ++q) {
+        const double* o = shm->slots + (size_t)q * (2 * nz + 2);
+        for (int z = 0; z < nz; ++z) {
+          sums[z] += o[z];
+          counts[z] += o[nz + z];
+        }
+      }
+      shm->barrier();  // the slots may be reused
+    }
   }
 
   void max_speed2(double& v2, bool& finite) {
@@ -359,6 +558,19 @@ struct pgpu_dist {
       allreduce(h, 2, ncclMax);
       v2 = h[0];
       finite = h[1] == 0.0;
+    }
+    if (use_ipc && world > 1) {
+      const int nz = ranks[0].sim->nz;
+      double* slot = shm->slots + (size_t)ranks[0].rank * (2 * nz + 2);
+      slot[0] = v2;
+      slot[1] = finite ? 0.0 : 1.0;
+      shm->barrier();
+      for (int q = 0; q < world; ++q) {
+        const double* o = shm->slots + (size_t)q * (2 * nz + 2);
+        v2 = std::max(v2, o[0]);
+        finite = finite && o[1] == 0.0;
+      }
+      shm->barrier();
     }
   }
 
@@ -408,7 +620,7 @@ struct pgpu_dist {
 
 namespace {
 
-void setup_rank(pgpu_dist* d, DistRank& r) {
+void setup_rank(pgpu_dist* d, DistRank& r, bool ipc = false) {
   pgpu_sim* s = r.sim;
   if (!s->slab) throw ConfigError("multi-GPU runs need slab simulations (pgpu_voxelize_slab)");
   if (s->pending) throw ConfigError("split step in progress");
@@ -418,8 +630,10 @@ void setup_rank(pgpu_dist* d, DistRank& r) {
   // high priority: the edge part and the exchange are dispatched ahead of the
   // interior sweep's remaining blocks
   CK(cudaStreamCreateWithPriority(&r.edge, cudaStreamNonBlocking, hi));
-  for (cudaEvent_t* e : {&r.ev_main, &r.ev_copy, &r.ev_join, &r.ev_edge[0], &r.ev_edge[1]})
+  for (cudaEvent_t* e : {&r.ev_main, &r.ev_copy, &r.ev_join})
     CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&r.ev_edge[0], &r.ev_edge[1]})
+    CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming | (ipc ? cudaEventInterprocess : 0u)));
   const int64_t n = d->halo_n;
   CK(cudaMalloc(&r.halo, sizeof(double) * 6 * (size_t)n));
   CK(cudaMemsetAsync(r.halo, 0, sizeof(double) * 6 * (size_t)n, s->stream));
@@ -511,6 +725,103 @@ int pgpu_dist_create_local(pgpu_sim* const* sims, int32_t world, pgpu_dist** out
   });
 }
 
+int pgpu_dist_create_ipc(pgpu_sim* sim, int32_t rank, int32_t world, pgpu_dist** out) {
+  return guard([&] {
+    if (!sim || !out) throw std::invalid_argument("null pointer");
+    *out = nullptr;
+    if (world < 1 || world > kMaxIpcRanks || rank < 0 || rank >= world)
+      throw ConfigError("rank out of range");
+    std::unique_ptr<pgpu_dist> d(new pgpu_dist());
+    d->world = world;
+    d->use_ipc = true;
+    d->halo_n = 5 * (int64_t)sim->ny * sim->nz;
+    d->ranks.resize(1);
+    d->ranks[0].sim = sim;
+    d->ranks[0].rank = rank;
+    setup_rank(d.get(), d->ranks[0], true);
+    d->shm.reset(new ShmChannel());
+    if (rank == 0) {
+      static std::atomic<int> seq{0};
+      const std::string nm = "/pgpu_dist_" + std::to_string((long)getpid()) + "_" +
+                             std::to_string(seq.fetch_add(1));
+      d->shm->create(nm, world, 2 * sim->nz + 2);
+    }
+    *out = d.release();
+  });
+}
+
+int pgpu_dist_ipc_blob_size(int64_t* bytes) {
+  return guard([&] {
+    if (!bytes) throw std::invalid_argument("null pointer");
+    *bytes = (int64_t)sizeof(IpcBlob);
+  });
+}
+
+int pgpu_dist_ipc_export(pgpu_dist* d, void* blob) {
+  return guard([&] {
+    if (!d || !blob) throw std::invalid_argument("null pointer");
+    if (!d->use_ipc) throw ConfigError("not an IPC driver");
+    DistRank& r = d->ranks[0];
+    CK(cudaSetDevice(r.sim->device));
+    IpcBlob b;
+    std::memset(&b, 0, sizeof(b));
+    CK(cudaIpcGetMemHandle(&b.halo, r.halo));
+    for (int i = 0; i < 2; ++i) CK(cudaIpcGetEventHandle(&b.ev[i], r.ev_edge[i]));
+    b.rank = r.rank;
+    b.world = d->world;
+    b.device = r.sim->device;
+    b.halo_n = d->halo_n;
+    if (r.rank == 0) std::snprintf(b.shm, sizeof(b.shm), "%s", d->shm->name.c_str());
+    std::memcpy(blob, &b, sizeof(b));
+  });
+}
+
+// blobs: the `world` exported blobs in rank order
+int pgpu_dist_ipc_connect(pgpu_dist* d, const void* blobs) {
+  return guard([&] {
+    if (!d || !blobs) throw std::invalid_argument("null pointer");
+    if (!d->use_ipc || d->connected) throw ConfigError("not an unconnected IPC driver");
+    DistRank& r = d->ranks[0];
+    CK(cudaSetDevice(r.sim->device));
+    const IpcBlob* all = static_cast<const IpcBlob*>(blobs);
+    const int W = d->world;
+    for (int q = 0; q < W; ++q)
+      if (all[q].rank != q || all[q].world != W || all[q].halo_n != d->halo_n)
+        throw ConfigError("IPC blobs do not describe this decomposition");
+    if (r.rank != 0) d->shm->open_existing(all[0].shm, W, 2 * r.sim->nz + 2);
+    const int left = (r.rank + W - 1) % W, right = (r.rank + 1) % W;
+    const int64_t n = d->halo_n;
+    auto open = [&](int q, DistPeer& pr, DistPeer* same) {
+      double* base;
+      if (q == r.rank) {
+        pr.own = true;
+        base = r.halo;
+        pr.ev[0] = r.ev_edge[0];
+        pr.ev[1] = r.ev_edge[1];
+      } else if (same) {  // world 2: the left and right neighbours are one rank
+        pr = *same;
+        pr.own = true;  // owned (closed) through the other entry
+        return;
+      } else {
+        void* p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, all[q].halo, cudaIpcMemLazyEnablePeerAccess));
+        base = static_cast<double*>(p);
+        pr.base = base;
+        for (int i = 0; i < 2; ++i) CK(cudaIpcOpenEventHandle(&pr.ev[i], all[q].ev[i]));
+      }
+      pr.recv_lo[0] = base + 2 * n;
+      pr.recv_lo[1] = base + 3 * n;
+      pr.recv_hi[0] = base + 4 * n;
+      pr.recv_hi[1] = base + 5 * n;
+    };
+    open(left, d->peer_l, nullptr);
+    open(right, d->peer_r, right == left && left != r.rank ? &d->peer_l : nullptr);
+    d->shm->h->attached.fetch_add(1, std::memory_order_acq_rel);
+    d->shm->barrier();  // every rank mapped its neighbours before any step
+    d->connected = true;
+  });
+}
+
 int pgpu_dist_set_graphs(pgpu_dist* d, int32_t enable) {
   return guard([&] {
     if (!d) throw std::invalid_argument("null handle");
@@ -521,6 +832,7 @@ int pgpu_dist_set_graphs(pgpu_dist* d, int32_t enable) {
 int pgpu_dist_step(pgpu_dist* d, int64_t n) {
   return guard([&] {
     if (!d) throw std::invalid_argument("null handle");
+    if (d->use_ipc && !d->connected) throw ConfigError("IPC driver not connected (pgpu_dist_ipc_connect)");
     if (n < 0) throw ConfigError("step count must be non-negative");
     d->step(n);
   });

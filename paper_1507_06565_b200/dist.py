@@ -110,7 +110,7 @@ class NativeDist:
     `nccl_id`/`rank`/`world` describe the communicator."""
 
     def __init__(self, sims, nccl_id: Optional[bytes] = None, rank: int = 0,
-                 world: Optional[int] = None):
+                 world: Optional[int] = None, ipc_allgather: Optional[Callable] = None):
         import ctypes as C
 
         from . import _lib
@@ -118,7 +118,20 @@ class NativeDist:
         self.sims = list(sims)
         self.world = int(world if world is not None else len(self.sims))
         self._h = C.c_void_p()
-        if nccl_id is None:
+        if ipc_allgather is not None:
+            # IPC transport: the edge kernel stores into the neighbours' ghost
+            # buffers; the blobs travel through the caller's all-gather
+            L = _lib.lib
+            P._check(L.pgpu_dist_create_ipc(self.sims[0]._h, int(rank), self.world,
+                                            C.byref(self._h)))
+            n = C.c_int64()
+            P._check(L.pgpu_dist_ipc_blob_size(C.byref(n)))
+            blob = (C.c_uint8 * n.value)()
+            P._check(L.pgpu_dist_ipc_export(self._h, blob))
+            blobs = ipc_allgather(bytes(blob))
+            allb = (C.c_uint8 * (n.value * self.world)).from_buffer_copy(b"".join(blobs))
+            P._check(L.pgpu_dist_ipc_connect(self._h, allb))
+        elif nccl_id is None:
             arr = (C.c_void_p * len(self.sims))(*[s._h.value for s in self.sims])
             P._check(_lib.lib.pgpu_dist_create_local(arr, len(self.sims), C.byref(self._h)))
         else:
@@ -277,7 +290,7 @@ class SlabSimulation:
     over torch.distributed when it is initialised); CPU engines: DistTransport."""
 
     def __init__(self, workload, rank: int, world: int, device=0, group=None, engine=None,
-                 geometry=None):
+                 geometry=None, transport: str = "nccl"):
         self.me = SlabRank(workload, rank, world, device, engine, geometry=geometry)
         self.sim = self.me.sim
         self.workload = workload
@@ -288,6 +301,15 @@ class SlabSimulation:
             return
         nid = None
         import torch.distributed as tdist
+        if transport == "ipc":
+            def allgather(blob: bytes):
+                if world == 1:
+                    return [blob]
+                out = [None] * world
+                tdist.all_gather_object(out, blob, group=group)
+                return out
+            self.native = NativeDist([self.sim], rank=rank, world=world, ipc_allgather=allgather)
+            return
         if world > 1 and tdist.is_available() and tdist.is_initialized():
             obj = [NativeDist.nccl_unique_id() if rank == 0 else None]
             tdist.broadcast_object_list(obj, src=0, group=group)
