@@ -135,7 +135,21 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PGPU_BENCH_ONE_DEVICE") == "1":
+        local = 0  # test knob: every rank on cuda:0 (the IPC transport's multi-process check)
     return rank, world, local
+
+
+def all_reduce(dist, t, op=None):
+    """torch.distributed all-reduce of a CUDA tensor; through host memory when
+    the process group is gloo (the one-device multi-process check)."""
+    op = op if op is not None else dist.ReduceOp.SUM
+    if dist.get_backend() == "gloo":
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op)
 
 
 def ncu_traffic(config_name: str, math: str, kernel_hash: str):
@@ -242,7 +256,10 @@ def run_ours(args):
         # exchange overlaps the interior instead of queueing behind it
         opts = dist.ProcessGroupNCCL.Options()
         opts.is_high_priority_stream = True
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local), pg_options=opts)
+        if os.environ.get("PGPU_BENCH_BACKEND") == "gloo":  # test knob (with PGPU_BENCH_ONE_DEVICE)
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local), pg_options=opts)
     import paper_1507_06565_b200 as pg
     from paper_1507_06565_b200 import configs
 
@@ -280,7 +297,7 @@ def run_ours(args):
     links_total = links_local
     if dist is not None:
         t = torch.tensor([fluid_local, links_local], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
+        all_reduce(dist, t)
         fluid_total, links_total = int(t[0].item()), int(t[1].item())
         dist.barrier()
 
@@ -305,7 +322,7 @@ def run_ours(args):
     clk = clocks.stop()
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce(dist, t, dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
     value = fluid_total * args.steps / (ms * 1e-3) / 1e6
@@ -564,8 +581,8 @@ def e2e_run_dist(w, geom, steps, rank, world, device, dist, transport="nccl"):
     loc = torch.tensor([t1 - t0, tc - t0, td - tc, t1 - td], dtype=torch.float64, device="cuda")
     fl = torch.tensor([float(ss.sim.fluid_cells)], dtype=torch.float64, device="cuda")
     if dist is not None:
-        dist.all_reduce(loc, op=dist.ReduceOp.MAX)
-        dist.all_reduce(fl)
+        all_reduce(dist, loc, dist.ReduceOp.MAX)
+        all_reduce(dist, fl)
     tt, tcr, tst, tpr = (float(v) for v in loc.cpu())
     d2h = host.nbytes + 5 * prof.z.nbytes
     del ss

@@ -340,7 +340,8 @@ class SlabSimulation:
         import torch.distributed as tdist
         if self.me.world > 1 and tdist.is_initialized():
             import torch
-            t = torch.tensor([counts.sum()], dtype=torch.float64, device="cuda")
+            dev = "cpu" if tdist.get_backend() == "gloo" else "cuda"
+            t = torch.tensor([counts.sum()], dtype=torch.float64, device=dev)
             tdist.all_reduce(t)
             return int(t.item())
         return int(counts.sum())
