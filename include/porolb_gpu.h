@@ -259,7 +259,8 @@ int pgpu_get_layout(pgpu_sim* sim, int32_t* layout);
  * results are bit-identical): AUTO (the library's choice), CPIPE (per-thread
  * asynchronous copies, k_sweep_cpipe) or TMA (warp-specialised bulk-copy
  * pipeline, k_sweep_tma).  PGPU_SWEEP=cpipe|tma sets the default at creation. */
-enum pgpu_sweep_kernel { PGPU_SWEEP_AUTO = 0, PGPU_SWEEP_CPIPE = 1, PGPU_SWEEP_TMA = 2 };
+enum pgpu_sweep_kernel { PGPU_SWEEP_AUTO = 0, PGPU_SWEEP_CPIPE = 1, PGPU_SWEEP_TMA = 2,
+                         PGPU_SWEEP_TB2 = 3 /* two steps per launch (temporal blocking) */ };
 int pgpu_set_sweep_kernel(pgpu_sim* sim, int32_t kind);
 /* Instantiate the step's CUDA graphs now (no time step is taken; no reference
  * analogue): a later step() does not pay their capture.  Optional. */

@@ -105,6 +105,7 @@ struct pgpu_sim {
   unsigned long long* d_vmax = nullptr;
   double* d_sums = nullptr;
   uint32_t* d_tickets = nullptr;  // TMA sweep work counter (KParams::tickets)
+  TbState* tb = nullptr;          // two-step sweep buffers (ring, row tables, counters)
   // state
   int cur = 0;
   bool post = false;
@@ -144,6 +145,7 @@ struct pgpu_sim {
     cudaFree(d_vmax);
     cudaFree(d_sums);
     cudaFree(d_tickets);
+    tb_destroy(tb);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 
@@ -304,6 +306,7 @@ struct pgpu_sim {
   int resolved_sweep() const {
     if (!compact) return PGPU_SWEEP_AUTO;
     if (kp.sweep == PGPU_SWEEP_TMA && tma_sweep_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_TMA;
+    if (kp.sweep == PGPU_SWEEP_TB2 && tb_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_TB2;
     return PGPU_SWEEP_CPIPE;
   }
 
@@ -339,6 +342,7 @@ struct pgpu_sim {
     if (d_linkdesc) b += (n_links + 16) * (int64_t)sizeof(uint16_t);
     if (d_planes) b += nz * (int64_t)sizeof(PlaneCoef);
     if (d_scratch) b += scratch_n * (int64_t)sizeof(double);
+    b += tb_device_bytes(tb);
     b += (19 + 2 + 1 + nz) * 8;  // feq, flags, vmax, plane sums
     return b;
   }
@@ -457,6 +461,23 @@ struct pgpu_sim {
         }
         cudaGetLastError();
         persistent = false;  // not launchable here: fall back to graphs
+      }
+      if (n - i >= 2 && kp.sweep == PGPU_SWEEP_TB2 && compact) {
+        // two steps per launch (temporal blocking), one launch per pair
+        const SweepConfig c = sweep_cfg(0, 0);
+        if (tb_supported(c, kp)) {
+          if (!tb) tb = tb_create(kp, stream);
+          Nvtx r("K1x2 two-step sweep");
+          set_ghost_ptrs();
+          if (tb && launch_sweep_tb2(c, kp, tb, f[cur], f[1 - cur], stream)) {
+            check_launch();
+            launches += 2;  // the counter reset and the sweep
+            cur = 1 - cur;
+            steps += 2;
+            i += 2;
+            continue;
+          }
+        }
       }
       if (n - i >= kGraphSteps) {
         if (graph_stream != stream) drop_graphs();

@@ -74,7 +74,7 @@ class MathMode(enum.IntEnum):
 
 
 # pgpu_sweep_kernel (include/porolb_gpu.h), by value
-SWEEP_KERNELS = ("auto", "cpipe", "tma")
+SWEEP_KERNELS = ("auto", "cpipe", "tma", "tb2")
 
 
 class GlbmViscosity(enum.IntEnum):

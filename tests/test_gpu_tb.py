@@ -1,0 +1,163 @@
+"""The two-step sweep (temporal blocking, sweep_tb.cu, pgpu_sweep_kernel TB2)
+bit for bit: against the oracle in math mode EXACT (reference arithmetic) and
+against the one-step sweep (k_sweep_cpipe) in math mode FAST, on the corner
+cases of its schedule -- y-bands with halo rows (periodic y wraps the halo),
+row segments of 128 cells that are partial (nx = 160, 36, 20), x-periodic
+faces, odd step counts (the last step is a one-step sweep), walls, CLI beds, a
+moving lid (+inf records) and the GLBM collision."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def fluid_mask(geom):
+    nx, ny, nz = geom.dims
+    return geom.flags.reshape(nz, ny, nx) == 0
+
+
+def geometry(pg, dims, n, rmin, rmax, seed, periodic=(True, True, False), walls=True):
+    rng = np.random.default_rng(seed)
+    zlo, zhi = (1.0, dims[2] - 1.0) if walls else (0.0, float(dims[2]))
+    c = np.c_[rng.uniform(0, dims[0], n), rng.uniform(0, dims[1], n), rng.uniform(zlo, zhi, n)]
+    r = rng.uniform(rmin, rmax, n)
+    pack = pg.SpherePack(c, r, tuple(float(d) for d in dims))
+    return pg.voxelize(pack, dims, periodic, walls, walls)
+
+CASES = {
+    # name: dims, n spheres, r range, periodic, walls
+    "nx160_partial_segment": ((160, 20, 24), 14, 2.0, 5.0, (True, True, False), True),
+    "nx36_short_row": ((36, 18, 22), 6, 2.0, 4.0, (True, True, False), True),
+    "nx20_one_chunk": ((20, 18, 22), 6, 2.0, 4.0, (True, True, False), True),
+        "bed_128": ((128, 32, 40), 40, 3.0, 6.0, (True, True, False), True),
+}
+
+
+def _params(pg):
+    p = pg.relaxation_from_magic(0.08, 3.0 / 16.0)
+    p.body_force = (2e-6, 1e-6, -5e-7)
+    return p
+
+
+def _random_state(geom, seed):
+    nx, ny, nz = geom.dims
+    m = fluid_mask(geom)
+    rng = np.random.default_rng(seed)
+    f0 = 1e-3 * (2.0 * rng.random((19, nz, ny, nx)) - 1.0)
+    f0[:, ~m] = 0.0
+    return f0, m
+
+
+def _tma_sim(pg, monkeypatch, geom, p, scheme):
+    monkeypatch.setenv("PGPU_LAYOUT", "compact")
+    monkeypatch.setenv("PGPU_SWEEP", "tb2")
+    sim = pg.Simulation.from_params(geom, p, pg.WallScheme(scheme))
+    assert sim.layout == "fluid-only"
+    assert sim.sweep_kernel == "tb2", "the two-step sweep does not run for this simulation"
+    return sim
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_tb_exact_vs_oracle(gpu, orc, monkeypatch, case, scheme):
+    dims, n, rmin, rmax, per, walls = CASES[case]
+    geom = geometry(gpu, dims, n, rmin, rmax, seed=len(case) + 3, periodic=per, walls=walls)
+    assert geom.n_links > 0
+    p = _params(gpu)
+    sim = _tma_sim(gpu, monkeypatch, geom, p, scheme)
+    o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, scheme)
+    f0, m = _random_state(geom, 5)
+    sim.set_pdfs(f0)
+    o.set_pdfs(f0)
+    for k in (1, 2, 17, 20, 3):  # K0 + pairs, odd counts end on a one-step sweep
+        sim.step(k)
+        o.step(k)
+        got, want = sim.get_pdfs(), o.get_pdfs()
+        assert np.array_equal(got[:, m], want[:, m]), f"pdfs differ after {k} more steps"
+    d, ux, uy, uz = sim.macroscopic_fields()
+    od, oux, ouy, ouz = o.macroscopic_fields()
+    mf = m.reshape(-1)
+    for a, b in ((d, od), (ux, oux), (uy, ouy), (uz, ouz)):
+        assert np.array_equal(np.ravel(a)[mf], np.ravel(b)[mf])
+
+
+def test_tb_walled_channel(gpu, orc, monkeypatch):
+    """An all-fluid walled channel (5 links per cell next to the walls)."""
+    geom = gpu.make_box_geometry((128, 8, 12), (True, True, False), True, True)
+    for scheme in (0, 1):
+        p = _params(gpu)
+        sim = _tma_sim(gpu, monkeypatch, geom, p, scheme)
+        o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, scheme)
+        f0, m = _random_state(geom, 9)
+        sim.set_pdfs(f0)
+        o.set_pdfs(f0)
+        sim.step(7)
+        o.step(7)
+        assert np.array_equal(sim.get_pdfs()[:, m], o.get_pdfs()[:, m])
+
+
+def test_tb_moving_lid(gpu, orc, monkeypatch):
+    dims = (128, 16, 20)
+    geom = geometry(gpu, dims, 10, 2.0, 4.0, seed=21)
+    p = _params(gpu)
+    for scheme in (0, 1):
+        sim = _tma_sim(gpu, monkeypatch, geom, p, scheme)
+        o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, scheme)
+        f0, m = _random_state(geom, 3)
+        sim.set_pdfs(f0)
+        o.set_pdfs(f0)
+        sim.set_lid_velocity((0.01, -0.004, 0.0))
+        o.set_lid_velocity((0.01, -0.004, 0.0))
+        sim.step(19)
+        o.step(19)
+        assert np.array_equal(sim.get_pdfs()[:, m], o.get_pdfs()[:, m])
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_tb_fast_equals_cpipe_fast(gpu, monkeypatch, scheme):
+    """Math mode FAST: the two K1 kernels share the collision, so they agree
+    bit for bit (and FAST itself is checked against the reference in
+    test_gpu_fast.py)."""
+    dims = (128, 32, 40)
+    geom = geometry(gpu, dims, 40, 3.0, 6.0, seed=4)
+    p = _params(gpu)
+    sim = _tma_sim(gpu, monkeypatch, geom, p, scheme)
+    sim.math_mode = gpu.MathMode.FAST
+    monkeypatch.setenv("PGPU_SWEEP", "cpipe")
+    ref = gpu.Simulation.from_params(geom, p, gpu.WallScheme(scheme))
+    ref.math_mode = gpu.MathMode.FAST
+    assert ref.sweep_kernel == "cpipe"
+    f0, m = _random_state(geom, 7)
+    sim.set_pdfs(f0)
+    ref.set_pdfs(f0)
+    sim.step(37)
+    ref.step(37)
+    assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
+    # switching the kernel mid-run keeps the trajectory
+    sim.sweep_kernel = "cpipe"
+    ref.sweep_kernel = "tb2"
+    sim.step(5)
+    ref.step(5)
+    assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
+
+
+def test_tb_glbm_fluid_only(gpu, orc, monkeypatch):
+    """The GLBM collision (per-plane coefficients by z) on the TMA sweep."""
+    dims = (128, 12, 24)
+    geom = geometry(gpu, dims, 8, 2.0, 4.0, seed=33)
+    p = _params(gpu)
+    sim = _tma_sim(gpu, monkeypatch, geom, p, 1)
+    o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, 1)
+    nz = dims[2]
+    z = np.arange(nz)
+    eps = np.where(z < nz // 2, 0.6, 1.0) - 0.01 * (z % 3)
+    K = gpu.kozeny_carman(eps, 10.0)
+    gp = gpu.make_glbm_params(eps, K, 0.3, p.nu, 3.0 / 16.0, gpu.GlbmViscosity.Rescaled)
+    sim.set_porous(gp)
+    o.set_porous(gp.eps, gp.permeability, gp.omega_plus, gp.omega_minus, 0.3, True)
+    f0, m = _random_state(geom, 13)
+    sim.set_pdfs(f0)
+    o.set_pdfs(f0)
+    sim.step(21)
+    o.step(21)
+    assert np.array_equal(sim.get_pdfs()[:, m], o.get_pdfs()[:, m])
