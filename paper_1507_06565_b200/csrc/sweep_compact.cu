@@ -52,6 +52,10 @@ __device__ __forceinline__ void cpa4(void* smem_dst, const void* gsrc) {
                : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+// Programmatic dependent launch (no-ops without the launch attribute): let the
+// next sweep's blocks start, and wait for the previous grid's results.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
@@ -546,6 +550,9 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
   constexpr bool kStaticDesc = RECORDS && kS == 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Sm& S = *reinterpret_cast<Sm*>(smem_raw);
+  // with programmatic dependent launch the next sweep's blocks may be
+  // scheduled now: their static meta loads overlap this grid's tail
+  pdl_trigger();
   const int tx = threadIdx.x, lane = tx & 31, warp = tx >> 5;
   // warps are independent: a block covers 4 chunks of one row, or (edge part,
   // x-slab split) the first and last chunk of two rows
@@ -743,12 +750,14 @@ __global__ void __launch_bounds__(kCBXp, cp_minb(RECORDS))
     desc_load(0);
     if (z0 + 1 < z1) desc_load(1);
     cpa_commit();
+    pdl_wait();  // everything before read static data; populations come from the previous sweep
     issue(z0, 0, 0, 1);
     cpa_commit();
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // the descriptors (not the populations)
     __syncwarp();
     cnt_cur = issue(z0, 0, 0, 2);
   } else {
+    pdl_wait();
     cnt_cur = issue(z0, 0, 0);
   }
   __syncwarp();
@@ -935,8 +944,24 @@ void launch_compact_t(const SweepConfig& cfg, const KParams& p, const double* sr
       return true;
     }();
     (void)attr;
-    k_sweep_cpipe<CM, GLBM, RECORDS, SLAB, OP><<<grid, kCBXp, smem, s>>>(p, src, dst, cfg.part,
-                                                                         zper, cfg.zrev ? 1 : 0);
+    // whole-domain sweeps launch as programmatic dependents of the previous
+    // kernel (PGPU_PDL=0: off): their prologue overlaps its tail
+    static const bool pdl_env = [] {
+      const char* e = std::getenv("PGPU_PDL");
+      return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(kCBXp);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = (pdl_env && !SLAB && cfg.part == PART_ALL && OP == OP_STREAM_COLLIDE) ? 1 : 0;
+    cudaLaunchKernelEx(&lc, k_sweep_cpipe<CM, GLBM, RECORDS, SLAB, OP>, p, src, dst, cfg.part, zper,
+                       cfg.zrev ? 1 : 0);
   }
 }
 
