@@ -341,6 +341,9 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
     k_sweep_pipe(const KParams p, const double* __restrict__ src, double* __restrict__ dst,
                  int part, int zper) {
   extern __shared__ double smem[];
+  // programmatic dependent launch (no-op without the attribute): the next
+  // sweep's blocks may start during this grid's tail
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   constexpr int kStages = pipe_stages(RECORDS);
   const int tx = threadIdx.x;
   const int lane = tx & 31, warp = tx >> 5;
@@ -418,6 +421,8 @@ __global__ void __launch_bounds__(kPipeBX, pipe_minb(RECORDS))
   // row) and masked where used, so no select waits on a load in flight.
   CellWord cw_cur = kSkip;
   CellWord cw_next = ld_w(z0);
+  // static data only so far; the populations come from the previous sweep
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   int off_cur = 0;
   int s = kStages == 2 ? 1 : 0;
   for (int z = z0 - 1; z < z_end(); ++z) {
@@ -823,8 +828,21 @@ void launch_sweep_t(const KParams& p, const double* src, double* dst, int part,
       return true;
     }();
     (void)attr;
-    k_sweep_pipe<CM, GLBM, RECORDS, SLAB, OP><<<grid, kPipeBX, pipe_smem(RECORDS), s>>>(p, src, dst,
-                                                                                 part, zper);
+    static const bool pdl_env = [] {
+      const char* e = std::getenv("PGPU_PDL");
+      return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(kPipeBX);
+    lc.dynamicSmemBytes = pipe_smem(RECORDS);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = (pdl_env && !SLAB && part == PART_ALL && OP == OP_STREAM_COLLIDE) ? 1 : 0;
+    cudaLaunchKernelEx(&lc, k_sweep_pipe<CM, GLBM, RECORDS, SLAB, OP>, p, src, dst, part, zper);
   } else {
     k_sweep<CM, GLBM, RECORDS, SLAB, OP><<<sweep_grid(p), cell_block(p), 0, s>>>(p, src, dst,
                                                                                   part);
