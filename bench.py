@@ -269,6 +269,7 @@ def run_ours(args):
         w = configs.c4(nx_scale=world) if (args.config == "C4" and args.scaling == "weak") \
             else configs.ALL[args.config]()
         sim_obj = SlabSimulation(w, rank, world, device=local, transport=args.transport)
+        halo_transport = sim_obj.transport  # "ipc", or "nccl" (also the fallback)
         sim = sim_obj.sim
         fluid_local = sim.fluid_cells
         stepper = sim_obj.step
@@ -351,7 +352,7 @@ def run_ours(args):
         e2e = e2e_run(pg, configs, w, geom, args.steps, local, args.e2e_output)
     elif (world > 1 or args.force_slab) and not args.no_e2e:
         slab_geom = sim_obj.me.geometry
-        e2e = e2e_run_dist(w, slab_geom, args.steps, rank, world, local, dist, args.transport)
+        e2e = e2e_run_dist(w, slab_geom, args.steps, rank, world, local, dist, halo_transport)
     del sim, stepper
     if world > 1 or args.force_slab:
         del sim_obj
@@ -403,7 +404,7 @@ def run_ours(args):
             "per_config": per_config,
         }
         if world > 1 or args.force_slab:
-            line["halo_transport"] = args.transport
+            line["halo_transport"] = halo_transport
         if parity is not None:
             line["parity"] = parity
         print(json.dumps(line), flush=True)

@@ -37,6 +37,7 @@
 #include <unistd.h>
 
 #include <atomic>
+#include <exception>
 #include <chrono>
 #include <cstdlib>
 #include <memory>
@@ -814,10 +815,16 @@ int pgpu_dist_ipc_connect(pgpu_dist* d, const void* blobs) {
       pr.recv_hi[0] = base + 4 * n;
       pr.recv_hi[1] = base + 5 * n;
     };
-    open(left, d->peer_l, nullptr);
-    open(right, d->peer_r, right == left && left != r.rank ? &d->peer_l : nullptr);
+    std::exception_ptr err;
+    try {
+      open(left, d->peer_l, nullptr);
+      open(right, d->peer_r, right == left && left != r.rank ? &d->peer_l : nullptr);
+    } catch (...) {
+      err = std::current_exception();
+    }
     d->shm->h->attached.fetch_add(1, std::memory_order_acq_rel);
-    d->shm->barrier();  // every rank mapped its neighbours before any step
+    d->shm->barrier();  // every rank mapped its neighbours (or failed) before any step
+    if (err) std::rethrow_exception(err);
     d->connected = true;
   });
 }

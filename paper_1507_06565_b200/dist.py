@@ -120,17 +120,35 @@ class NativeDist:
         self._h = C.c_void_p()
         if ipc_allgather is not None:
             # IPC transport: the edge kernel stores into the neighbours' ghost
-            # buffers; the blobs travel through the caller's all-gather
+            # buffers; the blobs travel through the caller's all-gather.  Every
+            # step is collective, so a failure on one rank fails them all
+            # (self.ok) instead of leaving the others waiting.
             L = _lib.lib
-            P._check(L.pgpu_dist_create_ipc(self.sims[0]._h, int(rank), self.world,
-                                            C.byref(self._h)))
-            n = C.c_int64()
-            P._check(L.pgpu_dist_ipc_blob_size(C.byref(n)))
-            blob = (C.c_uint8 * n.value)()
-            P._check(L.pgpu_dist_ipc_export(self._h, blob))
-            blobs = ipc_allgather(bytes(blob))
-            allb = (C.c_uint8 * (n.value * self.world)).from_buffer_copy(b"".join(blobs))
-            P._check(L.pgpu_dist_ipc_connect(self._h, allb))
+            self.ok = False
+            blob = None
+            try:
+                P._check(L.pgpu_dist_create_ipc(self.sims[0]._h, int(rank), self.world,
+                                                C.byref(self._h)))
+                n = C.c_int64()
+                P._check(L.pgpu_dist_ipc_blob_size(C.byref(n)))
+                buf = (C.c_uint8 * n.value)()
+                P._check(L.pgpu_dist_ipc_export(self._h, buf))
+                blob = bytes(buf)
+            except Exception as e:  # noqa: BLE001
+                self.error = repr(e)
+            blobs = ipc_allgather(blob)
+            ok = all(b is not None for b in blobs)
+            if ok:
+                allb = (C.c_uint8 * len(b"".join(blobs))).from_buffer_copy(b"".join(blobs))
+                try:
+                    P._check(L.pgpu_dist_ipc_connect(self._h, allb))
+                except Exception as e:  # noqa: BLE001
+                    self.error = repr(e)
+                    ok = False
+            self.ok = all(ipc_allgather(ok))
+            if not self.ok:
+                self.close()
+            return
         elif nccl_id is None:
             arr = (C.c_void_p * len(self.sims))(*[s._h.value for s in self.sims])
             P._check(_lib.lib.pgpu_dist_create_local(arr, len(self.sims), C.byref(self._h)))
@@ -296,20 +314,28 @@ class SlabSimulation:
         self.workload = workload
         self._cpu = None
         self.native = None
+        self.transport = transport if engine is None else "gloo"
         if engine is not None:
             self._cpu = DistTransport(self.me, group)
             return
         nid = None
         import torch.distributed as tdist
         if transport == "ipc":
-            def allgather(blob: bytes):
+            def allgather(obj):
                 if world == 1:
-                    return [blob]
+                    return [obj]
                 out = [None] * world
-                tdist.all_gather_object(out, blob, group=group)
+                tdist.all_gather_object(out, obj, group=group)
                 return out
-            self.native = NativeDist([self.sim], rank=rank, world=world, ipc_allgather=allgather)
-            return
+            nd = NativeDist([self.sim], rank=rank, world=world, ipc_allgather=allgather)
+            if nd.ok:
+                self.native = nd
+                return
+            # CUDA IPC unavailable on some rank: every rank falls back to NCCL
+            import warnings
+            warnings.warn(f"IPC halo transport unavailable ({getattr(nd, 'error', 'another rank')}); "
+                          "using NCCL")
+            self.transport = "nccl"
         if world > 1 and tdist.is_available() and tdist.is_initialized():
             obj = [NativeDist.nccl_unique_id() if rank == 0 else None]
             tdist.broadcast_object_list(obj, src=0, group=group)
