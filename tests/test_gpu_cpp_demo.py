@@ -57,3 +57,15 @@ def test_dist_demo_cpp_multi_gpu_host_path(gpu):
         assert out["local_bitwise"] and out["local_profile"] and out["local_vmax_equal"], out
         assert out["nccl_error"] == "", out["nccl_error"]
         assert out["nccl_bitwise"] and out["nccl_profile"] and out["nccl_vmax_equal"], out
+
+
+def test_dist_demo_cpp_ipc_world2(gpu):
+    """DistSimulation::ipc (C++): two processes (fork, blobs through pipes) on
+    one B200, the edge kernels storing into each other's ghost buffers; each
+    slab bit-identical to the single domain, profile and max speed equal."""
+    exe = Path(__file__).resolve().parent / "cpp" / "dist_demo"
+    res = subprocess.run([str(exe), "ipc", "128", "32", "48", "15"], capture_output=True,
+                         text=True, timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr
+    out = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert out["error"] == "" and out["rank0_ok"] and out["rank1_ok"], (out, res.stderr[-2000:])
