@@ -3,7 +3,8 @@
 --page source --print-source=sass), plus profiles/ncu_traffic.json entries
 keyed by workload|math and the kernel build hash.
 
-usage: ncu_csv_summary.py DIR KERNEL_HASH [--traffic-json profiles/ncu_traffic.json]
+usage: ncu_csv_summary.py DIR KERNEL_HASH [--prefix r02] [--traffic-json profiles/ncu_traffic.json]
+The peak is MEASURED_PEAKS.json's hbm_gbs when present.
 """
 import csv
 import io
@@ -13,7 +14,10 @@ import sys
 from collections import defaultdict
 from pathlib import Path
 
-PEAK = 6551.7  # MEASURED_PEAKS.json hbm_gbs (copy bandwidth, GB/s)
+try:  # MEASURED_PEAKS.json hbm_gbs (copy bandwidth, GB/s), driver-written per pool
+    PEAK = float(json.loads(Path("MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+except Exception:  # noqa: BLE001
+    PEAK = 6551.7
 # name: (workload key of bench.py, math, fluid cells, warp-planes of the kernel)
 RUNS = {
     "c4_cli_fast": ("C4_bed_512x256x512_cli", "fast", 51785984, 16 * 256 * 512),
@@ -69,13 +73,14 @@ def main():
     d = Path(sys.argv[1])
     khash = sys.argv[2]
     tj = Path(sys.argv[sys.argv.index("--traffic-json") + 1]) if "--traffic-json" in sys.argv else None
+    pre = sys.argv[sys.argv.index("--prefix") + 1] if "--prefix" in sys.argv else "r02"
     out = ["| capture | kernel | time (ms) | DRAM read + write per launch | traffic / algorithmic |"
-           " DRAM GB/s (% of 6552) | algorithmic GB/s = roofline frac | warps active | regs |"
+           f" DRAM GB/s (% of {PEAK:.0f}) | algorithmic GB/s = roofline frac | warps active | regs |"
            " top stalls |", "|---|---|---|---|---|---|---|---|---|---|"]
     hist = []
     traffic = json.loads(tj.read_text()) if tj and tj.exists() else {}
     for name, (wl, math, fluid, wplanes) in RUNS.items():
-        rp = d / f"r02_{name}.raw.csv"
+        rp = d / f"{pre}_{name}.raw.csv"
         if not rp.exists():
             continue
         kname, get, stalls = raw(rp)
@@ -98,8 +103,8 @@ def main():
             "kernel": k, "kernel_hash": khash, "dram_bytes_per_launch": (rd + wr) * 1e9,
             "dram_read_bytes": rd * 1e9, "dram_write_bytes": wr * 1e9, "duration_ms_ncu": t_ms,
             "algorithmic_bytes_per_launch": 304 * fluid,
-            "source": f"profiles/r02_ncu_summary.md (ncu --set full, 1 launch, {name})"}
-        sp = d / f"r02_{name}.sass.csv"
+            "source": f"profiles/{pre}_ncu_summary.md (ncu --set full, 1 launch, {name})"}
+        sp = d / f"{pre}_{name}.sass.csv"
         if sp.exists():
             warp, thr = sass(sp)
             tw = sum(warp.values())
