@@ -182,23 +182,28 @@ def config_dict(name, fluid, cells, links, scheme, world, meta, slab=None):
 def reference_cpu_sample(sim, fluid_cells: int, budget_s: float, warmup: int = 3,
                          max_steps: int = 1_000_000):
     """The one sampler of both CPU legs: `warmup` (>= 3) untimed steps of the
-    reference Simulation::step(), then as many steps as fit in ~budget_s
-    (at most max_steps).  Returns (fluid MLUPS, steps, seconds, warmup)."""
+    reference Simulation::step(), then steps timed one by one until ~budget_s
+    (at most max_steps); the rate is taken at the MEDIAN step time, so a
+    transient disturbance of the shared host does not move either leg.
+    Returns (fluid MLUPS, steps, seconds, warmup)."""
     w = max(3, int(warmup))
-    t0 = time.perf_counter()
     sim.step(w)
-    per = (time.perf_counter() - t0) / w
-    n = max(1, min(int(max_steps), int(budget_s / max(per, 1e-9))))
-    t0 = time.perf_counter()
-    sim.step(n)
-    dt = time.perf_counter() - t0
-    return fluid_cells * n / dt / 1e6, n, dt, w
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max(1, int(max_steps)):
+        t0 = time.perf_counter()
+        sim.step(1)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start >= budget_s:
+            break
+    med = statistics.median(times)
+    return fluid_cells / med / 1e6, len(times), sum(times), w
 
 
 def cpu_sample_text(name, n, w, dt, threads):
-    return (f"{name}: {n} time steps of the reference Simulation::step() (oracle/_ref, OpenMP "
+    return (f"{name}: {n} time steps of the reference Simulation::step() (timed one by one; oracle/_ref, OpenMP "
             f"{threads} threads = physical cores, OMP_PLACES=cores OMP_PROC_BIND=close) after "
-            f"{w} warm-up steps, {dt:.1f} s")
+            f"{w} warm-up steps, {dt:.1f} s; rate at the median step time)")
 
 
 def run_reference_arm(args):

@@ -63,7 +63,7 @@ namespace {
 #define PGPU_TMA_PROD 2
 #endif
 #ifndef PGPU_TMA_BATCH
-#define PGPU_TMA_BATCH 4
+#define PGPU_TMA_BATCH 1
 #endif
 constexpr int kTNC = PGPU_TMA_NC;       // consumer warps = chunks per item
 constexpr int kTS = PGPU_TMA_STAGES;    // stages of the ring
