@@ -122,7 +122,9 @@ struct pgpu_sim {
   static constexpr int kGraphSteps = 16;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   bool persistent = false;  // L2-resident domain: cooperative multi-step sweep
-  bool zrev_on = true;      // alternate the z order of consecutive sweeps (PGPU_ZREV=0: off)
+  // alternate the z order of consecutive SBB sweeps (PGPU_ZREV=0: off); CLI
+  // sweeps keep the bed's link-heavy z-blocks first instead (less tail)
+  bool zrev_on = true;
   cudaStream_t graph_stream = nullptr;
   KParams kp{};
 
@@ -393,7 +395,7 @@ struct pgpu_sim {
     Nvtx r(part == 0 ? "K1 sweep" : (part == 1 ? "K1 edge columns" : "K1 interior columns"));
     set_ghost_ptrs();
     SweepConfig c = sweep_cfg(0, part);
-    c.zrev = zrev_on && cur == 1;
+    c.zrev = zrev_on && !c.records && cur == 1;
     launch_sweep(c, kp, f[cur], f[1 - cur], stream);
     check_launch();
     ++launches;
@@ -419,7 +421,7 @@ struct pgpu_sim {
     int c = start;
     for (int i = 0; i < kGraphSteps; ++i) {
       SweepConfig sc = sweep_cfg(0, 0);
-      sc.zrev = zrev_on && c == 1;
+      sc.zrev = zrev_on && !sc.records && c == 1;
       launch_sweep(sc, kp, f[c], f[1 - c], cs);
       c = 1 - c;
     }
