@@ -211,7 +211,8 @@ struct alignas(128) TSmem {
   TStage st[kTS];
   TMeta meta[kTP][kTM];
   uint64_t full[kTS];   // bulk bytes of the stage (and the producer's header stores)
-  uint64_t xfull[kTS];  // link-source copies of the stage (32 producer lanes)
+  uint64_t xfull[kTS];  // link-source copies of the stage (32 link-warp lanes)
+  uint64_t hdr[kTS];    // the stage header is written (the link warp starts on it)
   uint64_t empty[kTS];  // kTNC consumer warps released the stage
 };
 
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kTThreads, GLBM ? 1 : PGPU_TMA_MINB)
     for (int s = 0; s < kTS; ++s) {
       mbar_init(&S.full[s], 1);  // the producer's expect_tx arrival; the bulk bytes complete it
       mbar_init(&S.xfull[s], 32);
+      mbar_init(&S.hdr[s], 1);
       mbar_init(&S.empty[s], kTNC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -377,6 +379,7 @@ __global__ void __launch_bounds__(kTThreads, GLBM ? 1 : PGPU_TMA_MINB)
       if (t == kTDone) {  // publish the end of this producer's items
         if (lane == 0) {
           T.item = kTDone;
+          mbar_arrive(&S.hdr[s]);
           mbar_arrive_tx(&S.full[s], 0u);
         }
         break;
@@ -420,7 +423,7 @@ __global__ void __launch_bounds__(kTThreads, GLBM ? 1 : PGPU_TMA_MINB)
       if (lane == 0) {
         T.cb_lo = cb_lo;
         T.recoff = cb_lo & 1;
-        T.descoff = cb_lo & 7;
+        T.descoff = cb_lo & 1;
         T.x0 = it.x0;
         T.z = it.z;
         T.item = t;
@@ -441,8 +444,10 @@ __global__ void __launch_bounds__(kTThreads, GLBM ? 1 : PGPU_TMA_MINB)
         }
         T.wsrc[lane] = w;
       }
+      __syncwarp();  // the header is complete: the link warp may start on the item
+      if (lane == 0) mbar_arrive(&S.hdr[s]);
       // bulk copies: lanes 0..18 the direction runs, 19 the cell words, 20 the
-      // records, 21 the link descriptors
+      // records
       uint32_t bytes = 0, bdst = 0;
       const void* bsrc = nullptr;
       {
@@ -466,11 +471,6 @@ __global__ void __launch_bounds__(kTThreads, GLBM ? 1 : PGPU_TMA_MINB)
           bytes = (uint32_t)(((cb_lo + nl - a0) + 1) & ~1) * 8u;
           bsrc = p.links + a0;
           bdst = tsmem(&T.rec[0]);
-        } else if (lane == 21 && nl > 0) {
-          const int a0 = cb_lo & ~7;
-          bytes = (uint32_t)(((cb_lo + nl - a0) + 7) & ~7) * 2u;
-          bsrc = p.linkdesc + a0;
-          bdst = tsmem(&T.desc[0]);
         }
       }
       uint32_t total = bytes;
@@ -488,13 +488,15 @@ __global__ void __launch_bounds__(kTThreads, GLBM ? 1 : PGPU_TMA_MINB)
     twait_group<0>();
   } else if (warp == kTP) {
     // ------------------------------------------------------------------- link warp
-    // As soon as a stage's bulk data (descriptors, ranks) has landed, copy its
-    // link sources: g_k(x) and, for CLI, g_j(x) per link, and the x-wrap pulls.
+    // As soon as a stage's header is written (while its bulk copies fly), load
+    // the item's link descriptors, then copy its link sources: g_k(x) and, for
+    // CLI, g_j(x) per link, and the x-wrap pulls -- in parallel with the bulk
+    // data instead of after it.
     uint32_t fin = 0;
     for (uint32_t k = 0; fin != (1u << kTP) - 1u; ++k) {
       if ((fin >> (k % kTP)) & 1u) continue;
       const int s = (int)(k % kTS);
-      mbar_wait(&S.full[s], (k / kTS) & 1u);
+      mbar_wait(&S.hdr[s], (k / kTS) & 1u);
       TStage& T = S.st[s];
       if (T.item == kTDone) {
         fin |= 1u << (k % kTP);
@@ -502,6 +504,12 @@ __global__ void __launch_bounds__(kTThreads, GLBM ? 1 : PGPU_TMA_MINB)
       }
       const int nl = min(T.lofs[kTNC], kTLC);
       if (nl > 0) {
+        const int32_t cb = T.cb_lo;
+        const int a0 = cb & ~1, npairs = (cb + nl - a0 + 1) >> 1;
+        for (int i = lane; i < npairs; i += 32) tcpa4(&T.desc[2 * i], p.linkdesc + a0 + 2 * i);
+        tcommit();
+        twait_group<0>();
+        __syncwarp();
         int32_t lb[kTNC - 1];
 #pragma unroll
         for (int q = 0; q < kTNC - 1; ++q) lb[q] = T.lofs[q + 1];

@@ -10,6 +10,6 @@ import json; d=json.load(open('gpurun_out/ab_$l.json')); print('$l', round(d['va
 }
 run cpipe PGPU_SWEEP=cpipe
 run tma PGPU_SWEEP=tma
-run tma_b1 PGPU_SWEEP=tma PGPU_LIB=paper_1507_06565_b200/_variants/b1/libporolb_cuda.so
-run tma_nc8 PGPU_SWEEP=tma PGPU_LIB=paper_1507_06565_b200/_variants/nc8/libporolb_cuda.so
-run tma_s2 PGPU_SWEEP=tma PGPU_LIB=paper_1507_06565_b200/_variants/s2/libporolb_cuda.so
+
+
+
