@@ -788,13 +788,10 @@ dim3 cell_grid2(const KParams& p) {
   const int bx = cell_block(p).x;
   return dim3((p.nx + bx - 1) / bx, p.ny, p.nz);
 }
-// z-planes per block: long marching columns, but at least ~4 waves of blocks
-// over 148 SMs x 4 resident blocks.
+// z-planes per block: long marching columns, but at least ~6.5 waves of
+// blocks over 148 SMs x 4 resident blocks (zper_for, sweep_compact.cu).
 int pipe_zper(const KParams& p) {
-  if (const char* e = std::getenv("PGPU_ZPER")) return std::max(1, std::min(atoi(e), p.nz));
-  const int64_t cols = (int64_t)((p.nx + kPipeBX - 1) / kPipeBX) * p.ny;
-  int zper = (int)std::min<int64_t>(8, std::max<int64_t>(1, cols * p.nz / (148 * 4 * 4)));
-  return std::min(zper, p.nz);
+  return zper_for((int64_t)((p.nx + kPipeBX - 1) / kPipeBX) * p.ny, p.nz);
 }
 // PGPU_SWEEP=pipe (default) | plain: the async-copy pipeline, or the plain
 // one-cell-per-thread sweep kept as the round-1 reference point.

@@ -52,6 +52,8 @@ void launch_fill_compact(const KParams& p, int64_t nfluid, double* f, const doub
                          cudaStream_t s);
 // One cooperative launch running nsteps K1 sweeps (a -> b -> a ...); returns 0
 // on success, -1 if the cooperative launch is not possible.
+// z-planes per block of the marching sweeps (cols = blocks per z-plane)
+int zper_for(int64_t cols, int nz);
 int launch_sweep_persistent(const SweepConfig& cfg, const KParams& p, double* a, double* b,
                             int64_t nsteps, cudaStream_t s);
 void launch_collide_inplace(bool glbm, bool slab, const KParams& p, double* buf,

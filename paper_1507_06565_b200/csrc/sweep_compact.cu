@@ -922,13 +922,8 @@ dim3 ccell_grid(const KParams& p) {
   return dim3((p.nx + bx - 1) / bx, p.ny, p.nz);
 }
 
-// z-planes per warp: long marching columns, but >= ~4 waves of blocks over
-// 148 SMs x 4 resident blocks.
 int cpipe_zper(const KParams& p) {
-  if (const char* e = std::getenv("PGPU_ZPER")) return std::max(1, std::min(atoi(e), p.nz));
-  const int64_t cols = (int64_t)((p.nchunk + kCW - 1) / kCW) * p.ny;
-  const int zper = (int)std::min<int64_t>(8, std::max<int64_t>(1, cols * p.nz / (148 * 4 * 4)));
-  return std::min(zper, p.nz);
+  return zper_for((int64_t)((p.nchunk + kCW - 1) / kCW) * p.ny, p.nz);
 }
 
 template <int CM, bool GLBM, bool RECORDS, bool SLAB, int OP>
@@ -1062,4 +1057,18 @@ void launch_fill_compact(const KParams& p, int64_t nfluid, double* f, const doub
   k_fill_compact<<<(unsigned)((nfluid + 255) / 256), 256, 0, s>>>(p, nfluid, f, feq);
 }
 
+// z-planes per block: long marching columns (the per-block prologue is paid
+// once per column), but >= ~6.5 waves of blocks over 148 SMs x 4 resident
+// blocks, so the last wave -- the launch's tail -- is a small part of it.
+// Measured on one B200 (per_config): C2 zper 2/3/4 = 0.757/0.744/0.729, C5
+// (dense) 2/4/6 = 0.843/0.852/0.834, C4 4/8 = 0.786/0.799 (capped at 8).
+int zper_for(int64_t cols, int nz) {
+  if (const char* e = std::getenv("PGPU_ZPER")) return std::max(1, std::min(atoi(e), nz));
+  static const int64_t waves2 = [] {  // twice the target wave count
+    const char* e = std::getenv("PGPU_ZWAVES2");
+    return (int64_t)(e ? std::max(1, atoi(e)) : 13);
+  }();
+  const int zper = (int)std::min<int64_t>(8, std::max<int64_t>(1, 2 * cols * nz / (148 * 4 * waves2)));
+  return std::min(zper, nz);
+}
 }  // namespace pgpu
