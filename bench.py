@@ -308,6 +308,7 @@ def run_ours(args):
         dist.barrier()
 
     device_bytes = sim.device_bytes
+    sweep_kernel = getattr(sim, "sweep_kernel", None)
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = sim.launch_count
@@ -399,6 +400,7 @@ def run_ours(args):
                                   else int(np.prod(w.dims)), links_total, w.scheme.name,
                                   world, w.meta, slab=world > 1 or args.force_slab),
             "math": args.math,
+            "sweep_kernel": sweep_kernel,
             "device_bytes_per_gpu": device_bytes,
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -494,7 +496,8 @@ def per_config_run(pg, configs, skip, device, peak):
         gbs = BYTES_PER_FLUID_CELL * geom.fluid_cells * steps / (ms * 1e-3) / 1e9
         out[key] = {"workload": w.name, "value": mlups, "unit": "MLUPS", "steps": steps,
                     "ms_per_step": ms / steps, "frac": gbs / peak,
-                    "layout": sim.layout, "fluid_cells": geom.fluid_cells}
+                    "layout": sim.layout, "sweep_kernel": sim.sweep_kernel,
+                    "fluid_cells": geom.fluid_cells}
         del sim
     return out
 

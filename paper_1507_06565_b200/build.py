@@ -30,7 +30,7 @@ CUDA_INC = "/usr/local/cuda/include"
 # The image's $CXX (/opt/gcc) lacks libgomp specs; the system g++ is used.
 CXX = shutil.which("g++") or "g++"
 
-CU_SOURCES = ["kernels.cu", "sweep_compact.cu", "sweep_tma.cu", "sweep_tb.cu", "voxelize_device.cu", "setup.cu"]
+CU_SOURCES = ["kernels.cu", "sweep_compact.cu", "sweep_tma.cu", "sweep_units.cu", "voxelize_device.cu", "setup.cu"]
 CPP_SOURCES = ["params.cpp", "voxelize.cpp", "synth.cpp", "sim.cpp", "io.cpp", "dist.cpp"]
 HEADERS = ["kparams.h", "kernels.h", "lattice.cuh", "host_common.h", "voxel_geometry.h", "setup.h", "staging.h",
            "sim_impl.h"]

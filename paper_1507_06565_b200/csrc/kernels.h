@@ -25,20 +25,17 @@ void launch_sweep(const SweepConfig& cfg, const KParams& p, const double* src, d
                   cudaStream_t s);
 void launch_sweep_compact(const SweepConfig& cfg, const KParams& p, const double* src,
                           double* dst, cudaStream_t s);
-// Two steps per launch (temporal blocking, sweep_tb.cu): step A into an
-// L2-resident ring of planes, step B from it; cooperative wavefront along z.
-struct TbState;
-TbState* tb_create(const KParams& p, cudaStream_t s);
-void tb_destroy(TbState* st);
-int64_t tb_device_bytes(const TbState* st);
-bool tb_supported(const SweepConfig& cfg, const KParams& p);
-bool launch_sweep_tb2(const SweepConfig& cfg, const KParams& p, TbState* st, const double* src,
-                      double* dst, cudaStream_t s);
 // K1 of the fluid-only layout as a warp-specialised TMA pipeline (sweep_tma.cu):
 // whole-domain stream+collide, no slab, no folded links, nx % 4 == 0.
 bool tma_sweep_supported(const SweepConfig& cfg, const KParams& p);
 bool launch_sweep_tma(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
                       cudaStream_t s);
+// K1 of the fluid-only layout by units of 32 consecutive fluid slots
+// (sweep_units.cu): whole-domain stream+collide, no slab, no folded links;
+// needs KParams::units / slotw (/ udesc with records).
+bool units_sweep_supported(const SweepConfig& cfg, const KParams& p);
+bool launch_sweep_units(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+                        cudaStream_t s);
 // K0 of the fluid-only layout: pre-collision f(n) -> post-collision g(n) in
 // place (with records in math mode fast + PGPU_FOLD: folded CLI slots).
 void launch_collide_compact(bool glbm, bool slab, bool records, const KParams& p, double* buf,

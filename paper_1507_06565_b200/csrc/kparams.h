@@ -33,6 +33,25 @@ struct alignas(8) ChunkEnt {
   uint32_t mask;
 };
 
+// Units sweep (sweep_units.cu): a unit is a run of <= 32 consecutive fluid
+// slots of one row whose cells lie in <= 3 consecutive chunks, so a warp that
+// sweeps a unit has no lane on a solid cell.  Units are numbered in slot order.
+//   yz   = y | z << 16
+//   info = n (bits 0..5) | holds x = 0 (bit 6) | holds x = nx-1 (bit 7)
+//          | first chunk c0 (bits 8..19) | link records (bits 20..31)
+struct alignas(16) UnitRec {
+  uint32_t s0;     // first fluid slot
+  uint32_t lbase;  // first link record (the unit's records are contiguous)
+  uint32_t yz;
+  uint32_t info;
+};
+// Per fluid slot (units sweep): the cell word's bits 0..18 | position relative
+// to the unit's first chunk, (chunk - c0) * 32 + (x & 31), in bits 19..25 |
+// x == 0 (bit 26) | x == nx-1 (bit 27).
+constexpr int kSlotRelShift = 19;
+constexpr uint32_t kSlotX0 = 1u << 26;
+constexpr uint32_t kSlotXN = 1u << 27;
+
 struct alignas(8) CellWord {
   uint32_t w;
   int32_t base;  // first link record of the cell
@@ -105,7 +124,12 @@ struct KParams {
   int32_t fast;
   int32_t fold;    // fast mode, fluid-only layout, records present: links folded
   int32_t moving;  // some link is a moving wall (records hold +inf for it)
-  int32_t sweep;   // fluid-only K1 kernel: pgpu_sweep_kernel (0 auto, 1 cpipe, 2 tma)
+  int32_t sweep;   // fluid-only K1 kernel: pgpu_sweep_kernel (0 auto, 1 cpipe, 2 tma, 3 units)
+  // units sweep (sweep_units.cu; built when it is selected)
+  const UnitRec* units;
+  const uint32_t* slotw;   // per fluid slot
+  const uint16_t* udesc;   // per link record: owner lane in its unit | j << 5
+  int64_t nunits;
   uint32_t* tickets;  // TMA sweep: [0] next work item, [1] finished blocks (zero between launches)
   int32_t stream_stores;  // sweeps store the new state evict-first (domains far larger than L2)
   FastCoef fc;

@@ -262,6 +262,67 @@ __global__ void k_linkdesc(const uint32_t* __restrict__ cellw, const int32_t* __
   }
 }
 
+// Units of one row per thread (greedy: up to 32 fluid cells from at most 3
+// consecutive chunks).  FILL = false counts them; FILL = true writes the unit
+// records, the per-slot words and the per-record descriptors.
+template <bool FILL>
+__global__ void k_units(const ChunkEnt* __restrict__ ctab, const uint32_t* __restrict__ cellw,
+                        const int32_t* __restrict__ cellbase, int nx, int ny, int64_t rows,
+                        int nchunk, const int32_t* __restrict__ ubase, int32_t* __restrict__ cnt,
+                        UnitRec* __restrict__ units, uint32_t* __restrict__ slotw,
+                        uint16_t* __restrict__ udesc) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const uint32_t y = (uint32_t)(row % ny), z = (uint32_t)(row / ny);
+  const int64_t u0 = FILL ? ubase[row] : 0;
+  int nu = 0, n = 0, c0 = 0, nl = 0;
+  uint32_t s0 = 0, lbase = 0, wrap = 0;
+  auto close = [&] {
+    if (FILL)
+      units[u0 + nu] = UnitRec{s0, lbase, y | z << 16,
+                               (uint32_t)n | wrap << 6 | (uint32_t)c0 << 8 | (uint32_t)nl << 20};
+    ++nu;
+    n = 0;
+  };
+  for (int c = 0; c < nchunk; ++c) {
+    const ChunkEnt e = ctab[row * nchunk + c];
+    uint32_t m = e.mask, slot = e.rank;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      if (n && (n == 32 || c - c0 >= 3)) close();
+      const int x = c * 32 + b;
+      const int64_t cell = row * nx + x;
+      if (!n) {
+        c0 = c;
+        s0 = slot;
+        nl = 0;
+        wrap = 0;
+        if (FILL) lbase = (uint32_t)cellbase[cell];
+      }
+      if (FILL) {
+        const uint32_t w = cellw[cell];
+        const uint32_t fx = (x == 0 ? kSlotX0 : 0u) | (x == nx - 1 ? kSlotXN : 0u);
+        slotw[slot] = (w & 0x7FFFFu) | (uint32_t)((c - c0) * 32 + b) << kSlotRelShift | fx;
+        wrap |= (x == 0 ? 1u : 0u) | (x == nx - 1 ? 2u : 0u);
+        uint32_t mm = w & kBounceMask;
+        int32_t r = cellbase[cell];
+        while (mm) {
+          const int j = __ffs(mm) - 1;
+          mm &= mm - 1;
+          if (udesc) udesc[r] = (uint16_t)(n | (j << 5));
+          ++r;
+          ++nl;
+        }
+      }
+      ++n;
+      ++slot;
+    }
+  }
+  if (n) close();
+  if (!FILL) cnt[row] = nu;
+}
+
 __global__ void k_unpack_flags(const uint32_t* __restrict__ cellw, uint8_t* __restrict__ out,
                                int64_t cells) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -365,6 +426,39 @@ int64_t build_ctab(const uint32_t* cellw, int nx, int64_t rows, int nchunk, Chun
   cudaFree(rank);
   cudaFree(tmp);
   return (int64_t)last[0] + last[1];
+}
+
+int64_t build_units(const ChunkEnt* ctab, const uint32_t* cellw, const int32_t* cellbase, int nx,
+                    int ny, int64_t rows, int nchunk, UnitRec** units_out, uint32_t* slotw,
+                    uint16_t* udesc, cudaStream_t s) {
+  int32_t *cnt = nullptr, *ubase = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  ck(cudaMalloc(&cnt, sizeof(int32_t) * rows), "units alloc");
+  ck(cudaMalloc(&ubase, sizeof(int32_t) * rows), "units alloc");
+  k_units<false><<<blocks(rows, 128), 128, 0, s>>>(ctab, cellw, cellbase, nx, ny, rows, nchunk,
+                                                    nullptr, cnt, nullptr, nullptr, nullptr);
+  ck(cudaGetLastError(), "k_units count");
+  ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, ubase, rows, s), "units scan size");
+  ck(cudaMalloc(&tmp, tb), "units alloc");
+  ck(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, ubase, rows, s), "units scan");
+  int32_t last[2] = {0, 0};
+  ck(cudaMemcpyAsync(&last[0], ubase + rows - 1, 4, cudaMemcpyDeviceToHost, s), "units total");
+  ck(cudaMemcpyAsync(&last[1], cnt + rows - 1, 4, cudaMemcpyDeviceToHost, s), "units total");
+  ck(cudaStreamSynchronize(s), "units sync");
+  const int64_t nunits = (int64_t)last[0] + last[1];
+  UnitRec* units = nullptr;
+  ck(cudaMalloc(&units, sizeof(UnitRec) * (nunits + 4)), "units alloc");
+  ck(cudaMemsetAsync(units, 0, sizeof(UnitRec) * (nunits + 4), s), "units clear");
+  k_units<true><<<blocks(rows, 128), 128, 0, s>>>(ctab, cellw, cellbase, nx, ny, rows, nchunk,
+                                                   ubase, nullptr, units, slotw, udesc);
+  ck(cudaGetLastError(), "k_units fill");
+  ck(cudaStreamSynchronize(s), "units sync");
+  cudaFree(cnt);
+  cudaFree(ubase);
+  cudaFree(tmp);
+  *units_out = units;
+  return nunits;
 }
 
 void build_linkdesc(const uint32_t* cellw, const int32_t* cellbase, int nx, int64_t cells,

@@ -65,6 +65,12 @@ int64_t build_ctab(const uint32_t* cellw, int nx, int64_t rows, int nchunk, Chun
 // Per link record (x & 31) | j << 5 in record order (compact CLI sweep).
 void build_linkdesc(const uint32_t* cellw, const int32_t* cellbase, int nx, int64_t cells,
                     uint16_t* desc, cudaStream_t s);
+// Units of the units sweep (kparams.h UnitRec) with their per-slot words and
+// per-record descriptors (udesc may be null: no links); *units_out is
+// cudaMalloc'ed here (+ 4 zero records).  Returns the unit count.
+int64_t build_units(const ChunkEnt* ctab, const uint32_t* cellw, const int32_t* cellbase, int nx,
+                    int ny, int64_t rows, int nchunk, UnitRec** units_out, uint32_t* slotw,
+                    uint16_t* udesc, cudaStream_t s);
 void unpack_flags(const uint32_t* cellw, uint8_t* out, int64_t cells, cudaStream_t s);
 
 }  // namespace pgpu

@@ -378,8 +378,9 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
       s->zrev_on = !(z && z[0] == '0');
     }
     if (const char* e = std::getenv("PGPU_SWEEP"))
-      kp.sweep = (e[0] == 't' && e[1] == 'b') ? PGPU_SWEEP_TB2
+      kp.sweep = e[0] == 'u' ? PGPU_SWEEP_UNITS
                  : e[0] == 't' ? PGPU_SWEEP_TMA : (e[0] == 'c' ? PGPU_SWEEP_CPIPE : PGPU_SWEEP_AUTO);
+    if (kp.sweep == PGPU_SWEEP_UNITS) s->ensure_units();
     lap("alloc pdfs");
     s->refresh_params();
     CK(cudaStreamSynchronize(s->stream));
@@ -451,11 +452,12 @@ int pgpu_set_sweep_kernel(pgpu_sim* sim, int32_t kind) {
   return guard([&] {
     SIM_CHECK();
     if (kind != PGPU_SWEEP_AUTO && kind != PGPU_SWEEP_CPIPE && kind != PGPU_SWEEP_TMA &&
-        kind != PGPU_SWEEP_TB2)
+        kind != PGPU_SWEEP_UNITS)
       throw ConfigError("unknown sweep kernel");
     if (kind == sim->kp.sweep) return;
     sim->sync();
     sim->kp.sweep = kind;
+    if (kind == PGPU_SWEEP_UNITS) sim->ensure_units();
     sim->drop_graphs();  // graphs hold the kernel parameters by value
   });
 }

@@ -104,8 +104,11 @@ struct pgpu_sim {
   int* d_flags = nullptr;  // [0] err, [1] nonfinite
   unsigned long long* d_vmax = nullptr;
   double* d_sums = nullptr;
+  UnitRec* d_units = nullptr;     // units sweep (built when it is selected)
+  uint32_t* d_slotw = nullptr;
+  uint16_t* d_udesc = nullptr;
+  int64_t n_units = 0;
   uint32_t* d_tickets = nullptr;  // TMA sweep work counter (KParams::tickets)
-  TbState* tb = nullptr;          // two-step sweep buffers (ring, row tables, counters)
   // state
   int cur = 0;
   bool post = false;
@@ -146,8 +149,10 @@ struct pgpu_sim {
     cudaFree(d_flags);
     cudaFree(d_vmax);
     cudaFree(d_sums);
+    cudaFree(d_units);
+    cudaFree(d_slotw);
+    cudaFree(d_udesc);
     cudaFree(d_tickets);
-    tb_destroy(tb);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 
@@ -303,12 +308,29 @@ struct pgpu_sim {
     kp.linkdesc = d_linkdesc;
   }
 
+  // static data of the units sweep (fluid-only layout): unit records, per-slot
+  // words, per-record descriptors
+  void ensure_units() {
+    if (d_units || !compact || !d_ctab) return;
+    CK(cudaMalloc(&d_slotw, sizeof(uint32_t) * (kp.ks + 32)));
+    if (n_links > 0) {
+      CK(cudaMalloc(&d_udesc, sizeof(uint16_t) * (n_links + 16)));
+      CK(cudaMemsetAsync(d_udesc, 0, sizeof(uint16_t) * (n_links + 16), stream));
+    }
+    n_units = build_units(d_ctab, d_cellw, d_cellbase, nx, ny, (int64_t)ny * nz, kp.nchunk, &d_units,
+                          d_slotw, d_udesc, stream);
+    kp.units = d_units;
+    kp.slotw = d_slotw;
+    kp.udesc = d_udesc;
+    kp.nunits = n_units;
+  }
+
   // the K1 kernel the whole-domain step runs (pgpu_sweep_kernel; AUTO for the
   // dense layout, which has one)
   int resolved_sweep() const {
     if (!compact) return PGPU_SWEEP_AUTO;
     if (kp.sweep == PGPU_SWEEP_TMA && tma_sweep_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_TMA;
-    if (kp.sweep == PGPU_SWEEP_TB2 && tb_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_TB2;
+    if (kp.sweep == PGPU_SWEEP_UNITS && units_sweep_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_UNITS;
     return PGPU_SWEEP_CPIPE;
   }
 
@@ -342,9 +364,10 @@ struct pgpu_sim {
     if (d_recs) b += (n_links + 2) * (int64_t)sizeof(LinkRec);
     if (d_recs_fold) b += n_links * (int64_t)sizeof(LinkRec);
     if (d_linkdesc) b += (n_links + 16) * (int64_t)sizeof(uint16_t);
+    if (d_units) b += (n_units + 4) * (int64_t)sizeof(UnitRec) + (kp.ks + 32) * (int64_t)sizeof(uint32_t);
+    if (d_udesc) b += (n_links + 16) * (int64_t)sizeof(uint16_t);
     if (d_planes) b += nz * (int64_t)sizeof(PlaneCoef);
     if (d_scratch) b += scratch_n * (int64_t)sizeof(double);
-    b += tb_device_bytes(tb);
     b += (19 + 2 + 1 + nz) * 8;  // feq, flags, vmax, plane sums
     return b;
   }
@@ -463,23 +486,6 @@ struct pgpu_sim {
         }
         cudaGetLastError();
         persistent = false;  // not launchable here: fall back to graphs
-      }
-      if (n - i >= 2 && kp.sweep == PGPU_SWEEP_TB2 && compact) {
-        // two steps per launch (temporal blocking), one launch per pair
-        const SweepConfig c = sweep_cfg(0, 0);
-        if (tb_supported(c, kp)) {
-          if (!tb) tb = tb_create(kp, stream);
-          Nvtx r("K1x2 two-step sweep");
-          set_ghost_ptrs();
-          if (tb && launch_sweep_tb2(c, kp, tb, f[cur], f[1 - cur], stream)) {
-            check_launch();
-            launches += 2;  // the counter reset and the sweep
-            cur = 1 - cur;
-            steps += 2;
-            i += 2;
-            continue;
-          }
-        }
       }
       if (n - i >= kGraphSteps) {
         if (graph_stream != stream) drop_graphs();

@@ -1,0 +1,461 @@
+// K1 over the fluid-only layout by units of fluid slots (sm_100a).
+//
+// Same step as sweep_compact.cu's k_sweep_cpipe -- g' = C(P(g)), P the pull
+// form of the reference's push streaming + link bounce-back
+// (simulation.cpp:278-342, boundary.cpp:19-41), C the TRT / GLBM collision
+// (simulation.cpp:150-274) -- with the lanes mapped to FLUID SLOTS instead of
+// x positions.  k_sweep_cpipe gives every lane one cell of a 32-cell chunk, so
+// inside a sphere packing (porosity 0.5) half of each warp's lanes sit on
+// solid cells while the warp still issues every instruction: per fluid cell
+// the bed costs twice the instructions of the free flow, and ncu shows the
+// sweep issue-bound there.  Here a warp sweeps a *unit*: a run of up to 32
+// consecutive fluid slots of one row (kparams.h UnitRec, built once by
+// setup.cu's k_units; the cells of a unit lie in at most 3 consecutive
+// chunks).  Every lane of a full unit updates a fluid cell, its 19 stores are
+// one contiguous 256-byte run per direction, and the instruction count per
+// fluid cell no longer depends on the porosity.
+//
+// Addresses: a lane's cell sits at bit b of chunk c0 + k of its row (the
+// per-slot word holds k and b); with the chunk entry {rank, mask} of source
+// row r at chunk c0 + k,  q_r = rank + popc(mask & ((1 << b) - 1))  is the slot
+// of the fluid cell at or after this x in that row, and the pull source is
+// q_r (e_x = 0), q_r - 1 (e_x = +1) or q_r + bit(mask, b) (e_x = -1), exactly
+// as in k_sweep_cpipe.  The 27 chunk entries of a unit (9 source rows x 3
+// chunks) and the 5 + 5 x-wrap partners are loaded by one lane each.
+//
+// Schedule: units are numbered in slot order (z, y, x); warp w of the grid
+// sweeps the units [w * upw, (w + 1) * upw) one after the other with a
+// four-level per-warp pipeline of 8-byte / 4-byte cp.async copies -- while
+// unit i is collided and stored, the populations (and link records, g_j(x))
+// of unit i+1, the slot words / chunk entries / link descriptors of unit i+2
+// and the unit record of i+3 are in flight.  Warps never synchronise with
+// each other.
+//
+// The arithmetic per cell is the sweep_compact.cu one (collide<CM, GLBM>, the
+// link closures in the reference order), so the results are bit-identical to
+// k_sweep_cpipe in EXACT and FAST (tests/test_gpu_units.py).  Whole-domain
+// stream+collide only; slab parts, KP and folded links stay on k_sweep_cpipe
+// (same state layout, so the kernels mix freely).
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstddef>
+#include <cstdint>
+#include <cstdlib>
+
+#include "kernels.h"
+#include "kparams.h"
+#include "lattice.cuh"
+
+namespace pgpu {
+namespace {
+
+#ifndef PGPU_UNITS_LCAP
+#define PGPU_UNITS_LCAP 128
+#endif
+#ifndef PGPU_UNITS_MINB
+#define PGPU_UNITS_MINB 4
+#endif
+#ifndef PGPU_BOUNDS
+#define PGPU_BOUNDS 0
+#endif
+#ifndef PGPU_STCS
+#define PGPU_STCS 1
+#endif
+constexpr int kUW = 4;                   // warps per block (independent)
+constexpr int kULCap = PGPU_UNITS_LCAP;  // links per unit closed cooperatively from the pool
+
+__device__ __forceinline__ uint32_t usmem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void ucpa16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(usmem(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void ucpa8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(usmem(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void ucpa4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(usmem(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void ucommit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void uwait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void updl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void updl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void ubounds(bool ok) {
+  if (PGPU_BOUNDS && !ok) __trap();
+}
+
+// Source rows exactly as in sweep_compact.cu: row r holds the directions with
+// (e_y, e_z) = (urow_ey(r), urow_ez(r)).
+//   r0 (0,0): 0 1 2   r1 (1,0): 3 7 10   r2 (-1,0): 4 8 9   r3 (0,1): 5 11 14
+//   r4 (0,-1): 6 12 13   r5 (1,1): 15   r6 (-1,-1): 16   r7 (1,-1): 17   r8 (-1,1): 18
+__host__ __device__ constexpr int urow_ey(int r) {
+  return (r == 1 || r == 5 || r == 7) ? 1 : ((r == 2 || r == 6 || r == 8) ? -1 : 0);
+}
+__host__ __device__ constexpr int urow_ez(int r) {
+  return (r == 3 || r == 5 || r == 8) ? 1 : ((r == 4 || r == 6 || r == 7) ? -1 : 0);
+}
+__host__ __device__ constexpr int urow_of(int j) {
+  return j <= 2 ? 0
+         : (j == 3 || j == 7 || j == 10) ? 1
+         : (j == 4 || j == 8 || j == 9)  ? 2
+         : (j == 5 || j == 11 || j == 14) ? 3
+         : (j == 6 || j == 12 || j == 13) ? 4
+                                          : j - 10;
+}
+constexpr uint32_t upack(int v0, int v1, int v2, int v3, int v4, int v5, int v6, int v7, int v8) {
+  return (uint32_t)(v0 + 1) | (uint32_t)(v1 + 1) << 2 | (uint32_t)(v2 + 1) << 4 |
+         (uint32_t)(v3 + 1) << 6 | (uint32_t)(v4 + 1) << 8 | (uint32_t)(v5 + 1) << 10 |
+         (uint32_t)(v6 + 1) << 12 | (uint32_t)(v7 + 1) << 14 | (uint32_t)(v8 + 1) << 16;
+}
+constexpr uint32_t kURowEY = upack(urow_ey(0), urow_ey(1), urow_ey(2), urow_ey(3), urow_ey(4),
+                                   urow_ey(5), urow_ey(6), urow_ey(7), urow_ey(8));
+constexpr uint32_t kURowEZ = upack(urow_ez(0), urow_ez(1), urow_ez(2), urow_ez(3), urow_ez(4),
+                                   urow_ez(5), urow_ez(6), urow_ez(7), urow_ez(8));
+__device__ __forceinline__ int urt_ey(int r) { return (int)((kURowEY >> (2 * r)) & 3u) - 1; }
+__device__ __forceinline__ int urt_ez(int r) { return (int)((kURowEZ >> (2 * r)) & 3u) - 1; }
+
+__device__ __forceinline__ bool uwrap(int& v, int n, int periodic) {
+  if (v >= 0 && v < n) return true;
+  if (!periodic) return false;
+  v = v < 0 ? v + n : v - n;
+  return true;
+}
+
+__device__ __forceinline__ int uscan_excl(int n, int lane, int* total) {
+  int v = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  *total = __shfl_sync(0xffffffffu, v, 31);
+  return v - n;
+}
+
+// Chunk entries of a unit: ent[3 * r + k] = source row r, chunk c0 + k;
+// ent[27 + r] = chunk nchunk-1 of source row r (the x = 0 cell's pulls with
+// e_x = +1, rows 0..4); ent[32 + r] = chunk 0 of source row r (x = nx-1).
+template <bool RECORDS>
+struct alignas(16) UMeta {
+  uint32_t sw[32];
+  ChunkEnt ent[40];
+  uint16_t ldesc[RECORDS ? kULCap + 8 : 8];
+};
+template <bool RECORDS>
+struct alignas(16) UWarp {
+  double stage[19][32];
+  double pool[RECORDS ? 2 * kULCap : 2];  // per link: record, g_j(x)
+  UMeta<RECORDS> meta[3];
+  UnitRec rec[4];
+};
+
+// Closure of one link in the stage (boundary.cpp:24-41 in pull form): slot j
+// of the owner holds g_k(x), slot k its pull value.
+__device__ __forceinline__ void uclose_link(double* stage, int owner, int j, double rec, double gj,
+                                            const KParams& p) {
+  if (rec == rec) {
+    const int k = (j & 1) ? j + 1 : j - 1;
+    double* sj = stage + j * 32 + owner;
+    const double gk = *sj;
+    if (!isinf(rec))
+      *sj = DADD(DSUB(DMUL(rec, stage[k * 32 + owner]), DMUL(rec, gj)), gk);
+    else
+      *sj = DSUB(gk, p.mw[k]);
+  }  // NaN: simple bounce-back, slot j already holds g_k(x)
+}
+
+template <int CM, bool GLBM, bool RECORDS>
+__global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
+    k_sweep_units(const KParams p, const double* __restrict__ src, double* __restrict__ dst, int upw,
+                  int rev) {
+  extern __shared__ __align__(16) unsigned char usmem_raw[];
+  updl_trigger();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  UWarp<RECORDS>& S = reinterpret_cast<UWarp<RECORDS>*>(usmem_raw)[warp];
+  const int64_t blk = rev ? (int64_t)gridDim.x - 1 - blockIdx.x : (int64_t)blockIdx.x;
+  const int64_t ub = (blk * kUW + warp) * upw;
+  if (ub >= p.nunits) return;  // whole warp; warps never synchronise with each other
+  const int nu = (int)min((int64_t)upw, p.nunits - ub);
+  const UnitRec* const U = p.units + ub;
+  // the chunk entry this lane loads for every unit: lanes 0..26 source row
+  // lane / 3, chunk c0 + lane % 3; lanes 27..31 the x = nx-1 partner of rows 0..4
+  const int er = lane < 27 ? lane / 3 : lane - 27;
+  const int ek = lane < 27 ? lane - 3 * er : 0;
+  const int eey = urt_ey(er), eez = urt_ez(er);
+  const uint32_t xn_below = (1u << ((p.nx - 1) & 31)) - 1u;
+
+  auto rec_load = [&](int i) {
+    if (lane == 0) ucpa16(&S.rec[i & 3], U + i);
+  };
+
+  // slot words, chunk entries and link descriptors of unit i (its record has landed)
+  auto meta_load = [&](int i) {
+    const UnitRec R = S.rec[i & 3];
+    UMeta<RECORDS>& M = S.meta[i % 3];
+    const int n = R.info & 63, c0 = (R.info >> 8) & 0xFFF;
+    const int y = R.yz & 0xFFFF, z = R.yz >> 16;
+    if (lane < n) {
+      ubounds((int64_t)R.s0 + lane < p.ks);
+      ucpa4(&M.sw[lane], p.slotw + R.s0 + lane);
+    }
+    {
+      int ys = y - eey, zs = z - eez;
+      const bool oky = uwrap(ys, p.ny, p.py), okz = uwrap(zs, p.nz, p.pz);
+      const ChunkEnt* row = p.ctab + ((int64_t)zs * p.ny + ys) * p.nchunk;
+      bool ok = oky && okz;
+      int c;
+      if (lane < 27) {
+        c = c0 + ek;
+        ok = ok && c < p.nchunk;
+      } else {
+        c = p.nchunk - 1;
+        ok = ok && (R.info & 64u);
+      }
+      if (ok)
+        ucpa8(&M.ent[lane], row + c);
+      else
+        M.ent[lane] = ChunkEnt{0u, 0u};
+    }
+    if ((R.info & 128u) && lane < 5) {  // warp-uniform: the unit holds x = nx-1 (pulls from x = 0)
+      int ys = y - urt_ey(lane), zs = z - urt_ez(lane);
+      const bool oky = uwrap(ys, p.ny, p.py), okz = uwrap(zs, p.nz, p.pz);
+      if (oky && okz)
+        ucpa8(&M.ent[32 + lane], p.ctab + ((int64_t)zs * p.ny + ys) * p.nchunk);
+      else
+        M.ent[32 + lane] = ChunkEnt{0u, 0u};
+    }
+    if (RECORDS) {
+      const int nl = min((int)(R.info >> 20), kULCap);
+      if (nl) {  // 4-byte pairs from the even record at or below the unit's first
+        const uint32_t a0 = R.lbase & ~1u;
+        const int npairs = (int)(R.lbase + nl - a0 + 1) >> 1;
+        for (int t = lane; t < npairs; t += 32) ucpa4(&M.ldesc[2 * t], p.udesc + a0 + 2 * t);
+      }
+    }
+  };
+
+  // populations and link extras of unit i into the stage / pool (its meta has landed)
+  auto issue = [&](int i) {
+    const UnitRec R = S.rec[i & 3];
+    const UMeta<RECORDS>& M = S.meta[i % 3];
+    const int n = R.info & 63;
+    if (lane < n) {
+      const uint32_t sw = M.sw[lane];
+      const int rel = (sw >> kSlotRelShift) & 127;
+      const int b = rel & 31;
+      const uint32_t below = (1u << b) - 1u;
+      const ChunkEnt* E = M.ent + (rel >> 5);
+      int q[9];
+      uint32_t bits = 0;  // bit r: source row r has a fluid cell at this x (rows 0..4)
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        const ChunkEnt e = E[3 * r];
+        q[r] = (int)e.rank + __popc(e.mask & below);
+        if (r < 5) bits |= ((e.mask >> b) & 1u) << r;
+      }
+      const uint32_t fc = R.s0 + lane;
+      ubounds((uint32_t)q[0] == fc);
+      double* const st = &S.stage[0][lane];
+      if (!(sw & (kSlotX0 | kSlotXN))) {
+#pragma unroll
+        for (int j = 0; j < 19; ++j) {
+          uint32_t idx;  // unsigned: 19 * ks may exceed 2^31
+          if (j == 0) {
+            idx = fc;
+          } else if ((sw >> j) & 1u) {
+            idx = fc + p.poff[opp(j)];  // bounce: g_k(x)
+          } else {
+            const int r = urow_of(j);
+            idx = q[r] + p.poff[j];
+            if (EX[j] == 1) idx -= 1;
+            if (EX[j] == -1) idx += (bits >> r) & 1u;
+          }
+          ubounds(idx < 19ull * p.ks);
+          ucpa8(st + j * 32, src + idx);
+        }
+      } else {  // cell on an x face: periodic partner chunk
+#pragma unroll
+        for (int j = 0; j < 19; ++j) {
+          uint32_t idx;
+          if (j == 0) {
+            idx = fc;
+          } else if ((sw >> j) & 1u) {
+            idx = fc + p.poff[opp(j)];
+          } else if (EX[j] == 1 && (sw & kSlotX0)) {
+            const ChunkEnt e = M.ent[27 + urow_of(j)];
+            idx = e.rank + __popc(e.mask & xn_below) + p.poff[j];
+          } else if (EX[j] == -1 && (sw & kSlotXN)) {
+            idx = M.ent[32 + urow_of(j)].rank + p.poff[j];
+          } else {
+            const int r = urow_of(j);
+            idx = q[r] + p.poff[j];
+            if (EX[j] == 1) idx -= 1;
+            if (EX[j] == -1) idx += (bits >> r) & 1u;
+          }
+          ubounds(idx < 19ull * p.ks);
+          ucpa8(st + j * 32, src + idx);
+        }
+      }
+    }
+    if (RECORDS) {
+      const int nl = min((int)(R.info >> 20), kULCap);
+      if (nl) {
+        const uint16_t* ld = M.ldesc + (R.lbase & 1u);
+        for (int e = lane; e < nl; e += 32) {
+          const int d = ld[e];
+          ubounds((int64_t)R.lbase + e < p.nrec);
+          ucpa8(S.pool + 2 * e, p.links + R.lbase + e);
+          ucpa8(S.pool + 2 * e + 1, src + (uint32_t)(R.s0 + (d & 31) + p.poff[d >> 5]));
+        }
+      }
+    }
+  };
+
+  // prologue: three dependent levels of static data, then the first populations
+  rec_load(0);
+  if (nu > 1) rec_load(1);
+  if (nu > 2) rec_load(2);
+  ucommit();
+  uwait_all();
+  __syncwarp();
+  meta_load(0);
+  if (nu > 1) meta_load(1);
+  ucommit();
+  uwait_all();
+  __syncwarp();
+  updl_wait();  // everything above is static; populations come from the previous sweep
+  issue(0);
+  ucommit();
+
+  for (int i = 0; i < nu; ++i) {
+    uwait_all();
+    __syncwarp();
+    const UnitRec R = S.rec[i & 3];
+    const UMeta<RECORDS>& M = S.meta[i % 3];
+    const int n = R.info & 63;
+    const bool fluid = lane < n;
+    const uint32_t sw = fluid ? M.sw[lane] : 0u;
+    const uint32_t fc = R.s0 + lane;
+    if (RECORDS) {
+      const int nl = (int)(R.info >> 20);
+      if (nl) {  // warp-uniform
+        double* const stage = &S.stage[0][0];
+        const int ncoop = min(nl, kULCap);
+        const uint16_t* ld = M.ldesc + (R.lbase & 1u);
+        for (int e = lane; e < ncoop; e += 32) {
+          const int d = ld[e];
+          uclose_link(stage, d & 31, d >> 5, S.pool[2 * e], S.pool[2 * e + 1], p);
+        }
+        if (nl > kULCap) {  // pool overflow: each lane closes the rest of its own links
+          int tot;
+          const int off = uscan_excl(__popc(sw & kBounceMask), lane, &tot);
+          uint32_t mm = sw & kBounceMask;
+          int k = 0;
+          while (mm) {
+            const int j = __ffs(mm) - 1;
+            mm &= mm - 1;
+            if (off + k >= kULCap)
+              uclose_link(stage, lane, j, __ldg(p.links + R.lbase + off + k),
+                          __ldg(src + (uint32_t)(fc + p.poff[j])), p);
+            ++k;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    double f[19];
+    if (fluid) {
+#pragma unroll
+      for (int j = 0; j < 19; ++j) f[j] = S.stage[j][lane];
+    }
+    __syncwarp();  // stage and pool consumed: refill them with unit i+1
+    if (i + 1 < nu) issue(i + 1);
+    if (i + 2 < nu) meta_load(i + 2);
+    if (i + 3 < nu) rec_load(i + 3);
+    ucommit();
+    if (fluid) {
+      collide<CM, GLBM>(f, p, (int)(R.yz >> 16));
+#pragma unroll
+      for (int j = 0; j < 19; ++j) {
+        if (PGPU_STCS && p.stream_stores)
+          __stcs(dst + (uint32_t)(fc + p.poff[j]), f[j]);
+        else
+          dst[(uint32_t)(fc + p.poff[j])] = f[j];
+      }
+    }
+  }
+  uwait_all();
+}
+
+int units_upw(const KParams& p) {
+  const char* e = std::getenv("PGPU_UPW");  // experiments and tests (read per launch / graph capture)
+  const int env = e ? std::atoi(e) : 0;
+  if (env > 0) return env;
+  // one wave of warps (148 SMs x 16) when that leaves each a short run, else
+  // runs of 16 units (many waves: the tail is a few runs)
+  const int64_t slots = 148 * 4 * PGPU_UNITS_MINB;
+  const int64_t one = (p.nunits + slots - 1) / slots;
+  return (int)(one <= 24 ? std::max<int64_t>(one, 1) : 16);
+}
+
+template <int CM, bool GLBM, bool RECORDS>
+bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+                  cudaStream_t s) {
+  constexpr int smem = (int)sizeof(UWarp<RECORDS>) * kUW;
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_sweep_units<CM, GLBM, RECORDS>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)attr;
+  static const bool pdl_env = [] {
+    const char* e = std::getenv("PGPU_PDL");
+    return !(e && e[0] == '0');
+  }();
+  const int upw = units_upw(p);
+  const int64_t nwarps = (p.nunits + upw - 1) / upw;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)((nwarps + kUW - 1) / kUW));
+  lc.blockDim = dim3(kUW * 32);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl_env ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, k_sweep_units<CM, GLBM, RECORDS>, p, src, dst, upw,
+                            cfg.zrev ? 1 : 0) == cudaSuccess;
+}
+
+template <int CM>
+bool units_cm(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+              cudaStream_t s) {
+  if (cfg.glbm)
+    return cfg.records ? units_launch<CM, true, true>(cfg, p, src, dst, s)
+                       : units_launch<CM, true, false>(cfg, p, src, dst, s);
+  return cfg.records ? units_launch<CM, false, true>(cfg, p, src, dst, s)
+                     : units_launch<CM, false, false>(cfg, p, src, dst, s);
+}
+
+}  // namespace
+
+bool units_sweep_supported(const SweepConfig& cfg, const KParams& p) {
+  return p.ctab && p.units && p.slotw && p.nunits > 0 && !cfg.slab && cfg.part == PART_ALL &&
+         cfg.op == OP_STREAM_COLLIDE && collide_mode(p) != CM_FAST_FOLD &&
+         (p.udesc || !cfg.records) && p.nchunk <= 4096 && p.ny <= 65535 && p.nz <= 65535;
+}
+
+bool launch_sweep_units(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+                        cudaStream_t s) {
+  switch (collide_mode(p)) {
+    case CM_FAST: return units_cm<CM_FAST>(cfg, p, src, dst, s);
+    case CM_EXACT_RHO1: return units_cm<CM_EXACT_RHO1>(cfg, p, src, dst, s);
+    case CM_EXACT: return units_cm<CM_EXACT>(cfg, p, src, dst, s);
+    default: return false;
+  }
+}
+
+}  // namespace pgpu

@@ -74,7 +74,7 @@ class MathMode(enum.IntEnum):
 
 
 # pgpu_sweep_kernel (include/porolb_gpu.h), by value
-SWEEP_KERNELS = ("auto", "cpipe", "tma", "tb2")
+SWEEP_KERNELS = ("auto", "cpipe", "tma", "units")
 
 
 class GlbmViscosity(enum.IntEnum):
@@ -568,7 +568,7 @@ class Simulation:
 
     @property
     def sweep_kernel(self) -> str:
-        """Fluid-only K1 kernel: "auto", "cpipe" or "tma" (pgpu_get_sweep_kernel)."""
+        """Fluid-only K1 kernel: "auto", "cpipe", "tma" or "units" (pgpu_get_sweep_kernel)."""
         m = C.c_int32()
         _check(lib.pgpu_get_sweep_kernel(self._h, C.byref(m)))
         return SWEEP_KERNELS[m.value]

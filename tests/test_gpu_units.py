@@ -1,10 +1,12 @@
-"""The two-step sweep (temporal blocking, sweep_tb.cu, pgpu_sweep_kernel TB2)
-bit for bit: against the oracle in math mode EXACT (reference arithmetic) and
-against the one-step sweep (k_sweep_cpipe) in math mode FAST, on the corner
-cases of its schedule -- y-bands with halo rows (periodic y wraps the halo),
-row segments of 128 cells that are partial (nx = 160, 36, 20), x-periodic
-faces, odd step counts (the last step is a one-step sweep), walls, CLI beds, a
-moving lid (+inf records) and the GLBM collision."""
+"""The units sweep (sweep_units.cu, pgpu_sweep_kernel UNITS: warps sweep runs of
+up to 32 consecutive fluid slots instead of 32-cell chunks) bit for bit:
+against the oracle in math mode EXACT (reference arithmetic) and against the
+chunk sweep (k_sweep_cpipe) in math mode FAST, on the corner cases of its
+addressing -- rows whose last chunk is partial (nx = 160, 36, 20), units that
+hold both x faces, x-periodic wrap pulls, a fully periodic box, wall planes
+whose units overflow the link pool (5 links per cell), CLI beds (units spanning
+three chunks), a moving lid (+inf records), the GLBM collision, and several
+units-per-warp settings (pipeline lengths 1, 2, 3 and longer)."""
 import numpy as np
 import pytest
 
@@ -29,7 +31,8 @@ CASES = {
     "nx160_partial_segment": ((160, 20, 24), 14, 2.0, 5.0, (True, True, False), True),
     "nx36_short_row": ((36, 18, 22), 6, 2.0, 4.0, (True, True, False), True),
     "nx20_one_chunk": ((20, 18, 22), 6, 2.0, 4.0, (True, True, False), True),
-        "bed_128": ((128, 32, 40), 40, 3.0, 6.0, (True, True, False), True),
+    "fully_periodic": ((64, 24, 28), 14, 2.0, 5.0, (True, True, True), False),
+    "bed_128": ((128, 32, 40), 40, 3.0, 6.0, (True, True, False), True),
 }
 
 
@@ -48,28 +51,28 @@ def _random_state(geom, seed):
     return f0, m
 
 
-def _tma_sim(pg, monkeypatch, geom, p, scheme):
+def _units_sim(pg, monkeypatch, geom, p, scheme):
     monkeypatch.setenv("PGPU_LAYOUT", "compact")
-    monkeypatch.setenv("PGPU_SWEEP", "tb2")
+    monkeypatch.setenv("PGPU_SWEEP", "units")
     sim = pg.Simulation.from_params(geom, p, pg.WallScheme(scheme))
     assert sim.layout == "fluid-only"
-    assert sim.sweep_kernel == "tb2", "the two-step sweep does not run for this simulation"
+    assert sim.sweep_kernel == "units", "the units sweep does not run for this simulation"
     return sim
 
 
 @pytest.mark.parametrize("scheme", [0, 1])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_tb_exact_vs_oracle(gpu, orc, monkeypatch, case, scheme):
+def test_units_exact_vs_oracle(gpu, orc, monkeypatch, case, scheme):
     dims, n, rmin, rmax, per, walls = CASES[case]
     geom = geometry(gpu, dims, n, rmin, rmax, seed=len(case) + 3, periodic=per, walls=walls)
     assert geom.n_links > 0
     p = _params(gpu)
-    sim = _tma_sim(gpu, monkeypatch, geom, p, scheme)
+    sim = _units_sim(gpu, monkeypatch, geom, p, scheme)
     o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, scheme)
     f0, m = _random_state(geom, 5)
     sim.set_pdfs(f0)
     o.set_pdfs(f0)
-    for k in (1, 2, 17, 20, 3):  # K0 + pairs, odd counts end on a one-step sweep
+    for k in (1, 2, 17, 20):  # 20: one graph replay of 16 K1 launches
         sim.step(k)
         o.step(k)
         got, want = sim.get_pdfs(), o.get_pdfs()
@@ -81,12 +84,14 @@ def test_tb_exact_vs_oracle(gpu, orc, monkeypatch, case, scheme):
         assert np.array_equal(np.ravel(a)[mf], np.ravel(b)[mf])
 
 
-def test_tb_walled_channel(gpu, orc, monkeypatch):
-    """An all-fluid walled channel (5 links per cell next to the walls)."""
+def test_units_wall_planes_overflow_pool(gpu, orc, monkeypatch):
+    """An all-fluid walled channel: every cell of the planes next to the walls
+    has 5 links, 160 per unit -- more than the pool holds, so the overflow
+    closes from global memory."""
     geom = gpu.make_box_geometry((128, 8, 12), (True, True, False), True, True)
     for scheme in (0, 1):
         p = _params(gpu)
-        sim = _tma_sim(gpu, monkeypatch, geom, p, scheme)
+        sim = _units_sim(gpu, monkeypatch, geom, p, scheme)
         o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, scheme)
         f0, m = _random_state(geom, 9)
         sim.set_pdfs(f0)
@@ -96,12 +101,12 @@ def test_tb_walled_channel(gpu, orc, monkeypatch):
         assert np.array_equal(sim.get_pdfs()[:, m], o.get_pdfs()[:, m])
 
 
-def test_tb_moving_lid(gpu, orc, monkeypatch):
+def test_units_moving_lid(gpu, orc, monkeypatch):
     dims = (128, 16, 20)
     geom = geometry(gpu, dims, 10, 2.0, 4.0, seed=21)
     p = _params(gpu)
     for scheme in (0, 1):
-        sim = _tma_sim(gpu, monkeypatch, geom, p, scheme)
+        sim = _units_sim(gpu, monkeypatch, geom, p, scheme)
         o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, scheme)
         f0, m = _random_state(geom, 3)
         sim.set_pdfs(f0)
@@ -114,14 +119,14 @@ def test_tb_moving_lid(gpu, orc, monkeypatch):
 
 
 @pytest.mark.parametrize("scheme", [0, 1])
-def test_tb_fast_equals_cpipe_fast(gpu, monkeypatch, scheme):
+def test_units_fast_equals_cpipe_fast(gpu, monkeypatch, scheme):
     """Math mode FAST: the two K1 kernels share the collision, so they agree
     bit for bit (and FAST itself is checked against the reference in
     test_gpu_fast.py)."""
     dims = (128, 32, 40)
     geom = geometry(gpu, dims, 40, 3.0, 6.0, seed=4)
     p = _params(gpu)
-    sim = _tma_sim(gpu, monkeypatch, geom, p, scheme)
+    sim = _units_sim(gpu, monkeypatch, geom, p, scheme)
     sim.math_mode = gpu.MathMode.FAST
     monkeypatch.setenv("PGPU_SWEEP", "cpipe")
     ref = gpu.Simulation.from_params(geom, p, gpu.WallScheme(scheme))
@@ -135,18 +140,37 @@ def test_tb_fast_equals_cpipe_fast(gpu, monkeypatch, scheme):
     assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
     # switching the kernel mid-run keeps the trajectory
     sim.sweep_kernel = "cpipe"
-    ref.sweep_kernel = "tb2"
+    ref.sweep_kernel = "units"
     sim.step(5)
     ref.step(5)
     assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
 
 
-def test_tb_glbm_fluid_only(gpu, orc, monkeypatch):
-    """The GLBM collision (per-plane coefficients by z) on the TMA sweep."""
+@pytest.mark.parametrize("upw", [1, 2, 3, 5, 64])
+def test_units_per_warp_settings(gpu, monkeypatch, upw):
+    """Pipeline lengths: 1, 2, 3 units per warp (the prologue's partial cases),
+    5 and 64 (steady state) -- all bit-identical to the chunk sweep."""
+    dims = (96, 20, 26)
+    geom = geometry(gpu, dims, 16, 2.0, 5.0, seed=11)
+    p = _params(gpu)
+    monkeypatch.setenv("PGPU_UPW", str(upw))
+    sim = _units_sim(gpu, monkeypatch, geom, p, 1)
+    monkeypatch.setenv("PGPU_SWEEP", "cpipe")
+    ref = gpu.Simulation.from_params(geom, p, gpu.WallScheme(1))
+    f0, m = _random_state(geom, 17)
+    sim.set_pdfs(f0)
+    ref.set_pdfs(f0)
+    sim.step(19)
+    ref.step(19)
+    assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
+
+
+def test_units_glbm_fluid_only(gpu, orc, monkeypatch):
+    """The GLBM collision (per-plane coefficients by z) on the UNITS sweep."""
     dims = (128, 12, 24)
     geom = geometry(gpu, dims, 8, 2.0, 4.0, seed=33)
     p = _params(gpu)
-    sim = _tma_sim(gpu, monkeypatch, geom, p, 1)
+    sim = _units_sim(gpu, monkeypatch, geom, p, 1)
     o = orc.simulation(geom, p.nu, p.omega_plus, p.omega_minus, p.body_force, 1)
     nz = dims[2]
     z = np.arange(nz)
