@@ -380,7 +380,10 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     if (const char* e = std::getenv("PGPU_SWEEP"))
       kp.sweep = e[0] == 'u' ? PGPU_SWEEP_UNITS
                  : e[0] == 't' ? PGPU_SWEEP_TMA : (e[0] == 'c' ? PGPU_SWEEP_CPIPE : PGPU_SWEEP_AUTO);
-    if (kp.sweep == PGPU_SWEEP_UNITS) s->ensure_units();
+    // AUTO: large whole-domain simulations run the units sweep (a unit holds <= 32 fluid cells)
+    if (kp.sweep == PGPU_SWEEP_UNITS ||
+        (kp.sweep == PGPU_SWEEP_AUTO && s->compact && !s->slab && sweep_ks >= 32 * kUnitsAutoMin))
+      s->ensure_units();
     lap("alloc pdfs");
     s->refresh_params();
     CK(cudaStreamSynchronize(s->stream));

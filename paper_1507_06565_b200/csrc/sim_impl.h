@@ -330,7 +330,9 @@ struct pgpu_sim {
   int resolved_sweep() const {
     if (!compact) return PGPU_SWEEP_AUTO;
     if (kp.sweep == PGPU_SWEEP_TMA && tma_sweep_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_TMA;
-    if (kp.sweep == PGPU_SWEEP_UNITS && units_sweep_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_UNITS;
+    if ((kp.sweep == PGPU_SWEEP_UNITS || (kp.sweep == PGPU_SWEEP_AUTO && kp.nunits >= kUnitsAutoMin)) &&
+        units_sweep_supported(sweep_cfg(0, 0), kp))
+      return PGPU_SWEEP_UNITS;
     return PGPU_SWEEP_CPIPE;
   }
 

@@ -1022,7 +1022,9 @@ void collide_compact_cm(bool glbm, bool slab, const KParams& p, double* buf, cud
 void launch_sweep_compact(const SweepConfig& cfg, const KParams& p, const double* src,
                           double* dst, cudaStream_t s) {
   if (p.sweep == 2 && tma_sweep_supported(cfg, p) && launch_sweep_tma(cfg, p, src, dst, s)) return;
-  if (p.sweep == 3 && units_sweep_supported(cfg, p) && launch_sweep_units(cfg, p, src, dst, s)) return;
+  if ((p.sweep == 3 || (p.sweep == 0 && p.nunits >= kUnitsAutoMin)) && units_sweep_supported(cfg, p) &&
+      launch_sweep_units(cfg, p, src, dst, s))
+    return;
   switch (collide_mode(p)) {
     case CM_FAST: cdispatch_cm<CM_FAST>(cfg, p, src, dst, s); break;
     case CM_FAST_FOLD: cdispatch_cm<CM_FAST_FOLD>(cfg, p, src, dst, s); break;

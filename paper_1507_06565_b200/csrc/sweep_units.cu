@@ -23,9 +23,9 @@
 // as in k_sweep_cpipe.  The 27 chunk entries of a unit (9 source rows x 3
 // chunks) and the 5 + 5 x-wrap partners are loaded by one lane each.
 //
-// Schedule: units are numbered in slot order (z, y, x); warp w of the grid
-// sweeps the units [w * upw, (w + 1) * upw) one after the other with a
-// four-level per-warp pipeline of 8-byte / 4-byte cp.async copies -- while
+// Schedule: units are numbered in slot order (z, y, x); a block owns a run of
+// 4 * upw consecutive units, dealt round-robin to its 4 warps, and each warp
+// sweeps its upw units one after the other with a four-level per-warp pipeline of 8-byte / 4-byte cp.async copies -- while
 // unit i is collided and stored, the populations (and link records, g_j(x))
 // of unit i+1, the slot words / chunk entries / link descriptors of unit i+2
 // and the unit record of i+3 are in flight.  Warps never synchronise with
@@ -50,7 +50,7 @@ namespace pgpu {
 namespace {
 
 #ifndef PGPU_UNITS_LCAP
-#define PGPU_UNITS_LCAP 128
+#define PGPU_UNITS_LCAP 160
 #endif
 #ifndef PGPU_UNITS_MINB
 #define PGPU_UNITS_MINB 4
@@ -169,15 +169,20 @@ __device__ __forceinline__ void uclose_link(double* stage, int owner, int j, dou
 template <int CM, bool GLBM, bool RECORDS>
 __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
     k_sweep_units(const KParams p, const double* __restrict__ src, double* __restrict__ dst, int upw,
-                  int rev) {
+                  int group, int rev) {
   extern __shared__ __align__(16) unsigned char usmem_raw[];
   updl_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   UWarp<RECORDS>& S = reinterpret_cast<UWarp<RECORDS>*>(usmem_raw)[warp];
+  // `group` consecutive blocks share a run of group * kUW * upw units, dealt
+  // round-robin to their warps: at every pipeline step the warps of a block
+  // (and, roughly, of the group) work on adjacent units -- per direction one
+  // contiguous stretch of memory, and the sectors two units share hit L1
   const int64_t blk = rev ? (int64_t)gridDim.x - 1 - blockIdx.x : (int64_t)blockIdx.x;
-  const int64_t ub = (blk * kUW + warp) * upw;
+  const int stride = group * kUW;
+  const int64_t ub = (blk / group) * ((int64_t)stride * upw) + (blk % group) * kUW + warp;
   if (ub >= p.nunits) return;  // whole warp; warps never synchronise with each other
-  const int nu = (int)min((int64_t)upw, p.nunits - ub);
+  const int nu = (int)min((int64_t)upw, (p.nunits - ub + stride - 1) / stride);
   const UnitRec* const U = p.units + ub;
   // the chunk entry this lane loads for every unit: lanes 0..26 source row
   // lane / 3, chunk c0 + lane % 3; lanes 27..31 the x = nx-1 partner of rows 0..4
@@ -187,7 +192,7 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
   const uint32_t xn_below = (1u << ((p.nx - 1) & 31)) - 1u;
 
   auto rec_load = [&](int i) {
-    if (lane == 0) ucpa16(&S.rec[i & 3], U + i);
+    if (lane == 0) ucpa16(&S.rec[i & 3], U + (int64_t)i * stride);
   };
 
   // slot words, chunk entries and link descriptors of unit i (its record has landed)
@@ -393,11 +398,8 @@ int units_upw(const KParams& p) {
   const char* e = std::getenv("PGPU_UPW");  // experiments and tests (read per launch / graph capture)
   const int env = e ? std::atoi(e) : 0;
   if (env > 0) return env;
-  // one wave of warps (148 SMs x 16) when that leaves each a short run, else
-  // runs of 16 units (many waves: the tail is a few runs)
-  const int64_t slots = 148 * 4 * PGPU_UNITS_MINB;
-  const int64_t one = (p.nunits + slots - 1) / slots;
-  return (int)(one <= 24 ? std::max<int64_t>(one, 1) : 16);
+  (void)p;
+  return 4;  // measured on C2/C3/C4 (tools/gpu_units_ab.sh): shorter runs pay the prologue, longer lose
 }
 
 template <int CM, bool GLBM, bool RECORDS>
@@ -415,9 +417,11 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
     return !(e && e[0] == '0');
   }();
   const int upw = units_upw(p);
-  const int64_t nwarps = (p.nunits + upw - 1) / upw;
+  const char* ge = std::getenv("PGPU_UGROUP");
+  const int group = std::max(1, ge ? std::atoi(ge) : 1);
+  const int64_t per_group = (int64_t)group * kUW * upw;
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)((nwarps + kUW - 1) / kUW));
+  lc.gridDim = dim3((unsigned)((p.nunits + per_group - 1) / per_group * group));
   lc.blockDim = dim3(kUW * 32);
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
@@ -426,7 +430,7 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = pdl_env ? 1 : 0;
-  return cudaLaunchKernelEx(&lc, k_sweep_units<CM, GLBM, RECORDS>, p, src, dst, upw,
+  return cudaLaunchKernelEx(&lc, k_sweep_units<CM, GLBM, RECORDS>, p, src, dst, upw, group,
                             cfg.zrev ? 1 : 0) == cudaSuccess;
 }
 
