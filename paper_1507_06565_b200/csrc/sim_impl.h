@@ -317,8 +317,9 @@ struct pgpu_sim {
       CK(cudaMalloc(&d_udesc, sizeof(uint16_t) * (n_links + 16)));
       CK(cudaMemsetAsync(d_udesc, 0, sizeof(uint16_t) * (n_links + 16), stream));
     }
-    n_units = build_units(d_ctab, d_cellw, d_cellbase, nx, ny, (int64_t)ny * nz, kp.nchunk, &d_units,
-                          d_slotw, d_udesc, stream);
+    const int eb = slab ? sweep_edge_band(nx) : 0;  // slab split: interior columns only
+    n_units = build_units(d_ctab, d_cellw, d_cellbase, nx, ny, (int64_t)ny * nz, kp.nchunk, eb, nx - eb,
+                          &d_units, d_slotw, d_udesc, stream);
     kp.units = d_units;
     kp.slotw = d_slotw;
     kp.udesc = d_udesc;
@@ -331,7 +332,7 @@ struct pgpu_sim {
     if (!compact) return PGPU_SWEEP_AUTO;
     if (kp.sweep == PGPU_SWEEP_TMA && tma_sweep_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_TMA;
     if ((kp.sweep == PGPU_SWEEP_UNITS || (kp.sweep == PGPU_SWEEP_AUTO && kp.nunits >= kUnitsAutoMin)) &&
-        units_sweep_supported(sweep_cfg(0, 0), kp))
+        units_sweep_supported(sweep_cfg(0, slab ? 2 : 0), kp))
       return PGPU_SWEEP_UNITS;
     return PGPU_SWEEP_CPIPE;
   }

@@ -33,9 +33,11 @@
 //
 // The arithmetic per cell is the sweep_compact.cu one (collide<CM, GLBM>, the
 // link closures in the reference order), so the results are bit-identical to
-// k_sweep_cpipe in EXACT and FAST (tests/test_gpu_units.py).  Whole-domain
-// stream+collide only; slab parts, KP and folded links stay on k_sweep_cpipe
-// (same state layout, so the kernels mix freely).
+// k_sweep_cpipe in EXACT and FAST (tests/test_gpu_units.py).  It sweeps the
+// whole domain or, in the x-slab split, the interior columns (the units are
+// then built over those columns only; interior cells read no ghosts and fill
+// no send buffers); the slab edge bands, KP and folded links stay on
+// k_sweep_cpipe (same state layout, so the kernels mix freely).
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstddef>
@@ -148,7 +150,7 @@ struct alignas(16) UWarp {
   double stage[19][32];
   double pool[RECORDS ? 2 * kULCap : 2];  // per link: record, g_j(x)
   UMeta<RECORDS> meta[3];
-  UnitRec rec[4];
+  UnitRec rec[8];
 };
 
 // Closure of one link in the stage (boundary.cpp:24-41 in pull form): slot j
@@ -169,21 +171,53 @@ __device__ __forceinline__ void uclose_link(double* stage, int owner, int j, dou
 template <int CM, bool GLBM, bool RECORDS>
 __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
     k_sweep_units(const KParams p, const double* __restrict__ src, double* __restrict__ dst, int upw,
-                  int group, int rev) {
+                  int group, int rev, int dyn) {
   extern __shared__ __align__(16) unsigned char usmem_raw[];
   updl_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   UWarp<RECORDS>& S = reinterpret_cast<UWarp<RECORDS>*>(usmem_raw)[warp];
-  // `group` consecutive blocks share a run of group * kUW * upw units, dealt
-  // round-robin to their warps: at every pipeline step the warps of a block
-  // (and, roughly, of the group) work on adjacent units -- per direction one
-  // contiguous stretch of memory, and the sectors two units share hit L1
+  // Static schedule: `group` consecutive blocks share a run of group * kUW * upw
+  // units, dealt round-robin to their warps: at every pipeline step the warps
+  // of a block (and, roughly, of the group) work on adjacent units -- per
+  // direction one contiguous stretch of memory, and the sectors two units
+  // share hit L1.  Dynamic schedule (dyn, small domains: one resident wave of
+  // warps, no tail): every warp draws its next unit from a global counter, one
+  // pipeline step ahead of the unit record's load.
   const int64_t blk = rev ? (int64_t)gridDim.x - 1 - blockIdx.x : (int64_t)blockIdx.x;
   const int stride = group * kUW;
   const int64_t ub = (blk / group) * ((int64_t)stride * upw) + (blk % group) * kUW + warp;
-  if (ub >= p.nunits) return;  // whole warp; warps never synchronise with each other
-  const int nu = (int)min((int64_t)upw, (p.nunits - ub + stride - 1) / stride);
-  const UnitRec* const U = p.units + ub;
+  uint32_t* const tk = p.tickets + 4 + 2 * (src < dst ? 1 : 0);  // per buffer parity (PDL overlaps two launches)
+  int drawn = 0;          // static: units handed out so far
+  uint32_t traw = 0;      // dynamic: lane 0's pending ticket
+  if (dyn) {
+    // the counters of this parity may still be in use two launches back (a
+    // dependent launch may start before its predecessor's predecessor ends)
+    updl_wait();
+    if (lane == 0) traw = atomicAdd(tk, 4u);
+  }
+  int head = 0;           // dynamic: tickets left of the first draw of 4
+  // index of the next unit of this warp, -1 when there is none (warp-uniform)
+  auto next_unit = [&]() -> int64_t {
+    if (!dyn) {
+      const int64_t u = ub + (int64_t)drawn * stride;
+      if (drawn >= upw || u >= p.nunits) return -1;
+      ++drawn;
+      return u;
+    }
+    uint32_t t;
+    if (drawn == 0 || head > 0) {  // the first four tickets are one draw
+      if (drawn == 0) head = 4;
+      t = __shfl_sync(0xffffffffu, traw, 0) + (uint32_t)(4 - head);
+      --head;
+      drawn = 1;
+      if (head == 0 && lane == 0) traw = atomicAdd(tk, 1u);
+    } else {
+      t = __shfl_sync(0xffffffffu, traw, 0);
+      if (lane == 0) traw = atomicAdd(tk, 1u);  // consumed one pipeline step later
+    }
+    if ((int64_t)t >= p.nunits) return -1;
+    return rev ? p.nunits - 1 - (int64_t)t : (int64_t)t;
+  };
   // the chunk entry this lane loads for every unit: lanes 0..26 source row
   // lane / 3, chunk c0 + lane % 3; lanes 27..31 the x = nx-1 partner of rows 0..4
   const int er = lane < 27 ? lane / 3 : lane - 27;
@@ -191,13 +225,13 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
   const int eey = urt_ey(er), eez = urt_ez(er);
   const uint32_t xn_below = (1u << ((p.nx - 1) & 31)) - 1u;
 
-  auto rec_load = [&](int i) {
-    if (lane == 0) ucpa16(&S.rec[i & 3], U + (int64_t)i * stride);
+  auto rec_load = [&](int i, int64_t u) {
+    if (lane == 0) ucpa16(&S.rec[i & 7], p.units + u);
   };
 
   // slot words, chunk entries and link descriptors of unit i (its record has landed)
   auto meta_load = [&](int i) {
-    const UnitRec R = S.rec[i & 3];
+    const UnitRec R = S.rec[i & 7];
     UMeta<RECORDS>& M = S.meta[i % 3];
     const int n = R.info & 63, c0 = (R.info >> 8) & 0xFFF;
     const int y = R.yz & 0xFFFF, z = R.yz >> 16;
@@ -243,7 +277,7 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
 
   // populations and link extras of unit i into the stage / pool (its meta has landed)
   auto issue = [&](int i) {
-    const UnitRec R = S.rec[i & 3];
+    const UnitRec R = S.rec[i & 7];
     const UMeta<RECORDS>& M = S.meta[i % 3];
     const int n = R.info & 63;
     if (lane < n) {
@@ -319,25 +353,36 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
   };
 
   // prologue: three dependent levels of static data, then the first populations
-  rec_load(0);
-  if (nu > 1) rec_load(1);
-  if (nu > 2) rec_load(2);
-  ucommit();
-  uwait_all();
-  __syncwarp();
-  meta_load(0);
-  if (nu > 1) meta_load(1);
-  ucommit();
-  uwait_all();
-  __syncwarp();
-  updl_wait();  // everything above is static; populations come from the previous sweep
-  issue(0);
-  ucommit();
-
-  for (int i = 0; i < nu; ++i) {
+  // v1..v3: the units i+1..i+3 exist
+  const int64_t u0 = next_unit();
+  bool v1 = false, v2 = false, v3 = false;
+  if (u0 >= 0) {  // whole warp; warps never synchronise with each other
+    rec_load(0, u0);
+    const int64_t u1 = next_unit(), u2 = u1 >= 0 ? next_unit() : -1;
+    v1 = u1 >= 0;
+    v2 = u2 >= 0;
+    if (v1) rec_load(1, u1);
+    if (v2) rec_load(2, u2);
+    ucommit();
     uwait_all();
     __syncwarp();
-    const UnitRec R = S.rec[i & 3];
+    meta_load(0);
+    if (v1) meta_load(1);
+    const int64_t u3 = v2 ? next_unit() : -1;
+    v3 = u3 >= 0;
+    if (v3) rec_load(3, u3);
+    ucommit();
+    uwait_all();
+    __syncwarp();
+    updl_wait();  // everything above is static; populations come from the previous sweep
+    issue(0);
+    ucommit();
+  }
+
+  for (int i = 0; u0 >= 0; ++i) {
+    uwait_all();
+    __syncwarp();
+    const UnitRec R = S.rec[i & 7];
     const UMeta<RECORDS>& M = S.meta[i % 3];
     const int n = R.info & 63;
     const bool fluid = lane < n;
@@ -376,9 +421,14 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
       for (int j = 0; j < 19; ++j) f[j] = S.stage[j][lane];
     }
     __syncwarp();  // stage and pool consumed: refill them with unit i+1
-    if (i + 1 < nu) issue(i + 1);
-    if (i + 2 < nu) meta_load(i + 2);
-    if (i + 3 < nu) rec_load(i + 3);
+    if (v1) issue(i + 1);
+    if (v2) meta_load(i + 2);
+    bool v4 = false;
+    if (v3) {  // unit i+3's record landed with this step's wait; fetch unit i+4's
+      const int64_t u4 = next_unit();
+      v4 = u4 >= 0;
+      if (v4) rec_load(i + 4, u4);
+    }
     ucommit();
     if (fluid) {
       collide<CM, GLBM>(f, p, (int)(R.yz >> 16));
@@ -390,8 +440,17 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
           dst[(uint32_t)(fc + p.poff[j])] = f[j];
       }
     }
+    if (!v1) break;
+    v1 = v2;
+    v2 = v3;
+    v3 = v4;
   }
   uwait_all();
+  // dynamic schedule: the last warp to run out of units zeroes the counters
+  if (dyn && lane == 0 && atomicAdd(tk + 1, 1u) == gridDim.x * kUW - 1) {
+    atomicExch(tk, 0u);
+    atomicExch(tk + 1, 0u);
+  }
 }
 
 int units_upw(const KParams& p) {
@@ -420,8 +479,14 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
   const char* ge = std::getenv("PGPU_UGROUP");
   const int group = std::max(1, ge ? std::atoi(ge) : 1);
   const int64_t per_group = (int64_t)group * kUW * upw;
+  // dynamic schedule (PGPU_UDYN=1|0; default: domains a resident wave sweeps
+  // in fewer than 64 units per warp): one wave of warps drawing units
+  const int64_t resident = 148 * PGPU_UNITS_MINB;
+  const char* de = std::getenv("PGPU_UDYN");
+  const bool dyn = p.tickets && (de ? de[0] == '1' : p.nunits < resident * kUW * 64);
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)((p.nunits + per_group - 1) / per_group * group));
+  lc.gridDim = dyn ? dim3((unsigned)std::min<int64_t>(resident, (p.nunits + kUW - 1) / kUW))
+                   : dim3((unsigned)((p.nunits + per_group - 1) / per_group * group));
   lc.blockDim = dim3(kUW * 32);
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
@@ -429,9 +494,9 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
-  lc.numAttrs = pdl_env ? 1 : 0;
+  lc.numAttrs = pdl_env && !cfg.slab ? 1 : 0;
   return cudaLaunchKernelEx(&lc, k_sweep_units<CM, GLBM, RECORDS>, p, src, dst, upw, group,
-                            cfg.zrev ? 1 : 0) == cudaSuccess;
+                            cfg.zrev ? 1 : 0, dyn ? 1 : 0) == cudaSuccess;
 }
 
 template <int CM>
@@ -446,9 +511,12 @@ bool units_cm(const SweepConfig& cfg, const KParams& p, const double* src, doubl
 
 }  // namespace
 
+int sweep_edge_band(int nx) { return edge_band(nx); }
+
 bool units_sweep_supported(const SweepConfig& cfg, const KParams& p) {
-  return p.ctab && p.units && p.slotw && p.nunits > 0 && !cfg.slab && cfg.part == PART_ALL &&
-         cfg.op == OP_STREAM_COLLIDE && collide_mode(p) != CM_FAST_FOLD &&
+  // slab split: the units cover the interior columns (sim_impl.h ensure_units)
+  return p.ctab && p.units && p.slotw && p.nunits > 0 &&
+         cfg.part == (cfg.slab ? PART_INTERIOR : PART_ALL) && cfg.op == OP_STREAM_COLLIDE && collide_mode(p) != CM_FAST_FOLD &&
          (p.udesc || !cfg.records) && p.nchunk <= 4096 && p.ny <= 65535 && p.nz <= 65535;
 }
 

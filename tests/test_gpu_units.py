@@ -146,16 +146,19 @@ def test_units_fast_equals_cpipe_fast(gpu, monkeypatch, scheme):
     assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
 
 
-@pytest.mark.parametrize("upw,group", [(1, 1), (2, 1), (3, 2), (5, 3), (64, 1), (4, 8)])
-def test_units_per_warp_settings(gpu, monkeypatch, upw, group):
+@pytest.mark.parametrize("upw,group,dyn", [(1, 1, 0), (2, 1, 0), (3, 2, 0), (5, 3, 0), (64, 1, 0),
+                                            (4, 8, 0), (4, 1, 1)])
+def test_units_per_warp_settings(gpu, monkeypatch, upw, group, dyn):
     """Pipeline lengths: 1, 2, 3 units per warp (the prologue's partial cases),
-    5 and 64 (steady state), and groups of blocks sharing a run of units -- all
-    bit-identical to the chunk sweep."""
+    5 and 64 (steady state), groups of blocks sharing a run of units, and the
+    dynamic schedule (warps draw units from a counter) -- all bit-identical to
+    the chunk sweep."""
     dims = (96, 20, 26)
     geom = geometry(gpu, dims, 16, 2.0, 5.0, seed=11)
     p = _params(gpu)
     monkeypatch.setenv("PGPU_UPW", str(upw))
     monkeypatch.setenv("PGPU_UGROUP", str(group))
+    monkeypatch.setenv("PGPU_UDYN", str(dyn))
     sim = _units_sim(gpu, monkeypatch, geom, p, 1)
     monkeypatch.setenv("PGPU_SWEEP", "cpipe")
     ref = gpu.Simulation.from_params(geom, p, gpu.WallScheme(1))
@@ -164,6 +167,9 @@ def test_units_per_warp_settings(gpu, monkeypatch, upw, group):
     ref.set_pdfs(f0)
     sim.step(19)
     ref.step(19)
+    assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
+    sim.step(40)  # graph replays: the dynamic schedule's counters reset between launches
+    ref.step(40)
     assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
 
 
@@ -187,3 +193,29 @@ def test_units_glbm_fluid_only(gpu, orc, monkeypatch):
     sim.step(21)
     o.step(21)
     assert np.array_equal(sim.get_pdfs()[:, m], o.get_pdfs()[:, m])
+
+
+@pytest.mark.parametrize("nx,world", [(256, 2), (200, 2), (96, 3)])
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_units_slab_interior(gpu, monkeypatch, nx, world, scheme):
+    """x-slab split: the units cover the interior columns of each slab (the
+    edge bands -- 32 columns, or the face columns of slabs narrower than 96 --
+    stay on the chunk sweep, which alone reads ghosts and fills the send
+    buffers).  Slabs of 128, 100 and 32 columns against the single domain on
+    the chunk sweep, bit for bit."""
+    from paper_1507_06565_b200 import configs
+    from paper_1507_06565_b200.dist import LocalTransport
+    from test_gpu_dist import bed_workload
+    monkeypatch.setenv("PGPU_LAYOUT", "compact")
+    monkeypatch.setenv("PGPU_SWEEP", "units")
+    w = bed_workload(gpu, scheme, nx=nx)
+    lt = LocalTransport(w, world, device=0)
+    assert all(r.sim.sweep_kernel == "units" for r in lt.ranks), "the slabs do not run the units sweep"
+    lt.step(w.steps)
+    monkeypatch.setenv("PGPU_SWEEP", "cpipe")
+    g = w.geometry()
+    sim = configs.make_simulation(w, g)
+    assert sim.sweep_kernel == "cpipe"
+    sim.step(w.steps)
+    fl = g.flags.reshape(w.dims[::-1]) == 0
+    assert np.array_equal(lt.gather_pdfs()[:, fl], sim.get_pdfs()[:, fl])
