@@ -48,10 +48,6 @@ struct alignas(16) UnitRec {
 // Per fluid slot (units sweep): the cell word's bits 0..18 | position relative
 // to the unit's first chunk, (chunk - c0) * 32 + (x & 31), in bits 19..25 |
 // x == 0 (bit 26) | x == nx-1 (bit 27).
-// AUTO runs the units sweep on domains of at least this many units (about
-// 5 M fluid cells: ~70 units per resident warp); below, the chunk sweep's
-// z-march measured the same or better (C2/C3: 26 k units).
-constexpr int64_t kUnitsAutoMin = 150000;
 constexpr int kSlotRelShift = 19;
 constexpr uint32_t kSlotX0 = 1u << 26;
 constexpr uint32_t kSlotXN = 1u << 27;

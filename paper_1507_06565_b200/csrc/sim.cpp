@@ -341,8 +341,8 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     CK(cudaMalloc(&s->d_flags, sizeof(int) * 2));
     CK(cudaMalloc(&s->d_vmax, sizeof(unsigned long long)));
     CK(cudaMalloc(&s->d_sums, sizeof(double) * s->nz));
-    CK(cudaMalloc(&s->d_tickets, sizeof(uint32_t) * 8));  // [0..1] TMA sweep, [4..7] units sweep
-    CK(cudaMemsetAsync(s->d_tickets, 0, sizeof(uint32_t) * 8, s->stream));
+    CK(cudaMalloc(&s->d_tickets, sizeof(uint32_t) * 2));
+    CK(cudaMemsetAsync(s->d_tickets, 0, sizeof(uint32_t) * 2, s->stream));
     KParams& kp = s->kp;
     kp.nx = s->nx;
     kp.ny = s->ny;
@@ -380,10 +380,8 @@ int pgpu_create(const pgpu_geometry* g, const pgpu_fluid_params* params, int32_t
     if (const char* e = std::getenv("PGPU_SWEEP"))
       kp.sweep = e[0] == 'u' ? PGPU_SWEEP_UNITS
                  : e[0] == 't' ? PGPU_SWEEP_TMA : (e[0] == 'c' ? PGPU_SWEEP_CPIPE : PGPU_SWEEP_AUTO);
-    // AUTO: large whole-domain simulations run the units sweep (a unit holds <= 32 fluid cells)
-    if (kp.sweep == PGPU_SWEEP_UNITS ||
-        (kp.sweep == PGPU_SWEEP_AUTO && s->compact && sweep_ks >= 32 * kUnitsAutoMin))
-      s->ensure_units();
+    // AUTO: the fluid-only layout runs the units sweep
+    if (kp.sweep == PGPU_SWEEP_UNITS || (kp.sweep == PGPU_SWEEP_AUTO && s->compact)) s->ensure_units();
     lap("alloc pdfs");
     s->refresh_params();
     CK(cudaStreamSynchronize(s->stream));

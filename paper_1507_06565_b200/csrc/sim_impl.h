@@ -331,7 +331,7 @@ struct pgpu_sim {
   int resolved_sweep() const {
     if (!compact) return PGPU_SWEEP_AUTO;
     if (kp.sweep == PGPU_SWEEP_TMA && tma_sweep_supported(sweep_cfg(0, 0), kp)) return PGPU_SWEEP_TMA;
-    if ((kp.sweep == PGPU_SWEEP_UNITS || (kp.sweep == PGPU_SWEEP_AUTO && kp.nunits >= kUnitsAutoMin)) &&
+    if ((kp.sweep == PGPU_SWEEP_UNITS || kp.sweep == PGPU_SWEEP_AUTO) &&
         units_sweep_supported(sweep_cfg(0, slab ? 2 : 0), kp))
       return PGPU_SWEEP_UNITS;
     return PGPU_SWEEP_CPIPE;

@@ -1022,7 +1022,7 @@ void collide_compact_cm(bool glbm, bool slab, const KParams& p, double* buf, cud
 void launch_sweep_compact(const SweepConfig& cfg, const KParams& p, const double* src,
                           double* dst, cudaStream_t s) {
   if (p.sweep == 2 && tma_sweep_supported(cfg, p) && launch_sweep_tma(cfg, p, src, dst, s)) return;
-  if ((p.sweep == 3 || (p.sweep == 0 && p.nunits >= kUnitsAutoMin)) && units_sweep_supported(cfg, p) &&
+  if ((p.sweep == 3 || p.sweep == 0) && units_sweep_supported(cfg, p) &&
       launch_sweep_units(cfg, p, src, dst, s))
     return;
   switch (collide_mode(p)) {

@@ -171,52 +171,27 @@ __device__ __forceinline__ void uclose_link(double* stage, int owner, int j, dou
 template <int CM, bool GLBM, bool RECORDS>
 __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
     k_sweep_units(const KParams p, const double* __restrict__ src, double* __restrict__ dst, int upw,
-                  int group, int rev, int dyn) {
+                  int group, int rev) {
   extern __shared__ __align__(16) unsigned char usmem_raw[];
   updl_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   UWarp<RECORDS>& S = reinterpret_cast<UWarp<RECORDS>*>(usmem_raw)[warp];
-  // Static schedule: `group` consecutive blocks share a run of group * kUW * upw
-  // units, dealt round-robin to their warps: at every pipeline step the warps
-  // of a block (and, roughly, of the group) work on adjacent units -- per
-  // direction one contiguous stretch of memory, and the sectors two units
-  // share hit L1.  Dynamic schedule (dyn, small domains: one resident wave of
-  // warps, no tail): every warp draws its next unit from a global counter, one
-  // pipeline step ahead of the unit record's load.
+  // `group` consecutive blocks share a run of group * kUW * upw units, dealt
+  // round-robin to their warps: at every pipeline step the warps of a block
+  // (and, roughly, of the group) work on adjacent units -- per direction one
+  // contiguous stretch of memory, and the sectors two units share hit L1.
+  // (A dynamic schedule -- one resident wave of warps drawing units from a
+  // global counter -- measured the same or worse on C2/C3 and was removed.)
   const int64_t blk = rev ? (int64_t)gridDim.x - 1 - blockIdx.x : (int64_t)blockIdx.x;
   const int stride = group * kUW;
   const int64_t ub = (blk / group) * ((int64_t)stride * upw) + (blk % group) * kUW + warp;
-  uint32_t* const tk = p.tickets + 4 + 2 * (src < dst ? 1 : 0);  // per buffer parity (PDL overlaps two launches)
-  int drawn = 0;          // static: units handed out so far
-  uint32_t traw = 0;      // dynamic: lane 0's pending ticket
-  if (dyn) {
-    // the counters of this parity may still be in use two launches back (a
-    // dependent launch may start before its predecessor's predecessor ends)
-    updl_wait();
-    if (lane == 0) traw = atomicAdd(tk, 4u);
-  }
-  int head = 0;           // dynamic: tickets left of the first draw of 4
+  int drawn = 0;  // units handed out so far
   // index of the next unit of this warp, -1 when there is none (warp-uniform)
   auto next_unit = [&]() -> int64_t {
-    if (!dyn) {
-      const int64_t u = ub + (int64_t)drawn * stride;
-      if (drawn >= upw || u >= p.nunits) return -1;
-      ++drawn;
-      return u;
-    }
-    uint32_t t;
-    if (drawn == 0 || head > 0) {  // the first four tickets are one draw
-      if (drawn == 0) head = 4;
-      t = __shfl_sync(0xffffffffu, traw, 0) + (uint32_t)(4 - head);
-      --head;
-      drawn = 1;
-      if (head == 0 && lane == 0) traw = atomicAdd(tk, 1u);
-    } else {
-      t = __shfl_sync(0xffffffffu, traw, 0);
-      if (lane == 0) traw = atomicAdd(tk, 1u);  // consumed one pipeline step later
-    }
-    if ((int64_t)t >= p.nunits) return -1;
-    return rev ? p.nunits - 1 - (int64_t)t : (int64_t)t;
+    const int64_t u = ub + (int64_t)drawn * stride;
+    if (drawn >= upw || u >= p.nunits) return -1;
+    ++drawn;
+    return u;
   };
   // the chunk entry this lane loads for every unit: lanes 0..26 source row
   // lane / 3, chunk c0 + lane % 3; lanes 27..31 the x = nx-1 partner of rows 0..4
@@ -297,45 +272,47 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
       const uint32_t fc = R.s0 + lane;
       ubounds((uint32_t)q[0] == fc);
       double* const st = &S.stage[0][lane];
-      if (!(sw & (kSlotX0 | kSlotXN))) {
+      // slot of the e_x = +1 / -1 source per row (rows 0..4 hold those
+      // directions).  A cell on an x face pulls from the periodic partner
+      // column instead: its slots replace the values (selects, no divergent
+      // path; x faces that are not periodic carry bounce bits, so the values
+      // go unused there).
+      int qp[5], qn[5];
 #pragma unroll
-        for (int j = 0; j < 19; ++j) {
-          uint32_t idx;  // unsigned: 19 * ks may exceed 2^31
-          if (j == 0) {
-            idx = fc;
-          } else if ((sw >> j) & 1u) {
-            idx = fc + p.poff[opp(j)];  // bounce: g_k(x)
-          } else {
-            const int r = urow_of(j);
-            idx = q[r] + p.poff[j];
-            if (EX[j] == 1) idx -= 1;
-            if (EX[j] == -1) idx += (bits >> r) & 1u;
-          }
-          ubounds(idx < 19ull * p.ks);
-          ucpa8(st + j * 32, src + idx);
-        }
-      } else {  // cell on an x face: periodic partner chunk
+      for (int r = 0; r < 5; ++r) {
+        qp[r] = q[r] - 1;
+        qn[r] = q[r] + (int)((bits >> r) & 1u);
+      }
+      if (R.info & 64u) {  // warp-uniform: the unit holds x = 0
+        const bool me = sw & kSlotX0;
 #pragma unroll
-        for (int j = 0; j < 19; ++j) {
-          uint32_t idx;
-          if (j == 0) {
-            idx = fc;
-          } else if ((sw >> j) & 1u) {
-            idx = fc + p.poff[opp(j)];
-          } else if (EX[j] == 1 && (sw & kSlotX0)) {
-            const ChunkEnt e = M.ent[27 + urow_of(j)];
-            idx = e.rank + __popc(e.mask & xn_below) + p.poff[j];
-          } else if (EX[j] == -1 && (sw & kSlotXN)) {
-            idx = M.ent[32 + urow_of(j)].rank + p.poff[j];
-          } else {
-            const int r = urow_of(j);
-            idx = q[r] + p.poff[j];
-            if (EX[j] == 1) idx -= 1;
-            if (EX[j] == -1) idx += (bits >> r) & 1u;
-          }
-          ubounds(idx < 19ull * p.ks);
-          ucpa8(st + j * 32, src + idx);
+        for (int r = 0; r < 5; ++r) {
+          const ChunkEnt e = M.ent[27 + r];
+          const int v = (int)e.rank + __popc(e.mask & xn_below);
+          if (me) qp[r] = v;
         }
+      }
+      if (R.info & 128u) {  // ... x = nx-1
+        const bool me = sw & kSlotXN;
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+          const int v = (int)M.ent[32 + r].rank;
+          if (me) qn[r] = v;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 19; ++j) {
+        uint32_t idx;  // unsigned: 19 * ks may exceed 2^31
+        if (j == 0) {
+          idx = fc;
+        } else if ((sw >> j) & 1u) {
+          idx = fc + p.poff[opp(j)];  // bounce: g_k(x)
+        } else {
+          const int r = urow_of(j);
+          idx = (EX[j] == 0 ? q[r] : (EX[j] == 1 ? qp[r] : qn[r])) + p.poff[j];
+        }
+        ubounds(idx < 19ull * p.ks);
+        ucpa8(st + j * 32, src + idx);
       }
     }
     if (RECORDS) {
@@ -446,11 +423,6 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
     v3 = v4;
   }
   uwait_all();
-  // dynamic schedule: the last warp to run out of units zeroes the counters
-  if (dyn && lane == 0 && atomicAdd(tk + 1, 1u) == gridDim.x * kUW - 1) {
-    atomicExch(tk, 0u);
-    atomicExch(tk + 1, 0u);
-  }
 }
 
 int units_upw(const KParams& p) {
@@ -479,14 +451,8 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
   const char* ge = std::getenv("PGPU_UGROUP");
   const int group = std::max(1, ge ? std::atoi(ge) : 1);
   const int64_t per_group = (int64_t)group * kUW * upw;
-  // dynamic schedule (PGPU_UDYN=1|0; default: domains a resident wave sweeps
-  // in fewer than 64 units per warp): one wave of warps drawing units
-  const int64_t resident = 148 * PGPU_UNITS_MINB;
-  const char* de = std::getenv("PGPU_UDYN");
-  const bool dyn = p.tickets && (de ? de[0] == '1' : p.nunits < resident * kUW * 64);
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dyn ? dim3((unsigned)std::min<int64_t>(resident, (p.nunits + kUW - 1) / kUW))
-                   : dim3((unsigned)((p.nunits + per_group - 1) / per_group * group));
+  lc.gridDim = dim3((unsigned)((p.nunits + per_group - 1) / per_group * group));
   lc.blockDim = dim3(kUW * 32);
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
@@ -496,7 +462,7 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
   lc.attrs = at;
   lc.numAttrs = pdl_env && !cfg.slab ? 1 : 0;
   return cudaLaunchKernelEx(&lc, k_sweep_units<CM, GLBM, RECORDS>, p, src, dst, upw, group,
-                            cfg.zrev ? 1 : 0, dyn ? 1 : 0) == cudaSuccess;
+                            cfg.zrev ? 1 : 0) == cudaSuccess;
 }
 
 template <int CM>

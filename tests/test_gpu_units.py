@@ -146,19 +146,16 @@ def test_units_fast_equals_cpipe_fast(gpu, monkeypatch, scheme):
     assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
 
 
-@pytest.mark.parametrize("upw,group,dyn", [(1, 1, 0), (2, 1, 0), (3, 2, 0), (5, 3, 0), (64, 1, 0),
-                                            (4, 8, 0), (4, 1, 1)])
-def test_units_per_warp_settings(gpu, monkeypatch, upw, group, dyn):
+@pytest.mark.parametrize("upw,group", [(1, 1), (2, 1), (3, 2), (5, 3), (64, 1), (4, 8)])
+def test_units_per_warp_settings(gpu, monkeypatch, upw, group):
     """Pipeline lengths: 1, 2, 3 units per warp (the prologue's partial cases),
-    5 and 64 (steady state), groups of blocks sharing a run of units, and the
-    dynamic schedule (warps draw units from a counter) -- all bit-identical to
-    the chunk sweep."""
+    5 and 64 (steady state) and groups of blocks sharing a run of units -- all
+    bit-identical to the chunk sweep."""
     dims = (96, 20, 26)
     geom = geometry(gpu, dims, 16, 2.0, 5.0, seed=11)
     p = _params(gpu)
     monkeypatch.setenv("PGPU_UPW", str(upw))
     monkeypatch.setenv("PGPU_UGROUP", str(group))
-    monkeypatch.setenv("PGPU_UDYN", str(dyn))
     sim = _units_sim(gpu, monkeypatch, geom, p, 1)
     monkeypatch.setenv("PGPU_SWEEP", "cpipe")
     ref = gpu.Simulation.from_params(geom, p, gpu.WallScheme(1))
@@ -168,7 +165,7 @@ def test_units_per_warp_settings(gpu, monkeypatch, upw, group, dyn):
     sim.step(19)
     ref.step(19)
     assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
-    sim.step(40)  # graph replays: the dynamic schedule's counters reset between launches
+    sim.step(40)  # graph replays
     ref.step(40)
     assert np.array_equal(sim.get_pdfs()[:, m], ref.get_pdfs()[:, m])
 

@@ -19,7 +19,7 @@ cfg, k, upw, rc = sys.argv[1:5]
 try:
     d = json.loads(open('gpurun_out/u_tmp.json').read().strip().splitlines()[-1])
     import os
-    print(cfg, k, 'upw=' + upw, 'group=' + os.environ.get('PGPU_UGROUP', '1'), 'dyn=' + os.environ.get('PGPU_UDYN', 'auto'), round(d['value']), round(d['roofline']['frac'], 4), d['clocks']['sm_mhz'], d.get('sweep_kernel'))
+    print(cfg, k, 'upw=' + upw, 'group=' + os.environ.get('PGPU_UGROUP', '1'), round(d['value']), round(d['roofline']['frac'], 4), d['clocks']['sm_mhz'], d.get('sweep_kernel'))
 except Exception as e:
     print(cfg, k, upw, 'rc=' + rc, 'failed', e)
 PY
