@@ -184,15 +184,14 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
   // global counter -- measured the same or worse on C2/C3 and was removed.)
   const int64_t blk = rev ? (int64_t)gridDim.x - 1 - blockIdx.x : (int64_t)blockIdx.x;
   const int stride = group * kUW;
-  const int64_t ub = (blk / group) * ((int64_t)stride * upw) + (blk % group) * kUW + warp;
-  int drawn = 0;  // units handed out so far
-  // index of the next unit of this warp, -1 when there is none (warp-uniform)
-  auto next_unit = [&]() -> int64_t {
-    const int64_t u = ub + (int64_t)drawn * stride;
-    if (drawn >= upw || u >= p.nunits) return -1;
-    ++drawn;
-    return u;
-  };
+  // first unit of the block and its pipeline length: block-uniform by
+  // construction (blockIdx and kernel parameters only), so the compiler keeps
+  // the loop control and the memory descriptors in uniform registers.  Only
+  // the last block's warps 1..3 may run one unit past the end: the unit array
+  // ends with zero records (n = 0: nothing to load, collide or store).
+  const int64_t first = (blk / group) * ((int64_t)stride * upw) + (blk % group) * kUW;
+  const int nu = (int)min((int64_t)upw, (p.nunits - first + stride - 1) / stride);
+  const UnitRec* const U = p.units + first + warp;
   // the chunk entry this lane loads for every unit: lanes 0..26 source row
   // lane / 3, chunk c0 + lane % 3; lanes 27..31 the x = nx-1 partner of rows 0..4
   const int er = lane < 27 ? lane / 3 : lane - 27;
@@ -200,8 +199,8 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
   const int eey = urt_ey(er), eez = urt_ez(er);
   const uint32_t xn_below = (1u << ((p.nx - 1) & 31)) - 1u;
 
-  auto rec_load = [&](int i, int64_t u) {
-    if (lane == 0) ucpa16(&S.rec[i & 7], p.units + u);
+  auto rec_load = [&](int i) {
+    if (lane == 0) ucpa16(&S.rec[i & 7], U + (int64_t)i * stride);
   };
 
   // slot words, chunk entries and link descriptors of unit i (its record has landed)
@@ -330,33 +329,23 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
   };
 
   // prologue: three dependent levels of static data, then the first populations
-  // v1..v3: the units i+1..i+3 exist
-  const int64_t u0 = next_unit();
-  bool v1 = false, v2 = false, v3 = false;
-  if (u0 >= 0) {  // whole warp; warps never synchronise with each other
-    rec_load(0, u0);
-    const int64_t u1 = next_unit(), u2 = u1 >= 0 ? next_unit() : -1;
-    v1 = u1 >= 0;
-    v2 = u2 >= 0;
-    if (v1) rec_load(1, u1);
-    if (v2) rec_load(2, u2);
-    ucommit();
-    uwait_all();
-    __syncwarp();
-    meta_load(0);
-    if (v1) meta_load(1);
-    const int64_t u3 = v2 ? next_unit() : -1;
-    v3 = u3 >= 0;
-    if (v3) rec_load(3, u3);
-    ucommit();
-    uwait_all();
-    __syncwarp();
-    updl_wait();  // everything above is static; populations come from the previous sweep
-    issue(0);
-    ucommit();
-  }
+  rec_load(0);
+  if (nu > 1) rec_load(1);
+  if (nu > 2) rec_load(2);
+  ucommit();
+  uwait_all();
+  __syncwarp();
+  meta_load(0);
+  if (nu > 1) meta_load(1);
+  if (nu > 3) rec_load(3);
+  ucommit();
+  uwait_all();
+  __syncwarp();
+  updl_wait();  // everything above is static; populations come from the previous sweep
+  issue(0);
+  ucommit();
 
-  for (int i = 0; u0 >= 0; ++i) {
+  for (int i = 0; i < nu; ++i) {
     uwait_all();
     __syncwarp();
     const UnitRec R = S.rec[i & 7];
@@ -371,9 +360,28 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
         double* const stage = &S.stage[0][0];
         const int ncoop = min(nl, kULCap);
         const uint16_t* ld = M.ldesc + (R.lbase & 1u);
-        for (int e = lane; e < ncoop; e += 32) {
-          const int d = ld[e];
-          uclose_link(stage, d & 31, d >> 5, S.pool[2 * e], S.pool[2 * e + 1], p);
+        // two links per lane and round, all shared-memory reads before the
+        // arithmetic (the closures of different links are independent: a
+        // link whose opposite direction is cut as well has no second fluid
+        // cell, so its record is SBB or moving and reads only its own slot)
+        for (int e0 = lane; e0 < ncoop; e0 += 64) {
+          const int e1 = e0 + 32;
+          const bool two = e1 < ncoop;
+          const int d0 = ld[e0], d1 = two ? ld[e1] : 0;
+          const double r0 = S.pool[2 * e0], g0 = S.pool[2 * e0 + 1];
+          const double r1 = two ? S.pool[2 * e1] : nan(""), g1 = two ? S.pool[2 * e1 + 1] : 0.0;
+          const int j0 = d0 >> 5, o0 = d0 & 31, j1 = d1 >> 5, o1 = d1 & 31;
+          const int k0 = (j0 & 1) ? j0 + 1 : j0 - 1, k1 = (j1 & 1) ? j1 + 1 : j1 - 1;
+          double* const s0 = stage + j0 * 32 + o0;
+          double* const s1 = stage + j1 * 32 + o1;
+          const double gk0 = *s0, pk0 = stage[k0 * 32 + o0];
+          double gk1 = 0.0, pk1 = 0.0;
+          if (two) {
+            gk1 = *s1;
+            pk1 = stage[k1 * 32 + o1];
+          }
+          if (r0 == r0) *s0 = isinf(r0) ? DSUB(gk0, p.mw[k0]) : DADD(DSUB(DMUL(r0, pk0), DMUL(r0, g0)), gk0);
+          if (r1 == r1) *s1 = isinf(r1) ? DSUB(gk1, p.mw[k1]) : DADD(DSUB(DMUL(r1, pk1), DMUL(r1, g1)), gk1);
         }
         if (nl > kULCap) {  // pool overflow: each lane closes the rest of its own links
           int tot;
@@ -398,29 +406,24 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
       for (int j = 0; j < 19; ++j) f[j] = S.stage[j][lane];
     }
     __syncwarp();  // stage and pool consumed: refill them with unit i+1
-    if (v1) issue(i + 1);
-    if (v2) meta_load(i + 2);
-    bool v4 = false;
-    if (v3) {  // unit i+3's record landed with this step's wait; fetch unit i+4's
-      const int64_t u4 = next_unit();
-      v4 = u4 >= 0;
-      if (v4) rec_load(i + 4, u4);
-    }
+    if (i + 1 < nu) issue(i + 1);
+    if (i + 2 < nu) meta_load(i + 2);
+    if (i + 4 < nu) rec_load(i + 4);
     ucommit();
     if (fluid) {
       collide<CM, GLBM>(f, p, (int)(R.yz >> 16));
+      // one 64-bit base per cell, the plane offset added per direction; the
+      // store kind is chosen once (inside the unrolled loop the compiler
+      // predicates both stores: 2 x 19 more instructions per unit)
+      double* const d0 = dst + fc;
+      if (PGPU_STCS && p.stream_stores) {
 #pragma unroll
-      for (int j = 0; j < 19; ++j) {
-        if (PGPU_STCS && p.stream_stores)
-          __stcs(dst + (uint32_t)(fc + p.poff[j]), f[j]);
-        else
-          dst[(uint32_t)(fc + p.poff[j])] = f[j];
+        for (int j = 0; j < 19; ++j) __stcs(d0 + p.poff[j], f[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 19; ++j) d0[p.poff[j]] = f[j];
       }
     }
-    if (!v1) break;
-    v1 = v2;
-    v2 = v3;
-    v3 = v4;
   }
   uwait_all();
 }
@@ -430,7 +433,7 @@ int units_upw(const KParams& p) {
   const int env = e ? std::atoi(e) : 0;
   if (env > 0) return env;
   (void)p;
-  return 4;  // measured on C2/C3/C4 (tools/gpu_units_ab.sh): shorter runs pay the prologue, longer lose
+  return 4;  // measured on C2/C3/C4 (tools/gpu_units_ab.sh): shorter runs pay the prologue, longer lose balance
 }
 
 template <int CM, bool GLBM, bool RECORDS>
