@@ -34,11 +34,17 @@ struct alignas(8) ChunkEnt {
 };
 
 // Units sweep (sweep_units.cu): a unit is a run of <= 32 consecutive fluid
-// slots of one row whose cells lie in <= 3 consecutive chunks, so a warp that
-// sweeps a unit has no lane on a solid cell.  Units are numbered in slot order.
+// slots of one row whose cells lie in <= 3 consecutive chunks and hold at most
+// kUnitLinkCap link records together (the warp closes them from a fixed pool
+// in shared memory), so a warp that sweeps a unit has no lane on a solid
+// cell.  Units are numbered in slot order.
 //   yz   = y | z << 16
 //   info = n (bits 0..5) | holds x = 0 (bit 6) | holds x = nx-1 (bit 7)
 //          | first chunk c0 (bits 8..19) | link records (bits 20..31)
+#ifndef PGPU_UNITS_LCAP
+#define PGPU_UNITS_LCAP 160  // a full unit next to a wall: 32 cells x 5 links
+#endif
+constexpr int kUnitLinkCap = PGPU_UNITS_LCAP;
 struct alignas(16) UnitRec {
   uint32_t s0;     // first fluid slot
   uint32_t lbase;  // first link record (the unit's records are contiguous)

@@ -296,9 +296,11 @@ __global__ void k_units(const ChunkEnt* __restrict__ ctab, const uint32_t* __res
       const int b = __ffs(m) - 1;
       m &= m - 1;
       const uint32_t slot = e.rank + __popc(e.mask & ((1u << b) - 1u));
-      if (n && (n == 32 || c - c0 >= 3)) close();
       const int x = c * 32 + b;
       const int64_t cell = row * nx + x;
+      const uint32_t w = cellw[cell];
+      const int wl = __popc(w & kBounceMask);
+      if (n && (n == 32 || c - c0 >= 3 || nl + wl > kUnitLinkCap)) close();
       if (!n) {
         c0 = c;
         s0 = slot;
@@ -307,7 +309,6 @@ __global__ void k_units(const ChunkEnt* __restrict__ ctab, const uint32_t* __res
         if (FILL) lbase = (uint32_t)cellbase[cell];
       }
       if (FILL) {
-        const uint32_t w = cellw[cell];
         const uint32_t fx = (x == 0 ? kSlotX0 : 0u) | (x == nx - 1 ? kSlotXN : 0u);
         slotw[slot] = (w & 0x7FFFFu) | (uint32_t)((c - c0) * 32 + b) << kSlotRelShift | fx;
         wrap |= (x == 0 ? 1u : 0u) | (x == nx - 1 ? 2u : 0u);
@@ -318,9 +319,9 @@ __global__ void k_units(const ChunkEnt* __restrict__ ctab, const uint32_t* __res
           mm &= mm - 1;
           if (udesc) udesc[r] = (uint16_t)(n | (j << 5));
           ++r;
-          ++nl;
         }
       }
+      nl += wl;
       ++n;
     }
   }

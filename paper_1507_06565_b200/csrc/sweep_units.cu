@@ -51,9 +51,6 @@
 namespace pgpu {
 namespace {
 
-#ifndef PGPU_UNITS_LCAP
-#define PGPU_UNITS_LCAP 160
-#endif
 #ifndef PGPU_UNITS_MINB
 #define PGPU_UNITS_MINB 4
 #endif
@@ -64,7 +61,7 @@ namespace {
 #define PGPU_STCS 1
 #endif
 constexpr int kUW = 4;                   // warps per block (independent)
-constexpr int kULCap = PGPU_UNITS_LCAP;  // links per unit closed cooperatively from the pool
+constexpr int kULCap = kUnitLinkCap;     // a unit holds at most this many link records (kparams.h)
 
 __device__ __forceinline__ uint32_t usmem(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -123,17 +120,6 @@ __device__ __forceinline__ bool uwrap(int& v, int n, int periodic) {
   if (!periodic) return false;
   v = v < 0 ? v + n : v - n;
   return true;
-}
-
-__device__ __forceinline__ int uscan_excl(int n, int lane, int* total) {
-  int v = n;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += t;
-  }
-  *total = __shfl_sync(0xffffffffu, v, 31);
-  return v - n;
 }
 
 // Chunk entries of a unit: ent[3 * r + k] = source row r, chunk c0 + k;
@@ -352,7 +338,6 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
     const UMeta<RECORDS>& M = S.meta[i % 3];
     const int n = R.info & 63;
     const bool fluid = lane < n;
-    const uint32_t sw = fluid ? M.sw[lane] : 0u;
     const uint32_t fc = R.s0 + lane;
     if (RECORDS) {
       const int nl = (int)(R.info >> 20);
@@ -382,20 +367,6 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
           }
           if (r0 == r0) *s0 = isinf(r0) ? DSUB(gk0, p.mw[k0]) : DADD(DSUB(DMUL(r0, pk0), DMUL(r0, g0)), gk0);
           if (r1 == r1) *s1 = isinf(r1) ? DSUB(gk1, p.mw[k1]) : DADD(DSUB(DMUL(r1, pk1), DMUL(r1, g1)), gk1);
-        }
-        if (nl > kULCap) {  // pool overflow: each lane closes the rest of its own links
-          int tot;
-          const int off = uscan_excl(__popc(sw & kBounceMask), lane, &tot);
-          uint32_t mm = sw & kBounceMask;
-          int k = 0;
-          while (mm) {
-            const int j = __ffs(mm) - 1;
-            mm &= mm - 1;
-            if (off + k >= kULCap)
-              uclose_link(stage, lane, j, __ldg(p.links + R.lbase + off + k),
-                          __ldg(src + (uint32_t)(fc + p.poff[j])), p);
-            ++k;
-          }
         }
         __syncwarp();
       }

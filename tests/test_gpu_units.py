@@ -4,8 +4,8 @@ against the oracle in math mode EXACT (reference arithmetic) and against the
 chunk sweep (k_sweep_cpipe) in math mode FAST, on the corner cases of its
 addressing -- rows whose last chunk is partial (nx = 160, 36, 20), units that
 hold both x faces, x-periodic wrap pulls, a fully periodic box, wall planes
-whose units overflow the link pool (5 links per cell), CLI beds (units spanning
-three chunks), a moving lid (+inf records), the GLBM collision, and several
+whose units fill the link pool (5 links per cell; cells next to a wall and a
+sphere end units early), CLI beds (units spanning three chunks), a moving lid (+inf records), the GLBM collision, and several
 units-per-warp settings (pipeline lengths 1, 2, 3 and longer)."""
 import numpy as np
 import pytest
@@ -86,8 +86,7 @@ def test_units_exact_vs_oracle(gpu, orc, monkeypatch, case, scheme):
 
 def test_units_wall_planes_overflow_pool(gpu, orc, monkeypatch):
     """An all-fluid walled channel: every cell of the planes next to the walls
-    has 5 links, 160 per unit -- more than the pool holds, so the overflow
-    closes from global memory."""
+    has 5 links, 160 per full unit -- exactly the link pool (kUnitLinkCap)."""
     geom = gpu.make_box_geometry((128, 8, 12), (True, True, False), True, True)
     for scheme in (0, 1):
         p = _params(gpu)
