@@ -60,7 +60,10 @@ namespace {
 #ifndef PGPU_STCS
 #define PGPU_STCS 1
 #endif
-constexpr int kUW = 4;                   // warps per block (independent)
+#ifndef PGPU_UNITS_WARPS
+#define PGPU_UNITS_WARPS 4
+#endif
+constexpr int kUW = PGPU_UNITS_WARPS;    // warps per block (independent)
 constexpr int kULCap = kUnitLinkCap;     // a unit holds at most this many link records (kparams.h)
 
 __device__ __forceinline__ uint32_t usmem(const void* p) {

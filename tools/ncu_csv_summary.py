@@ -26,6 +26,8 @@ RUNS = {
     "c2_fast": ("C2_bed_128x64x128_sbb", "fast", 834673, 4 * 64 * 128),
     "c3_fast": ("C3_bed_128x64x128_cli", "fast", 834673, 4 * 64 * 128),
     "c5_fast": ("C5_glbm_256x16x512", "fast", 2088960, 8 * 16 * 512),
+    # the chunk sweep on the headline workload, for comparison (not written to the traffic JSON)
+    "c4_cli_fast_cpipe": (None, "fast", 51785984, 16 * 256 * 512),
 }
 GROUP = {"DADD": "fp64", "DMUL": "fp64", "DFMA": "fp64", "DSETP": "fp64",
          "LDGSTS": "LDGSTS", "LDG": "LDG", "STG": "STG", "LDS": "LDS", "STS": "STS",
@@ -99,11 +101,15 @@ def main():
         out.append(f"| {name} | `{k}` | {t_ms:.4f} | {rd:.4f} + {wr:.4f} GB | {(rd + wr) / alg:.3f} |"
                    f" {dram_gbs:.0f} ({100 * dram_gbs / PEAK:.1f} %) | {alg_gbs:.0f} = **{alg_gbs / PEAK:.3f}** |"
                    f" {warps:.0f} % | {regs} | {st} |")
-        traffic[f"{wl}|{math}"] = {
+        if "k_sweep_units" in kname:  # warps sweep units (<= 32 fluid slots): 4 warps x 4 units per block
+            wplanes = int(get("launch__grid_size")[0]) * 16
+        per = "unit" if "k_sweep_units" in kname else "warp-plane"
+        if wl is not None:
+          traffic[f"{wl}|{math}"] = {
             "kernel": k, "kernel_hash": khash, "dram_bytes_per_launch": (rd + wr) * 1e9,
             "dram_read_bytes": rd * 1e9, "dram_write_bytes": wr * 1e9, "duration_ms_ncu": t_ms,
             "algorithmic_bytes_per_launch": 304 * fluid,
-            "source": f"profiles/{pre}_ncu_summary.md (ncu --set full, 1 launch, {name})"}
+            "source": f"profiles/{pre}_ncu_summary.md (ncu --set full, 1 launch, {name})"}  # noqa: E126
         sp = d / f"{pre}_{name}.sass.csv"
         if sp.exists():
             warp, thr = sass(sp)
@@ -112,11 +118,11 @@ def main():
             for op, v in thr.items():
                 grp[GROUP.get(op, "integer/control/other")] += v
             top = sorted(warp.items(), key=lambda kv: -kv[1])[:12]
-            hist.append(f"**{name}** — {tw / wplanes:.0f} warp instructions per warp-plane; thread "
+            hist.append(f"**{name}** — {tw / wplanes:.0f} warp instructions per {per}; thread "
                         "instructions per fluid cell by group: " +
                         ", ".join(f"{g} {v / fluid:.1f}" for g, v in
                                   sorted(grp.items(), key=lambda kv: -kv[1])) +
-                        "  \n  top opcodes (warp instr / warp-plane): " +
+                        f"  \n  top opcodes (warp instr / {per}): " +
                         ", ".join(f"{op} {v / wplanes:.1f}" for op, v in top) + "\n")
     print("\n".join(out))
     print("\n### SASS instruction histograms (executed, from the source page)\n")
