@@ -77,6 +77,7 @@ class ClockSampler:
         self.dev = device_index
         self.proc = None
         self.lines = []
+        self.first = 0
 
     def start(self):
         try:
@@ -93,14 +94,25 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark(self):
+        """Call right before the timed region: waits for nvidia-smi's first
+        sample (its start-up takes longer than a short timed region) and
+        drops everything sampled before the region."""
+        if not self.proc:
+            return
+        t_end = time.time() + 3.0
+        while not self.lines and time.time() < t_end:
+            time.sleep(0.01)
+        self.first = len(self.lines)
+
     def stop(self):
         if not self.proc:
             return None
         late = False
-        if not self.lines:  # timed region shorter than nvidia-smi's first sample
+        if len(self.lines) <= self.first:  # timed region shorter than one sampling period
             late = True
             t_end = time.time() + 3.0
-            while not self.lines and time.time() < t_end:
+            while len(self.lines) <= self.first and time.time() < t_end:
                 time.sleep(0.02)
         self.proc.terminate()
         try:
@@ -110,7 +122,7 @@ class ClockSampler:
         self.thread.join(timeout=2)
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[self.first:]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -317,6 +329,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
+    clocks.mark()
     with torch.cuda.stream(stream):
         ev0.record(stream)
         stepper(args.steps)
