@@ -16,6 +16,9 @@ struct SweepConfig {
   // visit the z-blocks in descending order: consecutive sweeps alternate, so
   // each starts on the planes the previous one wrote last (still in L2)
   bool zrev = false;
+  // the sweep reads buffer 1 (every second sweep of a run): the units sweep
+  // alternates its block order on it
+  bool odd = false;
 };
 
 // Dense layout (kernels.cu) or, when p.ctab is set, the fluid-only layout

@@ -422,6 +422,7 @@ struct pgpu_sim {
     set_ghost_ptrs();
     SweepConfig c = sweep_cfg(0, part);
     c.zrev = zrev_on && !c.records && cur == 1;
+    c.odd = zrev_on && cur == 1;
     launch_sweep(c, kp, f[cur], f[1 - cur], stream);
     check_launch();
     ++launches;
@@ -448,6 +449,7 @@ struct pgpu_sim {
     for (int i = 0; i < kGraphSteps; ++i) {
       SweepConfig sc = sweep_cfg(0, 0);
       sc.zrev = zrev_on && !sc.records && c == 1;
+      sc.odd = zrev_on && c == 1;
       launch_sweep(sc, kp, f[c], f[1 - c], cs);
       c = 1 - c;
     }

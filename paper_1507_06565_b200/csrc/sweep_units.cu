@@ -171,7 +171,15 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
   // contiguous stretch of memory, and the sectors two units share hit L1.
   // (A dynamic schedule -- one resident wave of warps drawing units from a
   // global counter -- measured the same or worse on C2/C3 and was removed.)
-  const int64_t blk = rev ? (int64_t)gridDim.x - 1 - blockIdx.x : (int64_t)blockIdx.x;
+  // block order (the hardware dispatches blockIdx.x ascending): 0 ascending in
+  // z, 1 descending (consecutive SBB sweeps alternate: each starts on the
+  // planes the last one wrote, still in L2), 2 two-ended (even blocks from the
+  // bottom, odd blocks from the top: link-heavy bed units and free-flow units
+  // are in flight together instead of one after the other)
+  // 3: two-ended outward (mode 2 backwards: from the middle to both ends).
+  int64_t blk = blockIdx.x;
+  if (rev == 1 || rev == 3) blk = (int64_t)gridDim.x - 1 - blk;
+  if (rev >= 2) blk = (blk & 1) ? (int64_t)gridDim.x - 1 - (blk >> 1) : (blk >> 1);
   const int stride = group * kUW;
   // first unit of the block and its pipeline length: block-uniform by
   // construction (blockIdx and kernel parameters only), so the compiler keeps
@@ -425,6 +433,16 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
     return !(e && e[0] == '0');
   }();
   const int upw = units_upw(p);
+  // Block order, alternating between consecutive sweeps so that each starts on
+  // the planes the last one wrote (still in L2).  States far above L2 (C4):
+  // ascending / descending.  Smaller ones (C2, C3; KParams::stream_stores is
+  // that size test): two-ended inward / outward -- the link-heavy bed units
+  // and the free-flow units are then in flight together instead of one after
+  // the other (C3 0.68 -> 0.72; on C4 the two fronts cost 2 %).
+  // PGPU_UORDER=ab (two digits: even / odd sweeps) overrides, for experiments.
+  const char* oe = std::getenv("PGPU_UORDER");
+  int order = p.stream_stores ? (cfg.odd ? 1 : 0) : (cfg.odd ? 3 : 2);
+  if (oe && oe[0] && oe[1]) order = (cfg.odd ? oe[1] : oe[0]) - '0';
   const char* ge = std::getenv("PGPU_UGROUP");
   const int group = std::max(1, ge ? std::atoi(ge) : 1);
   const int64_t per_group = (int64_t)group * kUW * upw;
@@ -439,7 +457,7 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
   lc.attrs = at;
   lc.numAttrs = pdl_env && !cfg.slab ? 1 : 0;
   return cudaLaunchKernelEx(&lc, k_sweep_units<CM, GLBM, RECORDS>, p, src, dst, upw, group,
-                            cfg.zrev ? 1 : 0) == cudaSuccess;
+                            order) == cudaSuccess;
 }
 
 template <int CM>
