@@ -256,8 +256,9 @@ int pgpu_set_math_mode(pgpu_sim* sim, int32_t mode);
 enum pgpu_layout { PGPU_LAYOUT_DENSE = 0, PGPU_LAYOUT_FLUID_ONLY = 1, PGPU_LAYOUT_DENSE_PERSISTENT = 2 };
 int pgpu_get_layout(pgpu_sim* sim, int32_t* layout);
 /* K1 kernel of the fluid-only layout (no reference analogue,
- * results are bit-identical): AUTO (the library's choice), CPIPE (per-thread
- * asynchronous copies, k_sweep_cpipe), TMA (warp-specialised bulk-copy
+ * results are bit-identical): AUTO (the library's choice: UNITS wherever it
+ * applies), CPIPE (per-thread asynchronous copies over 32-cell chunks,
+ * k_sweep_cpipe), TMA (warp-specialised bulk-copy
  * pipeline, k_sweep_tma) or UNITS (k_sweep_units: warps sweep runs of 32
  * consecutive fluid slots, so no lane idles on a solid cell).
  * PGPU_SWEEP=cpipe|tma|units sets the default at creation. */
