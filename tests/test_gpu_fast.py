@@ -282,8 +282,8 @@ def run_config_fast(pg, name):
 def test_fast_config_within_tolerance(gpu, name, layout):
     if layout == "dense" and name in ("C2", "C3"):
         pytest.skip("default layout of the bed configs is fluid-only (dense covered by C1/C5)")
-    if layout == "compact" and name in ("C1", "C5"):
-        pytest.skip("default layout of the channels is dense")
+    if layout == "compact" and name == "C1":
+        pytest.skip("C1 is L2-resident: the persistent dense sweep (C5 runs in both layouts)")
     print(name, run_config_fast(gpu, name))
 
 

@@ -26,6 +26,7 @@ RUNS = {
     "c2_fast": ("C2_bed_128x64x128_sbb", "fast", 834673, 4 * 64 * 128),
     "c3_fast": ("C3_bed_128x64x128_cli", "fast", 834673, 4 * 64 * 128),
     "c5_fast": ("C5_glbm_256x16x512", "fast", 2088960, 8 * 16 * 512),
+    "c5_fast_dense": (None, "fast", 2088960, 8 * 16 * 512),
     # the chunk sweep on the headline workload, for comparison (not written to the traffic JSON)
     "c4_cli_fast_cpipe": (None, "fast", 51785984, 16 * 256 * 512),
 }
