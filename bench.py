@@ -629,7 +629,7 @@ def main():
     ap.add_argument("--scheme", default=None, choices=["SBB", "CLI"],
                     help="override the config's wall scheme (experiments only)")
     ap.add_argument("--math", default="fast", choices=["fast", "exact"],
-                    help="pgpu_math_mode: fast = FMA-contracted collision + folded CLI links "
+                    help="pgpu_math_mode: fast = FMA-contracted collision "
                          "(<= 1e-12 vs the reference, tests/test_gpu_fast.py); exact = "
                          "bit-identical to the reference")
     ap.add_argument("--cpu-budget", type=float, default=15.0,

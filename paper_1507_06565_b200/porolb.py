@@ -68,7 +68,7 @@ class WallScheme(enum.IntEnum):
 
 class MathMode(enum.IntEnum):
     """pgpu_math_mode (include/porolb_gpu.h): EXACT is bit-identical to the
-    reference; FAST is FMA-contracted with folded CLI links (<= 1e-12)."""
+    reference; FAST is the FMA-contracted collision (<= 1e-12 vs the reference)."""
     EXACT = 0
     FAST = 1
 
