@@ -136,6 +136,10 @@ struct KParams {
   const uint32_t* slotw;   // per fluid slot
   const uint16_t* udesc;   // per link record: owner lane in its unit | j << 5
   int64_t nunits;
+  // x-slab split with 32-column edge bands: the units of the two bands (the
+  // edge part); `units` then covers the interior columns
+  const UnitRec* units_edge;
+  int64_t nunits_edge;
   uint32_t* tickets;  // TMA sweep: [0] next work item, [1] finished blocks (zero between launches)
   int32_t stream_stores;  // sweeps store the new state evict-first (domains far larger than L2)
   FastCoef fc;

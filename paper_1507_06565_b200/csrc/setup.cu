@@ -268,8 +268,8 @@ __global__ void k_linkdesc(const uint32_t* __restrict__ cellw, const int32_t* __
 template <bool FILL>
 __global__ void k_units(const ChunkEnt* __restrict__ ctab, const uint32_t* __restrict__ cellw,
                         const int32_t* __restrict__ cellbase, int nx, int ny, int64_t rows,
-                        int nchunk, int xlo, int xhi, const int32_t* __restrict__ ubase,
-                        int32_t* __restrict__ cnt,
+                        int nchunk, int xlo, int xhi, bool outside,
+                        const int32_t* __restrict__ ubase, int32_t* __restrict__ cnt,
                         UnitRec* __restrict__ units, uint32_t* __restrict__ slotw,
                         uint16_t* __restrict__ udesc) {
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -287,15 +287,18 @@ __global__ void k_units(const ChunkEnt* __restrict__ ctab, const uint32_t* __res
   };
   for (int c = 0; c < nchunk; ++c) {
     const ChunkEnt e = ctab[row * nchunk + c];
-    uint32_t m = e.mask;
-    // cells of [xlo, xhi) only (slab split: the edge bands are swept separately)
+    // cells of [xlo, xhi) only, or the cells outside it (slab split: interior
+    // columns and edge bands are swept by separate launches)
+    uint32_t rm = 0xffffffffu;
     const int lo = xlo - 32 * c, hi = xhi - 32 * c;
-    if (lo > 0) m &= lo >= 32 ? 0u : ~((1u << lo) - 1u);
-    if (hi < 32) m &= hi <= 0 ? 0u : ((1u << hi) - 1u);
+    if (lo > 0) rm &= lo >= 32 ? 0u : ~((1u << lo) - 1u);
+    if (hi < 32) rm &= hi <= 0 ? 0u : ((1u << hi) - 1u);
+    uint32_t m = e.mask & (outside ? ~rm : rm);
     while (m) {
       const int b = __ffs(m) - 1;
       m &= m - 1;
       const uint32_t slot = e.rank + __popc(e.mask & ((1u << b) - 1u));
+      if (n && slot != s0 + (uint32_t)n) close();  // a unit is a run of consecutive slots
       const int x = c * 32 + b;
       const int64_t cell = row * nx + x;
       const uint32_t w = cellw[cell];
@@ -435,15 +438,15 @@ int64_t build_ctab(const uint32_t* cellw, int nx, int64_t rows, int nchunk, Chun
 }
 
 int64_t build_units(const ChunkEnt* ctab, const uint32_t* cellw, const int32_t* cellbase, int nx,
-                    int ny, int64_t rows, int nchunk, int xlo, int xhi, UnitRec** units_out,
-                    uint32_t* slotw, uint16_t* udesc, cudaStream_t s) {
+                    int ny, int64_t rows, int nchunk, int xlo, int xhi, bool outside,
+                    UnitRec** units_out, uint32_t* slotw, uint16_t* udesc, cudaStream_t s) {
   int32_t *cnt = nullptr, *ubase = nullptr;
   void* tmp = nullptr;
   size_t tb = 0;
   ck(cudaMalloc(&cnt, sizeof(int32_t) * rows), "units alloc");
   ck(cudaMalloc(&ubase, sizeof(int32_t) * rows), "units alloc");
   k_units<false><<<blocks(rows, 128), 128, 0, s>>>(ctab, cellw, cellbase, nx, ny, rows, nchunk,
-                                                    xlo, xhi, nullptr, cnt, nullptr, nullptr, nullptr);
+                                                    xlo, xhi, outside, nullptr, cnt, nullptr, nullptr, nullptr);
   ck(cudaGetLastError(), "k_units count");
   ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, ubase, rows, s), "units scan size");
   ck(cudaMalloc(&tmp, tb), "units alloc");
@@ -457,7 +460,7 @@ int64_t build_units(const ChunkEnt* ctab, const uint32_t* cellw, const int32_t* 
   ck(cudaMalloc(&units, sizeof(UnitRec) * (nunits + 4)), "units alloc");
   ck(cudaMemsetAsync(units, 0, sizeof(UnitRec) * (nunits + 4), s), "units clear");
   k_units<true><<<blocks(rows, 128), 128, 0, s>>>(ctab, cellw, cellbase, nx, ny, rows, nchunk,
-                                                   xlo, xhi, ubase, nullptr, units, slotw, udesc);
+                                                   xlo, xhi, outside, ubase, nullptr, units, slotw, udesc);
   ck(cudaGetLastError(), "k_units fill");
   ck(cudaStreamSynchronize(s), "units sync");
   cudaFree(cnt);

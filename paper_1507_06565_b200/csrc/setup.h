@@ -67,11 +67,12 @@ void build_linkdesc(const uint32_t* cellw, const int32_t* cellbase, int nx, int6
                     uint16_t* desc, cudaStream_t s);
 // Units of the units sweep (kparams.h UnitRec) with their per-slot words and
 // per-record descriptors (udesc may be null: no links) over the cells with x in
-// [xlo, xhi) (slab split: the interior columns); *units_out is cudaMalloc'ed
-// here (+ 4 zero records).  Returns the unit count.
+// [xlo, xhi) (slab split: the interior columns) or, with `outside`, over the
+// other cells (the two edge bands); *units_out is cudaMalloc'ed here (+ 4 zero
+// records).  Returns the unit count.
 int64_t build_units(const ChunkEnt* ctab, const uint32_t* cellw, const int32_t* cellbase, int nx,
-                    int ny, int64_t rows, int nchunk, int xlo, int xhi, UnitRec** units_out,
-                    uint32_t* slotw, uint16_t* udesc, cudaStream_t s);
+                    int ny, int64_t rows, int nchunk, int xlo, int xhi, bool outside,
+                    UnitRec** units_out, uint32_t* slotw, uint16_t* udesc, cudaStream_t s);
 void unpack_flags(const uint32_t* cellw, uint8_t* out, int64_t cells, cudaStream_t s);
 
 }  // namespace pgpu

@@ -105,6 +105,8 @@ struct pgpu_sim {
   unsigned long long* d_vmax = nullptr;
   double* d_sums = nullptr;
   UnitRec* d_units = nullptr;     // units sweep (built when it is selected)
+  UnitRec* d_units_edge = nullptr;  // slab split: units of the edge bands
+  int64_t n_units_edge = 0;
   uint32_t* d_slotw = nullptr;
   uint16_t* d_udesc = nullptr;
   int64_t n_units = 0;
@@ -150,6 +152,7 @@ struct pgpu_sim {
     cudaFree(d_vmax);
     cudaFree(d_sums);
     cudaFree(d_units);
+    cudaFree(d_units_edge);
     cudaFree(d_slotw);
     cudaFree(d_udesc);
     cudaFree(d_tickets);
@@ -319,7 +322,13 @@ struct pgpu_sim {
     }
     const int eb = slab ? sweep_edge_band(nx) : 0;  // slab split: interior columns only
     n_units = build_units(d_ctab, d_cellw, d_cellbase, nx, ny, (int64_t)ny * nz, kp.nchunk, eb, nx - eb,
-                          &d_units, d_slotw, d_udesc, stream);
+                          false, &d_units, d_slotw, d_udesc, stream);
+    if (slab && eb == 32 && nx % 32 == 0) {  // whole-chunk edge bands: the edge part on units too
+      n_units_edge = build_units(d_ctab, d_cellw, d_cellbase, nx, ny, (int64_t)ny * nz, kp.nchunk, eb,
+                                 nx - eb, true, &d_units_edge, d_slotw, d_udesc, stream);
+      kp.units_edge = d_units_edge;
+      kp.nunits_edge = n_units_edge;
+    }
     kp.units = d_units;
     kp.slotw = d_slotw;
     kp.udesc = d_udesc;
@@ -368,6 +377,7 @@ struct pgpu_sim {
     if (d_recs_fold) b += n_links * (int64_t)sizeof(LinkRec);
     if (d_linkdesc) b += (n_links + 16) * (int64_t)sizeof(uint16_t);
     if (d_units) b += (n_units + 4) * (int64_t)sizeof(UnitRec) + (kp.ks + 32) * (int64_t)sizeof(uint32_t);
+    if (d_units_edge) b += (n_units_edge + 4) * (int64_t)sizeof(UnitRec);
     if (d_udesc) b += (n_links + 16) * (int64_t)sizeof(uint16_t);
     if (d_planes) b += nz * (int64_t)sizeof(PlaneCoef);
     if (d_scratch) b += scratch_n * (int64_t)sizeof(double);

@@ -34,10 +34,11 @@
 // The arithmetic per cell is the sweep_compact.cu one (collide<CM, GLBM>, the
 // link closures in the reference order), so the results are bit-identical to
 // k_sweep_cpipe in EXACT and FAST (tests/test_gpu_units.py).  It sweeps the
-// whole domain or, in the x-slab split, the interior columns (the units are
-// then built over those columns only; interior cells read no ghosts and fill
-// no send buffers); the slab edge bands, KP and folded links stay on
-// k_sweep_cpipe (same state layout, so the kernels mix freely).
+// whole domain or, in the x-slab split, the interior columns and the two
+// 32-column edge bands in separate launches over their own unit lists (the
+// EDGE instantiation reads ghost columns and fills the send buffers); KP,
+// folded links and the face columns of slabs narrower than 96 stay on
+// sweep_compact.cu's kernels (same state layout, so the kernels mix freely).
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstddef>
@@ -157,10 +158,15 @@ __device__ __forceinline__ void uclose_link(double* stage, int owner, int j, dou
   }  // NaN: simple bounce-back, slot j already holds g_k(x)
 }
 
-template <int CM, bool GLBM, bool RECORDS>
+// EDGE: the launch sweeps the edge bands of an x-slab (units_edge): cells in
+// the face columns pull their e_x = +-1 sources from the ghost columns and
+// store their 5 outgoing populations into the send buffers (write_sends of
+// sweep_compact.cu); everything else is the same kernel.
+template <int CM, bool GLBM, bool RECORDS, bool EDGE>
 __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
-    k_sweep_units(const KParams p, const double* __restrict__ src, double* __restrict__ dst, int upw,
-                  int group, int rev) {
+    k_sweep_units(const KParams p, const UnitRec* __restrict__ units, int64_t nunits,
+                  const double* __restrict__ src, double* __restrict__ dst, int upw, int group,
+                  int rev) {
   extern __shared__ __align__(16) unsigned char usmem_raw[];
   updl_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -187,8 +193,8 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
   // the last block's warps 1..3 may run one unit past the end: the unit array
   // ends with zero records (n = 0: nothing to load, collide or store).
   const int64_t first = (blk / group) * ((int64_t)stride * upw) + (blk % group) * kUW;
-  const int nu = (int)min((int64_t)upw, (p.nunits - first + stride - 1) / stride);
-  const UnitRec* const U = p.units + first + warp;
+  const int nu = (int)min((int64_t)upw, (nunits - first + stride - 1) / stride);
+  const UnitRec* const U = units + first + warp;
   // the chunk entry this lane loads for every unit: lanes 0..26 source row
   // lane / 3, chunk c0 + lane % 3; lanes 27..31 the x = nx-1 partner of rows 0..4
   const int er = lane < 27 ? lane / 3 : lane - 27;
@@ -221,14 +227,14 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
         ok = ok && c < p.nchunk;
       } else {
         c = p.nchunk - 1;
-        ok = ok && (R.info & 64u);
+        ok = ok && !EDGE && (R.info & 64u);
       }
       if (ok)
         ucpa8(&M.ent[lane], row + c);
       else
         M.ent[lane] = ChunkEnt{0u, 0u};
     }
-    if ((R.info & 128u) && lane < 5) {  // warp-uniform: the unit holds x = nx-1 (pulls from x = 0)
+    if (!EDGE && (R.info & 128u) && lane < 5) {  // warp-uniform: the unit holds x = nx-1 (pulls from x = 0)
       int ys = y - urt_ey(lane), zs = z - urt_ez(lane);
       const bool oky = uwrap(ys, p.ny, p.py), okz = uwrap(zs, p.nz, p.pz);
       if (oky && okz)
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
         qp[r] = q[r] - 1;
         qn[r] = q[r] + (int)((bits >> r) & 1u);
       }
-      if (R.info & 64u) {  // warp-uniform: the unit holds x = 0
+      if (!EDGE && (R.info & 64u)) {  // warp-uniform: the unit holds x = 0
         const bool me = sw & kSlotX0;
 #pragma unroll
         for (int r = 0; r < 5; ++r) {
@@ -288,12 +294,25 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
           if (me) qp[r] = v;
         }
       }
-      if (R.info & 128u) {  // ... x = nx-1
+      if (!EDGE && (R.info & 128u)) {  // ... x = nx-1
         const bool me = sw & kSlotXN;
 #pragma unroll
         for (int r = 0; r < 5; ++r) {
           const int v = (int)M.ent[32 + r].rank;
           if (me) qn[r] = v;
+        }
+      }
+      // slab edge bands: ghost-column element of the source row per row 0..4
+      int64_t hrow[5];
+      const bool face = EDGE && (sw & (kSlotX0 | kSlotXN));
+      if (EDGE && (R.info & 192u)) {  // warp-uniform: the unit holds a face column
+        const int y = R.yz & 0xFFFF, z = R.yz >> 16;
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+          int ys = y - urow_ey(r), zs = z - urow_ez(r);
+          uwrap(ys, p.ny, p.py);  // rows off a non-periodic axis carry bounce bits: unused
+          uwrap(zs, p.nz, p.pz);
+          hrow[r] = (int64_t)zs * p.ny + ys;
         }
       }
 #pragma unroll
@@ -307,8 +326,15 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
           const int r = urow_of(j);
           idx = (EX[j] == 0 ? q[r] : (EX[j] == 1 ? qp[r] : qn[r])) + p.poff[j];
         }
-        ubounds(idx < 19ull * p.ks);
-        ucpa8(st + j * 32, src + idx);
+        const double* a = src + idx;
+        if (EDGE && EX[j] != 0 && face && !((sw >> j) & 1u)) {
+          const int64_t hp = (int64_t)p.ny * p.nz;
+          if (EX[j] == 1 && (sw & kSlotX0)) a = p.ghost_lo + halo_slot(j) * hp + hrow[urow_of(j)];
+          if (EX[j] == -1 && (sw & kSlotXN)) a = p.ghost_hi + halo_slot(j) * hp + hrow[urow_of(j)];
+        } else {
+          ubounds(idx < 19ull * p.ks);
+        }
+        ucpa8(st + j * 32, a);
       }
     }
     if (RECORDS) {
@@ -405,6 +431,27 @@ __global__ void __launch_bounds__(kUW * 32, PGPU_UNITS_MINB)
 #pragma unroll
         for (int j = 0; j < 19; ++j) d0[p.poff[j]] = f[j];
       }
+      if (EDGE) {  // the 5 populations leaving through each face (sweep_compact.cu write_sends)
+        const uint32_t sw = M.sw[lane];
+        if (sw & (kSlotX0 | kSlotXN)) {
+          const int64_t hp = (int64_t)p.ny * p.nz;
+          const int64_t h = (int64_t)(R.yz >> 16) * p.ny + (R.yz & 0xFFFF);
+          if (sw & kSlotX0) {
+            p.send_lo[0 * hp + h] = f[2];
+            p.send_lo[1 * hp + h] = f[8];
+            p.send_lo[2 * hp + h] = f[10];
+            p.send_lo[3 * hp + h] = f[12];
+            p.send_lo[4 * hp + h] = f[14];
+          }
+          if (sw & kSlotXN) {
+            p.send_hi[0 * hp + h] = f[1];
+            p.send_hi[1 * hp + h] = f[7];
+            p.send_hi[2 * hp + h] = f[9];
+            p.send_hi[3 * hp + h] = f[11];
+            p.send_hi[4 * hp + h] = f[13];
+          }
+        }
+      }
     }
   }
   uwait_all();
@@ -418,12 +465,14 @@ int units_upw(const KParams& p) {
   return 4;  // measured on C2/C3/C4 (tools/gpu_units_ab.sh): shorter runs pay the prologue, longer lose balance
 }
 
-template <int CM, bool GLBM, bool RECORDS>
+template <int CM, bool GLBM, bool RECORDS, bool EDGE>
 bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
                   cudaStream_t s) {
+  const UnitRec* const units = EDGE ? p.units_edge : p.units;
+  const int64_t nunits = EDGE ? p.nunits_edge : p.nunits;
   constexpr int smem = (int)sizeof(UWarp<RECORDS>) * kUW;
   static bool attr = [] {
-    cudaFuncSetAttribute(k_sweep_units<CM, GLBM, RECORDS>,
+    cudaFuncSetAttribute(k_sweep_units<CM, GLBM, RECORDS, EDGE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
@@ -447,7 +496,7 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
   const int group = std::max(1, ge ? std::atoi(ge) : 1);
   const int64_t per_group = (int64_t)group * kUW * upw;
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)((p.nunits + per_group - 1) / per_group * group));
+  lc.gridDim = dim3((unsigned)((nunits + per_group - 1) / per_group * group));
   lc.blockDim = dim3(kUW * 32);
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
@@ -456,18 +505,24 @@ bool units_launch(const SweepConfig& cfg, const KParams& p, const double* src, d
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = pdl_env && !cfg.slab ? 1 : 0;
-  return cudaLaunchKernelEx(&lc, k_sweep_units<CM, GLBM, RECORDS>, p, src, dst, upw, group,
-                            order) == cudaSuccess;
+  return cudaLaunchKernelEx(&lc, k_sweep_units<CM, GLBM, RECORDS, EDGE>, p, units, nunits, src, dst,
+                            upw, group, order) == cudaSuccess;
 }
 
+template <int CM, bool EDGE>
+bool units_cm_e(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
+                cudaStream_t s) {
+  if (cfg.glbm)
+    return cfg.records ? units_launch<CM, true, true, EDGE>(cfg, p, src, dst, s)
+                       : units_launch<CM, true, false, EDGE>(cfg, p, src, dst, s);
+  return cfg.records ? units_launch<CM, false, true, EDGE>(cfg, p, src, dst, s)
+                     : units_launch<CM, false, false, EDGE>(cfg, p, src, dst, s);
+}
 template <int CM>
 bool units_cm(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
               cudaStream_t s) {
-  if (cfg.glbm)
-    return cfg.records ? units_launch<CM, true, true>(cfg, p, src, dst, s)
-                       : units_launch<CM, true, false>(cfg, p, src, dst, s);
-  return cfg.records ? units_launch<CM, false, true>(cfg, p, src, dst, s)
-                     : units_launch<CM, false, false>(cfg, p, src, dst, s);
+  return cfg.part == PART_EDGES ? units_cm_e<CM, true>(cfg, p, src, dst, s)
+                                : units_cm_e<CM, false>(cfg, p, src, dst, s);
 }
 
 }  // namespace
@@ -475,9 +530,11 @@ bool units_cm(const SweepConfig& cfg, const KParams& p, const double* src, doubl
 int sweep_edge_band(int nx) { return edge_band(nx); }
 
 bool units_sweep_supported(const SweepConfig& cfg, const KParams& p) {
-  // slab split: the units cover the interior columns (sim_impl.h ensure_units)
+  // slab split: `units` covers the interior columns, `units_edge` the two
+  // 32-column edge bands when the slab has them (sim_impl.h ensure_units)
+  const bool edges = cfg.slab && cfg.part == PART_EDGES && p.units_edge && p.nunits_edge > 0;
   return p.ctab && p.units && p.slotw && p.nunits > 0 &&
-         cfg.part == (cfg.slab ? PART_INTERIOR : PART_ALL) && cfg.op == OP_STREAM_COLLIDE && collide_mode(p) != CM_FAST_FOLD &&
+         (edges || cfg.part == (cfg.slab ? PART_INTERIOR : PART_ALL)) && cfg.op == OP_STREAM_COLLIDE && collide_mode(p) != CM_FAST_FOLD &&
          (p.udesc || !cfg.records) && p.nchunk <= 4096 && p.ny <= 65535 && p.nz <= 65535;
 }
 
