@@ -35,9 +35,10 @@ bool launch_sweep_tma(const SweepConfig& cfg, const KParams& p, const double* sr
                       cudaStream_t s);
 // K1 of the fluid-only layout by units of 32 consecutive fluid slots
 // (sweep_units.cu): stream+collide of the whole domain or, in the x-slab
-// split, of the interior columns (the units then cover those columns only:
-// [sweep_edge_band(nx), nx - sweep_edge_band(nx))); no folded links; needs
-// KParams::units / slotw (/ udesc with records).
+// split, of the interior columns [sweep_edge_band(nx), nx - sweep_edge_band(nx))
+// (KParams::units then covers those columns only) and of the 32-column edge
+// bands (KParams::units_edge); no folded links; needs KParams::units / slotw
+// (/ udesc with records).
 int sweep_edge_band(int nx);
 bool units_sweep_supported(const SweepConfig& cfg, const KParams& p);
 bool launch_sweep_units(const SweepConfig& cfg, const KParams& p, const double* src, double* dst,
